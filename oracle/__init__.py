@@ -1,0 +1,271 @@
+"""CPU oracle for the NMT output-layer hot path of arXiv 1805.09863 (Amun).
+
+TEST INFRASTRUCTURE ONLY. Nothing in the product path (the package
+`paper_1805_09863_b200`, its C-ABI library or kernels) may import, call or
+link anything here. Only `tests/`, `__graft_entry__.smoke()` and bench.py's
+`cpu_baseline` / `--impl reference` legs use it.
+
+What it computes is an exact definition: the top-k over a sentence's
+beam x vocab candidates of `prev_cost + log softmax(W x + b)`, plus the
+stable compaction of finished hypotheses. It follows the paper's four steps
+(§2.2 list) SEPARATELY and naively, in the structure of
+Algorithm 3: GEMM, then AddBias, then the 3-pass Softmax (max,
+sum, normalise), then a k-best search done as a full sort. Arithmetic is
+fp64 on the exact (up-cast) values the GPU reads; bf16 inputs are widened
+exactly. A library primitive serves as a step where noted (numpy matmul for
+step 1, numpy lexsort for the sort); there is no blocking, fusion or
+reordering beyond the definition.
+
+Readings of the paper (listed in DESIGN.md):
+  G1/G2 the online sum uses exp(Delta), not "Delta x sum"
+        -- only relevant to `online_stats`, which follows Alg. 4 literally.
+  G3    ties go to the lower index (strict '>' in ascending scans, P:174,
+        P:210): within a row lower v; across a sentence lower row r.
+  G4/G5 k-best across the beam: per sentence, the top-k_s of
+        cost = prev_cost[r] + log p[r][v] over its rows r and all v
+        (P:29); larger cost is better.
+  G6    optional per-sentence k_s <= k (shrinking beam); default k.
+  G8    compaction is stable.
+  G11   fewer valid candidates than k -> pad with (idx=-1, cost=-inf).
+
+Every function's pins (what fixes it independently of itself) are listed in
+tests/test_oracle.py; none of the functions below is "parity unpinned".
+"""
+from __future__ import annotations
+
+import numpy as np
+
+__all__ = [
+    "as_f64", "gemm", "add_bias", "softmax_3pass_stats", "log_softmax",
+    "find_best", "kbest_sentences", "output_layer", "shard_partial",
+    "combine_partials", "online_stats", "argmax_1best", "argmax_1best_parallel",
+    "compact", "decode_work",
+]
+
+
+def as_f64(t) -> np.ndarray:
+    """Exact widening of an fp32 / bf16 torch tensor or numpy array to fp64."""
+    try:
+        import torch
+        if isinstance(t, torch.Tensor):
+            t = t.detach().cpu()
+            if t.dtype == torch.bfloat16:
+                t = t.to(torch.float32)  # exact: bf16 is a prefix of fp32
+            return t.to(torch.float64).numpy()
+    except ImportError:  # pragma: no cover
+        pass
+    return np.asarray(t, dtype=np.float64)
+
+
+# ---------------------------------------------------------------- step 1 + 2
+def gemm(X: np.ndarray, W: np.ndarray) -> np.ndarray:
+    """Step 1, p = w x: L[r][v] = sum_h X[r][h] * W[v][h], fp64.
+    X is [N, H] (one decoder state per row), W is [V, H]. numpy's matmul is
+    the library primitive for this step."""
+    return np.asarray(X, np.float64) @ np.asarray(W, np.float64).T
+
+
+def add_bias(L: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """Step 2, AddBias (Alg. 3): p_i <- p_i + b_i."""
+    return L + np.asarray(b, np.float64)[None, :]
+
+
+# ---------------------------------------------------------------- step 3
+def softmax_3pass_stats(L: np.ndarray):
+    """The first two passes of Alg. 3 Softmax: max over the row,
+    then sum of exp(p_i - max). Returns (m[N], z[N])."""
+    m = L.max(axis=1)                            # pass 1: "calculate max"
+    z = np.exp(L - m[:, None]).sum(axis=1)       # pass 2: "calculate denominator"
+    return m, z
+
+
+def log_softmax(L: np.ndarray) -> np.ndarray:
+    """Third pass of Alg. 3 in log form:
+    log p_i = (p_i - max) - log(sum)."""
+    m, z = softmax_3pass_stats(L)
+    return L - (m + np.log(z))[:, None]
+
+
+def find_best(p: np.ndarray):
+    """Alg. 3 Find-Best on one vector: strict '>' in ascending i,
+    so the lowest index wins ties. Returns (max, best)."""
+    best, mx = -1, -np.inf
+    for i, x in enumerate(np.asarray(p, np.float64)):
+        if x > mx:
+            mx, best = x, i
+    return mx, best
+
+
+# ---------------------------------------------------------------- step 4
+def kbest_sentences(logp: np.ndarray, prev_cost, beam_offsets, k: int,
+                    k_per_sentence=None, V_total: int | None = None,
+                    v_offset: int = 0):
+    """Step 4 generalised to beam search ("k-best search is a
+    simple extension"; reading G5): for sentence s with rows
+    r in [o_s, o_{s+1}), every candidate (r, v) scores
+        cost = prev_cost[r] + logp[r][v];
+    all candidates are FULLY sorted by (cost desc, r asc, v asc) and the first
+    k_s are emitted as idx = r * V_total + (v_offset + v), cost rounded to fp32.
+
+    Returns (idx int64 [S, k], cost float32 [S, k], cost64 float64 [S, k],
+    next_cost float64 [S]) where next_cost is the (k_s+1)-th cost (-inf if
+    none) so a comparator can detect near-ties. Slots >= k_s or beyond the
+    available candidates are padded with (-1, -inf) (reading G11)."""
+    N, V = logp.shape
+    V_total = V if V_total is None else V_total
+    o = np.asarray(beam_offsets, np.int64)
+    S = len(o) - 1
+    pc = np.asarray(prev_cost, np.float64)
+    idx = np.full((S, k), -1, np.int64)
+    cost32 = np.full((S, k), -np.inf, np.float32)
+    cost64 = np.full((S, k), -np.inf, np.float64)
+    nxt = np.full(S, -np.inf, np.float64)
+    for s in range(S):
+        ks = k if k_per_sentence is None else int(k_per_sentence[s])
+        r0, r1 = int(o[s]), int(o[s + 1])
+        if r1 <= r0 or ks <= 0:
+            continue
+        rows = np.arange(r0, r1)
+        c = (pc[r0:r1, None] + logp[r0:r1, :]).reshape(-1)
+        rr = np.repeat(rows, V)
+        vv = np.tile(np.arange(V), r1 - r0)
+        order = np.lexsort((vv, rr, -c))           # primary key: -cost
+        take = order[:ks]
+        n = len(take)
+        idx[s, :n] = rr[take] * V_total + v_offset + vv[take]
+        cost64[s, :n] = c[take]
+        cost32[s, :n] = c[take].astype(np.float32)
+        if len(order) > ks:
+            nxt[s] = c[order[ks]]
+    return idx, cost32, cost64, nxt
+
+
+def output_layer(X, W, b, prev_cost, beam_offsets, k, k_per_sentence=None):
+    """The whole path on one GPU's worth of vocabulary: steps 1-4 run
+    separately (the unfused baseline structure of Alg. 3)."""
+    L = add_bias(gemm(X, W), b)
+    logp = log_softmax(L)
+    return kbest_sentences(logp, prev_cost, beam_offsets, k, k_per_sentence)
+
+
+# ------------------------------------------------- shards (Alg. 6 generalised)
+def shard_partial(L_shard: np.ndarray, k: int, v_offset: int = 0):
+    """Per-row state of one vocabulary shard p^j (Alg. 6, with the
+    max/sum of Alg. 3 and a k-best instead of a 1-best): m = max_v L,
+    s = sum_v exp(L - m), and the k largest biased logits by (l desc, v asc)
+    found by a full sort. Returns (m[N], s[N], l[N,k], v[N,k]); missing
+    entries are (-inf, -1)."""
+    N, V = L_shard.shape
+    m, s = softmax_3pass_stats(L_shard) if V > 0 else (np.full(N, -np.inf), np.zeros(N))
+    l = np.full((N, k), -np.inf)
+    v = np.full((N, k), -1, np.int64)
+    for r in range(N):
+        order = np.lexsort((np.arange(V), -L_shard[r]))[:k]
+        l[r, :len(order)] = L_shard[r, order]
+        v[r, :len(order)] = v_offset + order
+    return m, s, l, v
+
+
+def combine_partials(parts, k: int):
+    """The reduce step of Alg. 6 for (max, sum, k-best) states,
+    taken over shards in the given order: M = max_j m_j,
+    S = sum_j s_j * exp(m_j - M) (the rescale of P:195-197), and the k best
+    (l desc, v asc) of the union. Returns (M, S, l, v) like shard_partial."""
+    ms = np.stack([p[0] for p in parts])              # [G, N]
+    ss = np.stack([p[1] for p in parts])
+    M = ms.max(axis=0)
+    with np.errstate(invalid="ignore"):
+        w = np.where(np.isfinite(ms), np.exp(ms - M[None, :]), 0.0)
+    S = (ss * w).sum(axis=0)
+    L = np.concatenate([p[2] for p in parts], axis=1)  # [N, G*k]
+    Vv = np.concatenate([p[3] for p in parts], axis=1)
+    N = L.shape[0]
+    l = np.full((N, k), -np.inf)
+    v = np.full((N, k), -1, np.int64)
+    for r in range(N):
+        ok = Vv[r] >= 0
+        lr, vr = L[r][ok], Vv[r][ok]
+        order = np.lexsort((vr, -lr))[:k]
+        l[r, :len(order)] = lr[order]
+        v[r, :len(order)] = vr[order]
+    return M, S, l, v
+
+
+def online_stats(p, b=None):
+    """Alg. 4 Fused-Kernel on one vector, literally, with the
+    rescale written as exp(Delta) per the derivation P:193-200 (reading G1):
+    on a strictly larger p', sum <- exp(max - p') * sum + 1, max <- p',
+    best <- i; otherwise sum <- sum + exp(p' - max). Returns
+    (1/sum, best, max, sum). Used to pin the monoid algebra, not the path."""
+    p = np.asarray(p, np.float64)
+    b = np.zeros_like(p) if b is None else np.asarray(b, np.float64)
+    mx, sm, best = -np.inf, 0.0, -1
+    for i in range(len(p)):
+        x = p[i] + b[i]
+        if x > mx:
+            delta = mx - x
+            sm = np.exp(delta) * sm + 1.0
+            mx, best = x, i
+        else:
+            sm = sm + np.exp(x - mx)
+    return 1.0 / sm, best, mx, sm
+
+
+def argmax_1best(p, b):
+    """Alg. 5: argmax of p + b without any exp; lowest index on ties."""
+    return find_best(np.asarray(p, np.float64) + np.asarray(b, np.float64))[1]
+
+
+def argmax_1best_parallel(p, b, shards: int):
+    """Alg. 6: contiguous near-equal shards, per-shard (max, best),
+    then a serial reduce with strict '>' in shard order."""
+    x = np.asarray(p, np.float64) + np.asarray(b, np.float64)
+    bounds = np.linspace(0, len(x), shards + 1).round().astype(int)
+    mx, best = -np.inf, -1
+    for j in range(shards):
+        mj, bj = find_best(x[bounds[j]:bounds[j + 1]])
+        if bj >= 0 and mj > mx:
+            mx, best = mj, bounds[j] + bj
+    return best
+
+
+# ---------------------------------------------------------------- Alg. 2
+def compact(columns, alive, beam_offsets):
+    """Alg. 2 "Remove h from b", stable (reading G8):
+        j = 0; for r: if alive[r]: copy row r of every column to row j;
+                                   src_row[j] = r; j += 1
+    new_offsets[s] = number of alive rows with r < o_s; a sentence survives
+    iff it keeps at least one row. `columns` is a list of 2-D uint8 arrays
+    [N, row_bytes]. Returns (new_columns [N', row_bytes], new_offsets[S+1],
+    src_row[N'], N', S_alive)."""
+    alive = [bool(a) for a in np.asarray(alive).reshape(-1)]
+    N = len(alive)
+    src_row = []
+    for r in range(N):
+        if alive[r]:
+            src_row.append(r)
+    new_cols = [np.asarray(c)[src_row] if len(src_row) else np.asarray(c)[:0]
+                for c in columns]
+    o = [int(x) for x in np.asarray(beam_offsets).reshape(-1)]
+    new_off = []
+    for s in range(len(o)):
+        cnt = 0
+        for r in range(o[s]):
+            cnt += alive[r]
+        new_off.append(cnt)
+    S_alive = sum(1 for s in range(len(o) - 1) if new_off[s + 1] > new_off[s])
+    return (new_cols, np.array(new_off, np.int32), np.array(src_row, np.int32),
+            len(src_row), S_alive)
+
+
+def decode_work(finish_steps, beam: int, mode: str) -> int:
+    """Hypothesis-decodes of Alg. 1 (naive, read per G7 as "until
+    every hypothesis has finished") vs Alg. 2 (dynamic).
+    finish_steps[i][j] = number of steps hypothesis j of sentence i is decoded
+    (it emits EOS at that step). Naive decodes all S*beam slots for max steps;
+    dynamic decodes each hypothesis only while it is alive."""
+    f = [list(x) if hasattr(x, "__len__") else [x] * beam for x in finish_steps]
+    if mode == "naive":
+        T = max(max(x) for x in f)
+        return T * sum(len(x) for x in f)
+    return sum(sum(x) for x in f)
