@@ -1,0 +1,347 @@
+"""Benchmark of the NMT output-layer hot path (arXiv 1805.09863) on B200.
+
+Metric (BASELINE.json): hypothesis-rows/s through GEMM + softmax + k-best at
+V = 90k; % of roofline. One step = one pass of the whole path over one batch:
+fused GEMM/bias/softmax-stats/row-k-best kernel + merge/select kernel
+(amun_output_layer) on the 'beam' config (H=1024, V=90000, 128 x 5, k=5).
+
+N=1: one GPU, the whole vocabulary. N>1 (torchrun, one rank per GPU, NCCL):
+vocab-sharded — rank g owns V/N rows of W; each step = partial kernel +
+all_gather_into_tensor of the per-row partial records + merge on every rank
+(strong scaling: the batch is fixed).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "hypothesis-rows/sec through GEMM+softmax+k-best at V=90k"
+UNIT = "rows/s"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
+                "bf16_tflops_sustained": d.get("bf16_tflops_sustained"), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------- oracle arm
+def oracle_sample(w: synth.Workload, X, W, b, pc, n_sent: int):
+    """The oracle, as it stands, on the first n_sent sentences (all V)."""
+    import oracle as O
+    rows = n_sent * w.B
+    Xs = O.as_f64(X[:rows])
+    Wd = O.as_f64(W)
+    bd = O.as_f64(b)
+    pcs = O.as_f64(pc[:rows])
+    off = np.arange(n_sent + 1) * w.B
+    t0 = time.perf_counter()
+    L = O.add_bias(O.gemm(Xs, Wd), bd)
+    logp = O.log_softmax(L)
+    res = O.kbest_sentences(logp, pcs, off, w.k)
+    dt = time.perf_counter() - t0
+    return dt, rows, res, logp, pcs
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        n = [d.get("num_threads", 1) for d in info if d.get("user_api") == "blas"]
+        return max(n) if n else 1
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, w):
+    """--impl reference: the oracle timed on host cores, bounded sample/step."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    torch.manual_seed(0)
+    X, W, b, pc = synth.gen_X(w), synth.gen_W(w), synth.gen_b(w), synth.gen_prev_cost(w)
+    n_sent = int(os.environ.get("AMUN_REF_SENTENCES", "4"))
+    for _ in range(args.warmup):
+        oracle_sample(w, X, W, b, pc, n_sent)
+    times, rows = [], 0
+    for _ in range(args.steps):
+        dt, r, *_ = oracle_sample(w, X, W, b, pc, n_sent)
+        times.append(dt)
+        rows += r
+    total = sum(times)
+    v = rows / total
+    cores = blas_threads()
+    sample = f"first {n_sent} sentences ({n_sent * w.B} rows) x full V={w.V} per step"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": config_of(w, args),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def config_of(w, args):
+    return {"workload": f"{w.name}: H={w.H}, V={w.V}, {w.S} sentences x beam {w.B}, k={w.k}",
+            "H": w.H, "V": w.V, "sentences": w.S, "beam": w.B, "k": w.k, "rows": w.N,
+            "global_batch": w.N, "parallelism": f"vocab{args.gpus}" if args.gpus > 1 else "none",
+            "l2": "W rotated over 2 resident copies (2 x 184 MB > 126 MB L2) between steps",
+            "seed": w.seed, "dist": w.dist}
+
+
+# ---------------------------------------------------------------------- our arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="beam", choices=list(synth.CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    w = synth.CONFIGS[args.workload]
+
+    if args.impl == "reference":
+        return run_reference(args, w)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_1805_09863_b200 as amun
+    from paper_1805_09863_b200 import sharded
+
+    # inputs: generated on the host by the seeded generator (bit-identical to
+    # what the oracle reads), then made resident in HBM
+    X_h, pc_h, off_h = synth.gen_X(w), synth.gen_prev_cost(w), synth.gen_offsets(w)
+    v0, v1 = sharded.shard_range(w.V, world, rank)
+    W_h, b_h = synth.gen_W(w, v0, v1 - v0), synth.gen_b(w, v0, v1 - v0)
+    X, pc, off = X_h.to(dev), pc_h.to(dev), off_h.to(dev)
+    Ws = [W_h.to(dev)]
+    Ws.append(Ws[0].clone())            # 2 copies: W never served from L2 across steps
+    b = b_h.to(dev)
+    layer = sharded.ShardedOutputLayer(w.H, w.V, world, rank, dtype=w.dtype, k_max=w.k,
+                                       max_rows=w.N, max_sentences=w.S, device=dev)
+
+    def step(i, with_events=None):
+        Wc = Ws[i % 2]
+        return layer(X, Wc, b, pc, off, w.k, events=with_events)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+
+    # ---------------- device-timed region
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(K)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        start.record()
+        for i in range(K):
+            idx, cost = step(i, with_events=ev[i])
+        end.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    ms = start.elapsed_time(end)
+    kern_ms = [a.elapsed_time(c) for a, c in ev]
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / K
+    value = w.N / (ms_per_step * 1e-3)
+
+    # ---------------- end-to-end through the public API with host buffers
+    X_p = X_h.pin_memory()
+    pc_p = pc_h.pin_memory()
+    off_p = off_h.pin_memory()
+    idx_p = torch.empty((w.S, w.k), dtype=torch.int64).pin_memory()
+    cost_p = torch.empty((w.S, w.k), dtype=torch.float32).pin_memory()
+    Xd, pcd, offd = torch.empty_like(X), torch.empty_like(pc), torch.empty_like(off)
+
+    def e2e_step(i):
+        Xd.copy_(X_p, non_blocking=True)
+        pcd.copy_(pc_p, non_blocking=True)
+        offd.copy_(off_p, non_blocking=True)
+        ii, cc = layer(Xd, Ws[i % 2], b, pcd, offd, w.k)
+        idx_p.copy_(ii, non_blocking=True)
+        cost_p.copy_(cc, non_blocking=True)
+
+    for i in range(args.warmup):
+        e2e_step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s2.record()
+    for i in range(K):
+        e2e_step(i)
+    e2.record()
+    torch.cuda.synchronize()
+    e2e_ms = s2.elapsed_time(e2)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = w.N / (e2e_ms / K * 1e-3)
+    h2d = X_h.numel() * X_h.element_size() + pc_h.numel() * 4 + off_h.numel() * 4
+    d2h = w.S * w.k * (8 + 4)
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+
+    # ---------------- roofline of the dominant kernel (the fused GEMM kernel)
+    peaks = load_peaks()
+    Vl = v1 - v0
+    flops = 2.0 * w.N * w.H * Vl
+    kern_mean_ms = statistics.mean(kern_ms)
+    achieved = flops / (kern_mean_ms * 1e-3) / 1e12
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(w.name)
+        except Exception:
+            traffic = None
+    roof = {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"],
+            "unit": "TFLOP/s", "frac": achieved / peaks["bf16_tflops"], "traffic": traffic,
+            "kernel": "ol_tc_kernel (fused GEMM + bias + online softmax + row k-best)",
+            "kernel_ms_mean": kern_mean_ms, "kernel_share_of_step": kern_mean_ms / ms_per_step,
+            "peak_source": peaks["source"] + " bf16_tflops (burst)",
+            "frac_vs_sustained": (achieved / peaks["bf16_tflops_sustained"])
+            if peaks.get("bf16_tflops_sustained") else None,
+            "algorithmic": f"2*N*H*V_local = {flops:.4g} FLOP per launch"}
+
+    # ---------------- CPU baseline (oracle) + sampled parity, rank 0, N=1 only
+    cpu = None
+    parity = None
+    if world == 1 and not args.no_cpu_baseline:
+        n_sent = int(os.environ.get("AMUN_CPU_SENTENCES", "24"))
+        dt, rows, res, logp, pcs = oracle_sample(w, X_h, W_h, b_h, pc_h, n_sent)
+        cpu = {"value": rows / dt, "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
+               "sample": f"first {n_sent} sentences ({rows} rows) x full V={w.V}, one pass, "
+                         f"{dt:.1f} s"}
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        from tests.compare import compare_kbest
+        ii, cc = step(0)
+        torch.cuda.synchronize()
+        gi, gc = ii.cpu().numpy()[:n_sent], cc.cpu().numpy()[:n_sent]
+        oi, oc32, oc64, nxt = res
+        rep = compare_kbest(gi, gc, lambda s, r, v: pcs[r] + logp[r, v], oc64,
+                            np.full(n_sent, w.k), w.dtype, w.V, o_next=nxt)
+        parity = {"sentences": n_sent, **rep, "status": "pass"}
+
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": config_of(w, args),
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h,
+                "note": "X, prev_cost, beam_offsets pinned-host -> HBM and idx, cost HBM -> "
+                        "pinned-host inside the timed region every step; W, b resident"},
+        "gpu_launches": K * layer.launches_per_step,
+        "clocks": clk.summary(),
+        "parity": parity,
+        "gpu": torch.cuda.get_device_name(dev),
+    }
+    print(json.dumps(out))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,189 @@
+/*
+ * amun.h — C-ABI of the B200-native NMT output-layer hot path
+ * (arXiv 1805.09863, "Fast Neural Machine Translation Implementation",
+ *  Amun @ WNMT 2018). Library: paper_1805_09863_b200/libamun.so (sm_100a).
+ *
+ * The path (§2.2 list of the four output-layer steps):
+ *   1. p = W x   logits GEMM, tcgen05/TMEM
+ *   2. p = p + b   fused into the GEMM epilogue
+ *   3. softmax   online max / sum-of-exp
+ *                                             (Alg. 4, rescale
+ *                                             P:193-200 read with exp(Delta))
+ *   4. k-best                        ("k-best search is a simple
+ *                                             extension"), generalised to beam
+ *                                             search: per sentence, top-k_s over
+ *                                             beam x vocab of
+ *                                             cost = prev_cost[r] + log p[r][v]
+ *   + mini-batching (Alg. 2): remove finished hypotheses
+ *     ("Remove h from b") by stable compaction.
+ *
+ * Conventions (all entry points):
+ *   - Every pointer argument that names device memory is a CUDA device
+ *     pointer (cudaMalloc / torch CUDA storage) on the plan's device.
+ *     The CALLER owns all memory: inputs, outputs and workspace. The library
+ *     never allocates device memory and never synchronises the stream, except
+ *     amun_compact() when counts_host != NULL.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *     stream). Calls are stream-ordered and CUDA-graph capturable (except
+ *     amun_compact with counts_host).
+ *   - Layouts are row-major, C order. dtype AMUN_BF16 means IEEE bfloat16
+ *     storage (fp32 accumulation); AMUN_F32 means fp32 storage and true fp32
+ *     products (SIMT kernel).
+ *   - Errors: every call returns amun_status; no exception crosses the ABI.
+ *     The message of the last failure on the calling thread is returned by
+ *     amun_last_error(). Host-side validation happens before anything is
+ *     launched: on AMUN_EINVAL / AMUN_EUNSUPPORTED nothing was enqueued.
+ *     Inputs are assumed finite; non-finite inputs give
+ *     unspecified (but memory-safe) results.
+ *   - Ties (reading G3 of DESIGN.md, P:174/P:210/P:247 strict '>' scans):
+ *     equal biased logits in a row rank by lower token id; equal costs in a
+ *     sentence rank by lower row, then higher logit, then lower token id.
+ */
+#ifndef AMUN_H_
+#define AMUN_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AMUN_ABI_VERSION 1
+#define AMUN_MAX_K 16          /* largest k-best width per row / sentence */
+#define AMUN_MAX_COLUMNS 16    /* largest number of columns one amun_compact call moves */
+
+typedef enum amun_status {
+  AMUN_OK = 0,
+  AMUN_EINVAL = 1,        /* bad argument (shape, alignment, range, NULL) */
+  AMUN_EUNSUPPORTED = 2,  /* valid but not supported (device not sm_100, dtype) */
+  AMUN_ECUDA = 3          /* a CUDA runtime/driver call failed */
+} amun_status;
+
+typedef enum amun_dtype { AMUN_F32 = 0, AMUN_BF16 = 1 } amun_dtype;
+
+/* Opaque plan: shapes, kernel choice, persistent-grid schedule and cached TMA
+ * tensor maps. Not thread-safe: use one plan per host thread. */
+typedef struct amun_ol amun_ol;
+
+int         amun_abi_version(void);
+const char* amun_last_error(void);
+const char* amun_status_string(amun_status s);
+
+/* Create a plan for one vocabulary shard.
+ *   H         hidden size (K of the GEMM). bf16: H % 8 == 0; f32: H % 4 == 0
+ *             (TMA / vector alignment: a row is a multiple of 16 bytes).
+ *   V_local   rows of W (and entries of b) this plan owns, 1 <= V_local.
+ *   v_offset  global token id of local row 0 (vocab sharding; 0 on one GPU).
+ *   V_total   global vocabulary size; out_idx encodes r * V_total + token.
+ *             Requires v_offset + V_local <= V_total.
+ *   dtype     storage type of X and W.
+ *   k_max     largest k any later call uses, 1..AMUN_MAX_K. Partial records
+ *             hold k_max entries.
+ *   max_rows, max_sentences  capacity the workspace is sized for.
+ *   device    CUDA ordinal; must be compute capability 10.0 (B200, sm_100a).
+ * On success *plan is set; destroy with amun_ol_destroy. */
+amun_status amun_ol_create(amun_ol** plan, int H, int V_local, int v_offset, int V_total,
+                           amun_dtype dtype, int k_max, int max_rows, int max_sentences,
+                           int device);
+amun_status amun_ol_destroy(amun_ol* plan);
+
+/* Bytes of device workspace the caller must pass to the calls below
+ * (per-CTA partial states of the fused kernel). 256-byte aligned. */
+size_t amun_ol_workspace_bytes(const amun_ol* plan);
+
+/* Floats per row of a partial record: 2 + 2*k_max, laid out as
+ *   { m, s, l[0..k_max-1], v[0..k_max-1] }
+ * m = max biased logit of the covered vocabulary, s = sum exp(l - m) over it,
+ * l = the k_max largest biased logits (desc, ties -> lower v), v = their
+ * GLOBAL token ids stored as int32 bit patterns. Unused entries: (-inf, -1);
+ * a record covering no vocabulary has m = -inf, s = 0. */
+int amun_ol_partial_stride(const amun_ol* plan);
+
+/* Full single-GPU path: steps 1-4 (GEMM + bias + softmax + beam k-best).
+ *   X            [N, H] dtype; row r is the decoder state of hypothesis r.
+ *   W            [V_local, H] dtype (row v = output embedding of token
+ *                v_offset + v).
+ *   b            [V_local] fp32 bias (full precision).
+ *   prev_cost    [N] fp32 cumulative log-prob of each hypothesis.
+ *   beam_offsets [S+1] int32, o_0 = 0 <= o_1 <= ... <= o_S = N; sentence s
+ *                owns rows [o_s, o_{s+1}) (a sentence may be empty).
+ *   k_per_sentence  [S] int32 or NULL (then every sentence uses k);
+ *                0 <= k_s <= k (Amun-style shrinking beam, reading G6).
+ *   k            output width per sentence, 1 <= k <= k_max.
+ *   out_idx      [S, k] int64: r * V_total + token of the i-th best candidate
+ *                of sentence s (r = global row index), -1 padding.
+ *   out_cost     [S, k] fp32: prev_cost[r] + log p[r][token], -inf padding.
+ *                Each sentence's entries are sorted by cost, descending.
+ *   workspace    amun_ol_workspace_bytes(plan) bytes, 256-byte aligned.
+ * 0 <= N <= max_rows, 0 <= S <= max_sentences. X and W must be 16-byte
+ * aligned (TMA). Enqueues 2 kernels (fused GEMM/epilogue, then select). */
+amun_status amun_output_layer(amun_ol* plan, const void* X, const void* W, const float* b,
+                              const float* prev_cost, const int32_t* beam_offsets, int N, int S,
+                              const int32_t* k_per_sentence, int k, int64_t* out_idx,
+                              float* out_cost, void* workspace, void* stream);
+
+/* The two stages of amun_output_layer, exposed so a caller can time or
+ * overlap them: stage 1 writes per-(row, vocab split) partial records into
+ * `workspace`; stage 2 reads them (same N) and selects per sentence. */
+amun_status amun_ol_scores(amun_ol* plan, const void* X, const void* W, const float* b, int N,
+                           void* workspace, void* stream);
+amun_status amun_ol_select(amun_ol* plan, const void* workspace, const float* prev_cost,
+                           const int32_t* beam_offsets, int N, int S,
+                           const int32_t* k_per_sentence, int k, int64_t* out_idx,
+                           float* out_cost, void* stream);
+
+/* Vocab-sharded path, piece 1 (Alg. 6 shard step): the per-row
+ * partial record of THIS shard (all of its V_local tokens combined):
+ *   partial [N, amun_ol_partial_stride(plan)] fp32 (see layout above). */
+amun_status amun_output_layer_partial(amun_ol* plan, const void* X, const void* W,
+                                      const float* b, int N, float* partial, void* workspace,
+                                      void* stream);
+
+/* Vocab-sharded path, piece 2 (Alg. 6 reduce step): exact merge of
+ * G shards' partial records, combined in shard order g = 0..G-1, then the
+ * per-sentence selection of amun_output_layer.
+ *   partials [G, N, amun_ol_partial_stride(plan)] fp32 (e.g. the result of an
+ *            all-gather of every rank's amun_output_layer_partial output).
+ * Other arguments as amun_output_layer. Token ids are already global. */
+amun_status amun_merge_partials(amun_ol* plan, const float* partials, int G,
+                                const float* prev_cost, const int32_t* beam_offsets, int N, int S,
+                                const int32_t* k_per_sentence, int k, int64_t* out_idx,
+                                float* out_cost, void* stream);
+
+/* Test hook: steps 1-2 only. Writes the biased logits of the same tcgen05
+ * (bf16) or SIMT (f32) GEMM to logits [N, V_local] fp32 (these never reach
+ * HBM on the real path). For bit-exact GEMM checks in the integer regime. */
+amun_status amun_debug_logits(amun_ol* plan, const void* X, const void* W, const float* b, int N,
+                              float* logits, void* workspace, void* stream);
+
+/* Mini-batching (Alg. 2 "Remove h from b"): stable compaction.
+ * One column = one per-hypothesis state array of N rows of row_bytes bytes:
+ *   src  [N, row_bytes] device, dst [>= N', row_bytes] device (must not
+ *   overlap src). row_bytes % 4 == 0, src/dst 4-byte aligned (16-byte rows
+ *   and pointers take the vector path).
+ *   alive         [N] uint8, nonzero = hypothesis survives this step.
+ *   beam_offsets  [S+1] int32 of the input batch.
+ *   new_beam_offsets [S+1] int32 out: number of surviving rows before o_s.
+ *   src_row       [N] int32 out: src_row[j] = input row of output row j,
+ *                 for j < N' (entries >= N' are not written).
+ *   counts        [2] int32 device out: {N', S_alive} (S_alive = sentences
+ *                 that keep at least one row).
+ *   counts_host   optional host int32[2]; if non-NULL the call copies counts
+ *                 back and SYNCHRONISES the stream (not graph-capturable).
+ * 0 <= N, 0 <= S, n_cols <= AMUN_MAX_COLUMNS (n_cols may be 0: only the
+ * scan outputs are produced). One kernel launch. Bit-exact. */
+typedef struct amun_column {
+  const void* src;
+  void* dst;
+  int64_t row_bytes;
+} amun_column;
+
+amun_status amun_compact(const amun_column* cols, int n_cols, const uint8_t* alive, int N,
+                         const int32_t* beam_offsets, int S, int32_t* new_beam_offsets,
+                         int32_t* src_row, int32_t* counts, int32_t* counts_host, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AMUN_H_ */

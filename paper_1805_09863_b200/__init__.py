@@ -1,0 +1,204 @@
+"""B200-native NMT output-layer hot path (arXiv 1805.09863, Amun @ WNMT 2018).
+
+Thin Python binding over the C-ABI in include/amun.h (libamun.so). It only
+marshals arguments: tensors become device pointers, the stream is torch's
+current stream. Every step of the path runs in the library's sm_100a kernels;
+there is no CPU fallback (a missing library raises on import).
+
+    ol = OutputLayer(H, V, k_max=5, max_rows=640, max_sentences=128)
+    idx, cost = ol(X, W, b, prev_cost, beam_offsets, k=5)      # steps 1-4
+    n_alive, s_alive = compact([(src, dst), ...], alive, offsets, new_offsets, src_row)
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+from ._lib import AMUN_MAX_COLUMNS, AMUN_MAX_K, AmunError, check
+
+_L = _lib.load()
+
+__all__ = ["OutputLayer", "compact", "AmunError", "AMUN_MAX_K", "AMUN_MAX_COLUMNS", "lib_path"]
+
+lib_path = _lib.LIB_PATH
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(device):
+    return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+def _need(t, name, dtype, device, shape=None):
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if t.device != device:
+        raise ValueError(f"{name} is on {t.device}, expected {device}")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} has dtype {t.dtype}, expected {dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+
+
+class OutputLayer:
+    """Plan for one vocabulary shard [v_offset, v_offset + V_local) of V_total.
+
+    dtype "bf16": X, W bfloat16 (tcgen05 tensor cores, fp32 accumulate).
+    dtype "f32" : X, W float32 (SIMT, true fp32 products).
+    """
+
+    def __init__(self, H: int, V_local: int, *, v_offset: int = 0, V_total: int | None = None,
+                 dtype: str = "bf16", k_max: int = 16, max_rows: int = 1 << 16,
+                 max_sentences: int = 1 << 16, device: int | torch.device = 0):
+        dev = torch.device("cuda", device) if isinstance(device, int) else torch.device(device)
+        self.device = dev
+        self.H, self.V_local, self.v_offset = H, V_local, v_offset
+        self.V_total = V_local if V_total is None else V_total
+        self.dtype = dtype
+        self.tdtype = torch.bfloat16 if dtype == "bf16" else torch.float32
+        self.k_max, self.max_rows, self.max_sentences = k_max, max_rows, max_sentences
+        h = ctypes.c_void_p()
+        check(_L.amun_ol_create(ctypes.byref(h), H, V_local, v_offset, self.V_total,
+                                _lib.AMUN_BF16 if dtype == "bf16" else _lib.AMUN_F32,
+                                k_max, max_rows, max_sentences, dev.index or 0))
+        self._h = h
+        self.stride = _L.amun_ol_partial_stride(h)
+        nbytes = _L.amun_ol_workspace_bytes(h)
+        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            _L.amun_ol_destroy(h)
+            self._h = None
+
+    # ------------------------------------------------------------- checks
+    def _check_scores(self, X, W, b):
+        N = X.shape[0]
+        _need(X, "X", self.tdtype, self.device, (N, self.H))
+        _need(W, "W", self.tdtype, self.device, (self.V_local, self.H))
+        _need(b, "b", torch.float32, self.device, (self.V_local,))
+        return N
+
+    def _outputs(self, S, k, out_idx, out_cost):
+        if out_idx is None:
+            out_idx = torch.empty((S, k), dtype=torch.int64, device=self.device)
+        if out_cost is None:
+            out_cost = torch.empty((S, k), dtype=torch.float32, device=self.device)
+        _need(out_idx, "out_idx", torch.int64, self.device, (S, k))
+        _need(out_cost, "out_cost", torch.float32, self.device, (S, k))
+        return out_idx, out_cost
+
+    def _check_select(self, prev_cost, beam_offsets, N, k_per_sentence):
+        S = beam_offsets.shape[0] - 1
+        _need(prev_cost, "prev_cost", torch.float32, self.device, (N,))
+        _need(beam_offsets, "beam_offsets", torch.int32, self.device)
+        if k_per_sentence is not None:
+            _need(k_per_sentence, "k_per_sentence", torch.int32, self.device, (S,))
+        return S
+
+    # ------------------------------------------------------------- calls
+    def __call__(self, X, W, b, prev_cost, beam_offsets, k: int, k_per_sentence=None,
+                 out_idx=None, out_cost=None):
+        """Steps 1-4: returns (idx [S,k] int64 = row*V_total + token, cost [S,k] fp32)."""
+        N = self._check_scores(X, W, b)
+        S = self._check_select(prev_cost, beam_offsets, N, k_per_sentence)
+        out_idx, out_cost = self._outputs(S, k, out_idx, out_cost)
+        check(_L.amun_output_layer(self._h, _ptr(X), _ptr(W), _ptr(b), _ptr(prev_cost),
+                                   _ptr(beam_offsets), N, S, _ptr(k_per_sentence), k,
+                                   _ptr(out_idx), _ptr(out_cost), _ptr(self.workspace),
+                                   _stream(self.device)))
+        return out_idx, out_cost
+
+    def scores(self, X, W, b):
+        """Stage 1 only (fused GEMM + bias + online softmax stats + row k-best)."""
+        N = self._check_scores(X, W, b)
+        check(_L.amun_ol_scores(self._h, _ptr(X), _ptr(W), _ptr(b), N, _ptr(self.workspace),
+                                _stream(self.device)))
+
+    def select(self, N, prev_cost, beam_offsets, k: int, k_per_sentence=None, out_idx=None,
+               out_cost=None):
+        """Stage 2 only (merge + per-sentence selection) on the last scores()."""
+        S = self._check_select(prev_cost, beam_offsets, N, k_per_sentence)
+        out_idx, out_cost = self._outputs(S, k, out_idx, out_cost)
+        check(_L.amun_ol_select(self._h, _ptr(self.workspace), _ptr(prev_cost),
+                                _ptr(beam_offsets), N, S, _ptr(k_per_sentence), k,
+                                _ptr(out_idx), _ptr(out_cost), _stream(self.device)))
+        return out_idx, out_cost
+
+    def partial(self, X, W, b, out=None):
+        """Vocab-shard piece 1: per-row partial record [N, stride] fp32."""
+        N = self._check_scores(X, W, b)
+        if out is None:
+            out = torch.empty((N, self.stride), dtype=torch.float32, device=self.device)
+        _need(out, "partial", torch.float32, self.device, (N, self.stride))
+        check(_L.amun_output_layer_partial(self._h, _ptr(X), _ptr(W), _ptr(b), N, _ptr(out),
+                                           _ptr(self.workspace), _stream(self.device)))
+        return out
+
+    def merge(self, partials, prev_cost, beam_offsets, k: int, k_per_sentence=None,
+              out_idx=None, out_cost=None):
+        """Vocab-shard piece 2: partials [G, N, stride] -> (idx, cost)."""
+        if partials.dim() != 3 or partials.shape[2] != self.stride:
+            raise ValueError(f"partials must be [G, N, {self.stride}]")
+        G, N = partials.shape[0], partials.shape[1]
+        _need(partials, "partials", torch.float32, self.device)
+        S = self._check_select(prev_cost, beam_offsets, N, k_per_sentence)
+        out_idx, out_cost = self._outputs(S, k, out_idx, out_cost)
+        check(_L.amun_merge_partials(self._h, _ptr(partials), G, _ptr(prev_cost),
+                                     _ptr(beam_offsets), N, S, _ptr(k_per_sentence), k,
+                                     _ptr(out_idx), _ptr(out_cost), _stream(self.device)))
+        return out_idx, out_cost
+
+    def debug_logits(self, X, W, b):
+        """Test hook: the biased logits [N, V_local] of the same GEMM."""
+        N = self._check_scores(X, W, b)
+        out = torch.empty((N, self.V_local), dtype=torch.float32, device=self.device)
+        check(_L.amun_debug_logits(self._h, _ptr(X), _ptr(W), _ptr(b), N, _ptr(out),
+                                   _ptr(self.workspace), _stream(self.device)))
+        return out
+
+
+def compact(columns, alive, beam_offsets, new_offsets=None, src_row=None, counts=None,
+            sync: bool = True):
+    """Alg. 2 "Remove h from b": stable compaction of every (src, dst) column
+    pair (2-D tensors, row = hypothesis) by the uint8 `alive` mask.
+    Returns (N', S_alive, new_offsets, src_row, counts); with sync=False the
+    first two are None and the counts stay on the device (no host sync)."""
+    N = alive.shape[0]
+    dev = alive.device
+    S = beam_offsets.shape[0] - 1
+    _need(alive, "alive", torch.uint8, dev, (N,))
+    _need(beam_offsets, "beam_offsets", torch.int32, dev)
+    if new_offsets is None:
+        new_offsets = torch.empty(S + 1, dtype=torch.int32, device=dev)
+    if src_row is None:
+        src_row = torch.empty(max(N, 1), dtype=torch.int32, device=dev)
+    if counts is None:
+        counts = torch.empty(2, dtype=torch.int32, device=dev)
+    if len(columns) > AMUN_MAX_COLUMNS:
+        raise ValueError(f"at most {AMUN_MAX_COLUMNS} columns per call")
+    arr = (_lib.amun_column * max(1, len(columns)))()
+    for i, (src, dst) in enumerate(columns):
+        if src.shape[0] != N or not src.is_contiguous() or not dst.is_contiguous():
+            raise ValueError(f"column {i}: src must have N rows; src/dst contiguous")
+        rb = src.element_size()
+        for d in src.shape[1:]:
+            rb *= int(d)
+        if dst.numel() * dst.element_size() < rb * N:
+            raise ValueError(f"column {i}: dst too small")
+        arr[i] = _lib.amun_column(src.data_ptr(), dst.data_ptr(), rb)
+    host = (ctypes.c_int32 * 2)() if sync else None
+    check(_L.amun_compact(arr, len(columns), _ptr(alive), N, _ptr(beam_offsets), S,
+                          _ptr(new_offsets), _ptr(src_row), _ptr(counts),
+                          ctypes.cast(host, ctypes.c_void_p) if sync else None,
+                          _stream(dev)))
+    if sync:
+        return int(host[0]), int(host[1]), new_offsets, src_row, counts
+    return None, None, new_offsets, src_row, counts

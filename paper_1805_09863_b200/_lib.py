@@ -1,0 +1,78 @@
+"""ctypes loader for libamun.so (the C-ABI in include/amun.h).
+
+No fallback: if the library is missing or fails to load, importing the
+binding raises. Build it with `python -c "import __graft_entry__ as g; g.build()"`.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libamun.so")
+
+AMUN_OK, AMUN_EINVAL, AMUN_EUNSUPPORTED, AMUN_ECUDA = 0, 1, 2, 3
+AMUN_F32, AMUN_BF16 = 0, 1
+AMUN_MAX_K = 16
+AMUN_MAX_COLUMNS = 16
+
+EXPORTS = [
+    "amun_abi_version", "amun_last_error", "amun_status_string", "amun_ol_create",
+    "amun_ol_destroy", "amun_ol_workspace_bytes", "amun_ol_partial_stride",
+    "amun_output_layer", "amun_ol_scores", "amun_ol_select", "amun_output_layer_partial",
+    "amun_merge_partials", "amun_debug_logits", "amun_compact",
+]
+
+
+class amun_column(ctypes.Structure):
+    _fields_ = [("src", ctypes.c_void_p), ("dst", ctypes.c_void_p), ("row_bytes", ctypes.c_int64)]
+
+
+class AmunError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+_STATUS = {0: "AMUN_OK", 1: "AMUN_EINVAL", 2: "AMUN_EUNSUPPORTED", 3: "AMUN_ECUDA"}
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built; run __graft_entry__.build() (no CPU fallback exists)")
+    lib = ctypes.CDLL(LIB_PATH)
+    vp, i32, sz = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t
+    st = ctypes.c_int
+    sig = {
+        "amun_abi_version": (i32, []),
+        "amun_last_error": (ctypes.c_char_p, []),
+        "amun_status_string": (ctypes.c_char_p, [st]),
+        "amun_ol_create": (st, [ctypes.POINTER(vp), i32, i32, i32, i32, i32, i32, i32, i32, i32]),
+        "amun_ol_destroy": (st, [vp]),
+        "amun_ol_workspace_bytes": (sz, [vp]),
+        "amun_ol_partial_stride": (i32, [vp]),
+        "amun_output_layer": (st, [vp, vp, vp, vp, vp, vp, i32, i32, vp, i32, vp, vp, vp, vp]),
+        "amun_ol_scores": (st, [vp, vp, vp, vp, i32, vp, vp]),
+        "amun_ol_select": (st, [vp, vp, vp, vp, i32, i32, vp, i32, vp, vp, vp]),
+        "amun_output_layer_partial": (st, [vp, vp, vp, vp, i32, vp, vp, vp]),
+        "amun_merge_partials": (st, [vp, vp, i32, vp, vp, i32, i32, vp, i32, vp, vp, vp]),
+        "amun_debug_logits": (st, [vp, vp, vp, vp, i32, vp, vp, vp]),
+        "amun_compact": (st, [ctypes.POINTER(amun_column), i32, vp, i32, vp, i32, vp, vp, vp, vp, vp]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(status: int) -> None:
+    if status != AMUN_OK:
+        msg = load().amun_last_error().decode(errors="replace")
+        raise AmunError(status, msg)

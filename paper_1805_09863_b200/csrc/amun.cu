@@ -1,0 +1,495 @@
+// amun.cu — host side of the C-ABI declared in include/amun.h.
+// Validation, persistent-grid schedule, TMA tensor-map cache and launches.
+// No device memory is allocated here and no stream is synchronised (except
+// amun_compact with counts_host).
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+
+#include "../../include/amun.h"
+#include "compact.cuh"
+#include "merge.cuh"
+#include "ol_simt.cuh"
+#include "ol_tc.cuh"
+
+using namespace amun;
+
+namespace {
+
+thread_local std::string g_err;
+
+amun_status fail(amun_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+#define CUDA_TRY(expr)                                                                  \
+  do {                                                                                  \
+    cudaError_t e_ = (expr);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(AMUN_ECUDA, "%s failed: %s", #expr, cudaGetErrorString(e_));          \
+  } while (0)
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn get_encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+struct MapEntry {
+  const void* ptr = nullptr;
+  long long rows = -1;
+  CUtensorMap map;
+};
+
+inline int kbucket(int k) { return k <= 1 ? 1 : k <= 2 ? 2 : k <= 4 ? 4 : k <= 8 ? 8 : 16; }
+inline long long cdiv(long long a, long long b) { return (a + b - 1) / b; }
+
+}  // namespace
+
+struct amun_ol {
+  int H, V_local, v_offset, V_total, k_max, kb, max_rows, max_sentences, device, num_sms;
+  amun_dtype dtype;
+  int stride;
+  size_t ws_bytes;
+  MapEntry xmaps[4];
+  MapEntry wmaps[8];
+  int xnext = 0, wnext = 0;
+};
+
+namespace {
+
+// Tensor map of a row-major [rows, H] bf16 matrix, box [box_rows, 64],
+// 128-byte swizzle (matches sdesc_k_sw128), OOB rows/columns read as zero.
+amun_status encode_map(amun_ol* pl, const void* ptr, long long rows, int box_rows,
+                       CUtensorMap* out) {
+  EncodeTiledFn enc = get_encode_fn();
+  if (!enc) return fail(AMUN_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  cuuint64_t dims[2] = {(cuuint64_t)pl->H, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)pl->H * 2};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(AMUN_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return AMUN_OK;
+}
+
+amun_status get_map(amun_ol* pl, MapEntry* cache, int n, int& next, const void* ptr,
+                    long long rows, int box_rows, const CUtensorMap** out) {
+  for (int i = 0; i < n; ++i)
+    if (cache[i].ptr == ptr && cache[i].rows == rows) {
+      *out = &cache[i].map;
+      return AMUN_OK;
+    }
+  MapEntry& e = cache[next];
+  next = (next + 1) % n;
+  amun_status s = encode_map(pl, ptr, rows, box_rows, &e.map);
+  if (s != AMUN_OK) {
+    e.ptr = nullptr;
+    return s;
+  }
+  e.ptr = ptr;
+  e.rows = rows;
+  *out = &e.map;
+  return AMUN_OK;
+}
+
+Schedule make_schedule(const amun_ol* pl, int N, int* grid) {
+  Schedule s;
+  const long long n_mt = cdiv(N, 128);
+  s.Vp = cdiv(pl->V_local, 16) * 16;
+  s.total = n_mt * s.Vp;
+  s.C = cdiv(cdiv(s.total, pl->num_sms), 16) * 16;
+  if (s.C < 16) s.C = 16;
+  *grid = (int)cdiv(s.total, s.C);
+  return s;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+template <int KB>
+amun_status launch_tc(amun_ol* pl, const CUtensorMap* mx, const CUtensorMap* mw,
+                      const TcParams& tp, int grid, cudaStream_t st, int mode) {
+  void (*kern)(const CUtensorMap, const CUtensorMap, const TcParams) =
+      mode == 0 ? ol_tc_kernel<KB, 0> : ol_tc_kernel<1, 1>;
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM));
+  kern<<<grid, TC_THREADS, TC_SMEM, st>>>(*mx, *mw, tp);
+  CUDA_TRY(cudaGetLastError());
+  return AMUN_OK;
+}
+
+template <int KB>
+amun_status launch_simt(const SimtParams& sp, int grid, cudaStream_t st, int mode) {
+  if (mode == 0)
+    ol_simt_kernel<KB, 0><<<grid, 128, 0, st>>>(sp);
+  else
+    ol_simt_kernel<1, 1><<<grid, 128, 0, st>>>(sp);
+  CUDA_TRY(cudaGetLastError());
+  return AMUN_OK;
+}
+
+// Stage 1: fused GEMM + epilogue into the workspace slots (mode 0) or the
+// debug logits (mode 1).
+amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b, int N,
+                       void* workspace, float* logits, cudaStream_t st, int mode) {
+  if (N == 0) return AMUN_OK;
+  CUDA_TRY(cudaSetDevice(pl->device));
+  int grid;
+  Schedule sch = make_schedule(pl, N, &grid);
+  if (pl->dtype == AMUN_BF16) {
+    const CUtensorMap *mx, *mw;
+    amun_status s = get_map(pl, pl->xmaps, 4, pl->xnext, X, N, TC_BM, &mx);
+    if (s != AMUN_OK) return s;
+    s = get_map(pl, pl->wmaps, 8, pl->wnext, W, pl->V_local, TC_BN, &mw);
+    if (s != AMUN_OK) return s;
+    TcParams tp;
+    tp.N = N;
+    tp.V_local = pl->V_local;
+    tp.v_offset = pl->v_offset;
+    tp.n_kblk = (int)cdiv(pl->H, TC_BK);
+    tp.sch = sch;
+    tp.bias = b;
+    tp.part = static_cast<float*>(workspace);
+    tp.stride = pl->stride;
+    tp.k_max = pl->k_max;
+    tp.logits = logits;
+    switch (mode == 1 ? 1 : pl->kb) {
+      case 1: return launch_tc<1>(pl, mx, mw, tp, grid, st, mode);
+      case 2: return launch_tc<2>(pl, mx, mw, tp, grid, st, mode);
+      case 4: return launch_tc<4>(pl, mx, mw, tp, grid, st, mode);
+      case 8: return launch_tc<8>(pl, mx, mw, tp, grid, st, mode);
+      default: return launch_tc<16>(pl, mx, mw, tp, grid, st, mode);
+    }
+  } else {
+    SimtParams sp;
+    sp.N = N;
+    sp.V_local = pl->V_local;
+    sp.v_offset = pl->v_offset;
+    sp.H = pl->H;
+    sp.sch = sch;
+    sp.X = static_cast<const float*>(X);
+    sp.W = static_cast<const float*>(W);
+    sp.bias = b;
+    sp.part = static_cast<float*>(workspace);
+    sp.stride = pl->stride;
+    sp.k_max = pl->k_max;
+    sp.logits = logits;
+    switch (mode == 1 ? 1 : pl->kb) {
+      case 1: return launch_simt<1>(sp, grid, st, mode);
+      case 2: return launch_simt<2>(sp, grid, st, mode);
+      case 4: return launch_simt<4>(sp, grid, st, mode);
+      case 8: return launch_simt<8>(sp, grid, st, mode);
+      default: return launch_simt<16>(sp, grid, st, mode);
+    }
+  }
+}
+
+template <int KB>
+amun_status launch_merge(const MergeParams& mp, bool rows, int grid, cudaStream_t st) {
+  if (grid == 0) return AMUN_OK;
+  if (rows) {
+    merge_rows_kernel<KB><<<grid, 128, 0, st>>>(mp);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(128);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, merge_sentences_kernel<KB>, mp));
+  }
+  CUDA_TRY(cudaGetLastError());
+  return AMUN_OK;
+}
+
+amun_status run_merge(amun_ol* pl, const MergeParams& mp, bool rows, int grid, cudaStream_t st) {
+  switch (pl->kb) {
+    case 1: return launch_merge<1>(mp, rows, grid, st);
+    case 2: return launch_merge<2>(mp, rows, grid, st);
+    case 4: return launch_merge<4>(mp, rows, grid, st);
+    case 8: return launch_merge<8>(mp, rows, grid, st);
+    default: return launch_merge<16>(mp, rows, grid, st);
+  }
+}
+
+amun_status check_select_args(const amun_ol* pl, const float* prev_cost,
+                              const int32_t* beam_offsets, int N, int S, int k,
+                              const int64_t* out_idx, const float* out_cost) {
+  if (N < 0 || N > pl->max_rows) return fail(AMUN_EINVAL, "N=%d out of [0, max_rows=%d]", N, pl->max_rows);
+  if (S < 0 || S > pl->max_sentences)
+    return fail(AMUN_EINVAL, "S=%d out of [0, max_sentences=%d]", S, pl->max_sentences);
+  if (k < 1 || k > pl->k_max) return fail(AMUN_EINVAL, "k=%d out of [1, k_max=%d]", k, pl->k_max);
+  if (S > 0 && (!beam_offsets || !out_idx || !out_cost))
+    return fail(AMUN_EINVAL, "NULL beam_offsets/out_idx/out_cost");
+  if (N > 0 && !prev_cost) return fail(AMUN_EINVAL, "NULL prev_cost");
+  return AMUN_OK;
+}
+
+amun_status check_score_args(const amun_ol* pl, const void* X, const void* W, const float* b,
+                             int N, const void* workspace) {
+  if (!pl) return fail(AMUN_EINVAL, "NULL plan");
+  if (N < 0 || N > pl->max_rows) return fail(AMUN_EINVAL, "N=%d out of [0, max_rows=%d]", N, pl->max_rows);
+  if (N == 0) return AMUN_OK;
+  if (!X || !W || !b || !workspace) return fail(AMUN_EINVAL, "NULL X/W/b/workspace");
+  if (!aligned16(X) || !aligned16(W)) return fail(AMUN_EINVAL, "X and W must be 16-byte aligned");
+  if (!aligned16(b)) return fail(AMUN_EINVAL, "b must be 16-byte aligned");
+  if ((reinterpret_cast<uintptr_t>(workspace) & 255) != 0)
+    return fail(AMUN_EINVAL, "workspace must be 256-byte aligned");
+  return AMUN_OK;
+}
+
+MergeParams base_merge(const amun_ol* pl) {
+  MergeParams mp;
+  memset(&mp, 0, sizeof(mp));
+  mp.stride = pl->stride;
+  mp.k_max = pl->k_max;
+  mp.V_total = pl->V_total;
+  return mp;
+}
+
+}  // namespace
+
+extern "C" {
+
+int amun_abi_version(void) { return AMUN_ABI_VERSION; }
+
+const char* amun_last_error(void) { return g_err.c_str(); }
+
+const char* amun_status_string(amun_status s) {
+  switch (s) {
+    case AMUN_OK: return "AMUN_OK";
+    case AMUN_EINVAL: return "AMUN_EINVAL";
+    case AMUN_EUNSUPPORTED: return "AMUN_EUNSUPPORTED";
+    case AMUN_ECUDA: return "AMUN_ECUDA";
+  }
+  return "AMUN_UNKNOWN";
+}
+
+amun_status amun_ol_create(amun_ol** plan, int H, int V_local, int v_offset, int V_total,
+                           amun_dtype dtype, int k_max, int max_rows, int max_sentences,
+                           int device) {
+  if (!plan) return fail(AMUN_EINVAL, "NULL plan pointer");
+  *plan = nullptr;
+  if (dtype != AMUN_F32 && dtype != AMUN_BF16) return fail(AMUN_EINVAL, "unknown dtype %d", (int)dtype);
+  if (H < 1) return fail(AMUN_EINVAL, "H=%d must be >= 1", H);
+  if (dtype == AMUN_BF16 && H % 8 != 0) return fail(AMUN_EINVAL, "bf16 needs H %% 8 == 0 (H=%d)", H);
+  if (dtype == AMUN_F32 && H % 4 != 0) return fail(AMUN_EINVAL, "f32 needs H %% 4 == 0 (H=%d)", H);
+  if (V_local < 1) return fail(AMUN_EINVAL, "V_local=%d must be >= 1", V_local);
+  if (v_offset < 0 || V_total < 1 || (long long)v_offset + V_local > V_total)
+    return fail(AMUN_EINVAL, "need 0 <= v_offset and v_offset + V_local <= V_total");
+  if (k_max < 1 || k_max > AMUN_MAX_K) return fail(AMUN_EINVAL, "k_max=%d out of [1, %d]", k_max, AMUN_MAX_K);
+  if (max_rows < 0 || max_sentences < 0) return fail(AMUN_EINVAL, "negative capacity");
+  if ((long long)max_rows * V_total >= (1LL << 62)) return fail(AMUN_EINVAL, "max_rows * V_total overflows");
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(AMUN_EINVAL, "device %d out of range (%d devices)", device, ndev);
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10 || prop.minor != 0)
+    return fail(AMUN_EUNSUPPORTED, "device %d is sm_%d%d; this library is built for sm_100a (B200)",
+                device, prop.major, prop.minor);
+  amun_ol* pl = new (std::nothrow) amun_ol();
+  if (!pl) return fail(AMUN_EINVAL, "out of host memory");
+  pl->H = H;
+  pl->V_local = V_local;
+  pl->v_offset = v_offset;
+  pl->V_total = V_total;
+  pl->dtype = dtype;
+  pl->k_max = k_max;
+  pl->kb = kbucket(k_max);
+  pl->max_rows = max_rows;
+  pl->max_sentences = max_sentences;
+  pl->device = device;
+  pl->num_sms = prop.multiProcessorCount;
+  pl->stride = 2 + 2 * k_max;
+  const long long slots = pl->num_sms + cdiv(max_rows > 0 ? max_rows : 1, 128) + 1;
+  pl->ws_bytes = (size_t)cdiv(slots * 128LL * pl->stride * 4, 256) * 256;
+  *plan = pl;
+  return AMUN_OK;
+}
+
+amun_status amun_ol_destroy(amun_ol* plan) {
+  delete plan;
+  return AMUN_OK;
+}
+
+size_t amun_ol_workspace_bytes(const amun_ol* plan) { return plan ? plan->ws_bytes : 0; }
+
+int amun_ol_partial_stride(const amun_ol* plan) { return plan ? plan->stride : 0; }
+
+amun_status amun_ol_scores(amun_ol* plan, const void* X, const void* W, const float* b, int N,
+                           void* workspace, void* stream) {
+  amun_status s = check_score_args(plan, X, W, b, N, workspace);
+  if (s != AMUN_OK) return s;
+  return run_scores(plan, X, W, b, N, workspace, nullptr, static_cast<cudaStream_t>(stream), 0);
+}
+
+amun_status amun_ol_select(amun_ol* plan, const void* workspace, const float* prev_cost,
+                           const int32_t* beam_offsets, int N, int S,
+                           const int32_t* k_per_sentence, int k, int64_t* out_idx,
+                           float* out_cost, void* stream) {
+  if (!plan) return fail(AMUN_EINVAL, "NULL plan");
+  amun_status s = check_select_args(plan, prev_cost, beam_offsets, N, S, k, out_idx, out_cost);
+  if (s != AMUN_OK) return s;
+  if (N > 0 && !workspace) return fail(AMUN_EINVAL, "NULL workspace");
+  if (S == 0) return AMUN_OK;
+  CUDA_TRY(cudaSetDevice(plan->device));
+  MergeParams mp = base_merge(plan);
+  int grid_unused;
+  mp.part = static_cast<const float*>(workspace);
+  mp.layout = 0;
+  mp.sch = make_schedule(plan, N > 0 ? N : 1, &grid_unused);
+  mp.N = N;
+  mp.S = S;
+  mp.prev_cost = prev_cost;
+  mp.offsets = beam_offsets;
+  mp.k_s = k_per_sentence;
+  mp.k = k;
+  mp.out_idx = reinterpret_cast<long long*>(out_idx);
+  mp.out_cost = out_cost;
+  return run_merge(plan, mp, false, S, static_cast<cudaStream_t>(stream));
+}
+
+amun_status amun_output_layer(amun_ol* plan, const void* X, const void* W, const float* b,
+                              const float* prev_cost, const int32_t* beam_offsets, int N, int S,
+                              const int32_t* k_per_sentence, int k, int64_t* out_idx,
+                              float* out_cost, void* workspace, void* stream) {
+  amun_status s = check_score_args(plan, X, W, b, N, workspace);
+  if (s != AMUN_OK) return s;
+  s = check_select_args(plan, prev_cost, beam_offsets, N, S, k, out_idx, out_cost);
+  if (s != AMUN_OK) return s;
+  s = amun_ol_scores(plan, X, W, b, N, workspace, stream);
+  if (s != AMUN_OK) return s;
+  return amun_ol_select(plan, workspace, prev_cost, beam_offsets, N, S, k_per_sentence, k,
+                        out_idx, out_cost, stream);
+}
+
+amun_status amun_output_layer_partial(amun_ol* plan, const void* X, const void* W,
+                                      const float* b, int N, float* partial, void* workspace,
+                                      void* stream) {
+  amun_status s = check_score_args(plan, X, W, b, N, workspace);
+  if (s != AMUN_OK) return s;
+  if (N == 0) return AMUN_OK;
+  if (!partial) return fail(AMUN_EINVAL, "NULL partial");
+  s = run_scores(plan, X, W, b, N, workspace, nullptr, static_cast<cudaStream_t>(stream), 0);
+  if (s != AMUN_OK) return s;
+  MergeParams mp = base_merge(plan);
+  int grid_unused;
+  mp.part = static_cast<const float*>(workspace);
+  mp.layout = 0;
+  mp.sch = make_schedule(plan, N, &grid_unused);
+  mp.N = N;
+  mp.out_part = partial;
+  return run_merge(plan, mp, true, (int)cdiv(N, 4), static_cast<cudaStream_t>(stream));
+}
+
+amun_status amun_merge_partials(amun_ol* plan, const float* partials, int G,
+                                const float* prev_cost, const int32_t* beam_offsets, int N, int S,
+                                const int32_t* k_per_sentence, int k, int64_t* out_idx,
+                                float* out_cost, void* stream) {
+  if (!plan) return fail(AMUN_EINVAL, "NULL plan");
+  if (G < 1) return fail(AMUN_EINVAL, "G=%d must be >= 1", G);
+  amun_status s = check_select_args(plan, prev_cost, beam_offsets, N, S, k, out_idx, out_cost);
+  if (s != AMUN_OK) return s;
+  if (N > 0 && !partials) return fail(AMUN_EINVAL, "NULL partials");
+  if (S == 0) return AMUN_OK;
+  CUDA_TRY(cudaSetDevice(plan->device));
+  MergeParams mp = base_merge(plan);
+  mp.part = partials;
+  mp.layout = 1;
+  mp.G = G;
+  mp.N = N;
+  mp.S = S;
+  mp.prev_cost = prev_cost;
+  mp.offsets = beam_offsets;
+  mp.k_s = k_per_sentence;
+  mp.k = k;
+  mp.out_idx = reinterpret_cast<long long*>(out_idx);
+  mp.out_cost = out_cost;
+  return run_merge(plan, mp, false, S, static_cast<cudaStream_t>(stream));
+}
+
+amun_status amun_debug_logits(amun_ol* plan, const void* X, const void* W, const float* b, int N,
+                              float* logits, void* workspace, void* stream) {
+  amun_status s = check_score_args(plan, X, W, b, N, workspace);
+  if (s != AMUN_OK) return s;
+  if (N > 0 && !logits) return fail(AMUN_EINVAL, "NULL logits");
+  return run_scores(plan, X, W, b, N, workspace, logits, static_cast<cudaStream_t>(stream), 1);
+}
+
+amun_status amun_compact(const amun_column* cols, int n_cols, const uint8_t* alive, int N,
+                         const int32_t* beam_offsets, int S, int32_t* new_beam_offsets,
+                         int32_t* src_row, int32_t* counts, int32_t* counts_host, void* stream) {
+  if (n_cols < 0 || n_cols > AMUN_MAX_COLUMNS)
+    return fail(AMUN_EINVAL, "n_cols=%d out of [0, %d]", n_cols, AMUN_MAX_COLUMNS);
+  if (n_cols > 0 && !cols) return fail(AMUN_EINVAL, "NULL cols");
+  if (N < 0 || S < 0) return fail(AMUN_EINVAL, "negative N or S");
+  if (!beam_offsets || !new_beam_offsets || !counts) return fail(AMUN_EINVAL, "NULL offsets/counts");
+  if (N > 0 && (!alive || !src_row)) return fail(AMUN_EINVAL, "NULL alive/src_row");
+  CompactParams cp;
+  memset(&cp, 0, sizeof(cp));
+  for (int c = 0; c < n_cols; ++c) {
+    const amun_column& col = cols[c];
+    if (col.row_bytes <= 0 || (col.row_bytes & 3))
+      return fail(AMUN_EINVAL, "column %d: row_bytes=%lld must be a positive multiple of 4", c,
+                  (long long)col.row_bytes);
+    if (N > 0 && (!col.src || !col.dst)) return fail(AMUN_EINVAL, "column %d: NULL src/dst", c);
+    if (((reinterpret_cast<uintptr_t>(col.src) | reinterpret_cast<uintptr_t>(col.dst)) & 3) != 0)
+      return fail(AMUN_EINVAL, "column %d: src/dst must be 4-byte aligned", c);
+    const uintptr_t s0 = reinterpret_cast<uintptr_t>(col.src), d0 = reinterpret_cast<uintptr_t>(col.dst);
+    const uintptr_t len = (uintptr_t)col.row_bytes * (uintptr_t)N;
+    if (N > 0 && s0 < d0 + len && d0 < s0 + len)
+      return fail(AMUN_EINVAL, "column %d: src and dst overlap", c);
+    cp.col[c].src = static_cast<const uint8_t*>(col.src);
+    cp.col[c].dst = static_cast<uint8_t*>(col.dst);
+    cp.col[c].row_bytes = col.row_bytes;
+  }
+  cp.n_cols = n_cols;
+  cp.N = N;
+  cp.S = S;
+  cp.alive = alive;
+  cp.offsets = beam_offsets;
+  cp.new_offsets = new_beam_offsets;
+  cp.src_row = src_row;
+  cp.counts = counts;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int grid = N > 0 ? (int)cdiv(N, CP_ROWS) : 1;
+  compact_kernel<<<grid, CP_THREADS, 0, st>>>(cp);
+  CUDA_TRY(cudaGetLastError());
+  if (counts_host) {
+    CUDA_TRY(cudaMemcpyAsync(counts_host, counts, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  return AMUN_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,221 @@
+// merge.cuh — exact merge of partial states and per-sentence beam k-best.
+//
+// Row phase (the reduce step of Alg. 6, for (max, sum, k-best)
+// states): for row r, over its partial records j in fixed order,
+//   M = max_j m_j,  Z = sum_j s_j * exp(m_j - M)  (rescale of P:195-197),
+//   lse_r = M + log Z,  row k-best = best k of the union (l desc, v asc).
+// Sentence phase ("k-best ... simple extension", P:29 beam search;
+// readings G4/G5): only the winners are normalised (observation 2):
+//   cost = prev_cost[r] + (l - lse_r)
+// and the top-k_s over the sentence's rows is selected by
+// (cost desc, r asc, l desc, v asc). Per-row k-best with k >= k_s contains
+// the sentence's top-k_s, so the selection is exact.
+//
+// mode ROW: writes one merged partial record per row (vocab-shard output).
+// mode SENT: CTA per sentence, writes out_idx / out_cost.
+#pragma once
+#include "epilogue.cuh"
+
+namespace amun {
+
+struct MergeParams {
+  // partial locator: layout 0 = fused-kernel slots [slot][128][stride] with
+  // the Schedule; layout 1 = external [G][N][stride]
+  const float* __restrict__ part;
+  int stride, k_max, layout, G;
+  Schedule sch;
+  int N, S;
+  const float* __restrict__ prev_cost;
+  const int* __restrict__ offsets;
+  const int* __restrict__ k_s;
+  int k;
+  long long V_total;
+  long long* __restrict__ out_idx;
+  float* __restrict__ out_cost;
+  float* __restrict__ out_part;  // ROW mode: [N][stride]
+};
+
+__device__ __forceinline__ void row_splits(const MergeParams& p, int r, const float*& base,
+                                           long long& jstride, int& n) {
+  if (p.layout == 0) {
+    const int mt = r >> 7;
+    const long long c0 = p.sch.first_cta(mt), c1 = p.sch.last_cta(mt);
+    base = p.part + ((c0 + mt) * 128 + (r & 127)) * (long long)p.stride;
+    jstride = 128LL * p.stride;
+    n = (int)(c1 - c0 + 1);
+  } else {
+    base = p.part + (long long)r * p.stride;
+    jstride = (long long)p.N * p.stride;
+    n = p.G;
+  }
+}
+
+struct Cand {
+  float cost, l;
+  int r, v;
+};
+// a ranks before b in a sentence
+__device__ __forceinline__ bool better_cand(const Cand& a, const Cand& b) {
+  if (a.cost != b.cost) return a.cost > b.cost;
+  if (a.r != b.r) return a.r < b.r;
+  if (a.l != b.l) return a.l > b.l;
+  return a.v < b.v;
+}
+__device__ __forceinline__ Cand shfl_cand(const Cand& c, int src_xor) {
+  Cand o;
+  o.cost = __shfl_xor_sync(0xffffffffu, c.cost, src_xor);
+  o.l = __shfl_xor_sync(0xffffffffu, c.l, src_xor);
+  o.r = __shfl_xor_sync(0xffffffffu, c.r, src_xor);
+  o.v = __shfl_xor_sync(0xffffffffu, c.v, src_xor);
+  return o;
+}
+
+template <int KB>
+struct CandList {  // sorted by better_cand, capacity KB
+  Cand c[KB];
+  __device__ __forceinline__ void reset() {
+#pragma unroll
+    for (int i = 0; i < KB; ++i) c[i] = Cand{kNegInf, kNegInf, 0x7fffffff, 0x7fffffff};
+  }
+  __device__ __forceinline__ void insert(Cand x) {
+#pragma unroll
+    for (int i = 0; i < KB; ++i) {
+      const bool b = better_cand(x, c[i]);
+      const Cand t = c[i];
+      c[i] = b ? x : t;
+      x = b ? t : x;
+    }
+  }
+  __device__ __forceinline__ void pop() {
+#pragma unroll
+    for (int i = 0; i + 1 < KB; ++i) c[i] = c[i + 1];
+    c[KB - 1] = Cand{kNegInf, kNegInf, 0x7fffffff, 0x7fffffff};
+  }
+};
+
+// Row phase for row r, executed by one full warp. Returns lse (all lanes);
+// lane i < k_max receives the i-th best (l, v) of the row in (ol, ov).
+template <int KB>
+__device__ __forceinline__ void merge_row(const MergeParams& p, int r, int lane, float& M_out,
+                                          float& Z_out, float& ol, int& ov) {
+  const float* base;
+  long long js;
+  int n;
+  row_splits(p, r, base, js, n);
+  float M = kNegInf;
+  for (int j = lane; j < n; j += 32) M = fmaxf(M, base[j * js]);
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+  float Z = 0.f;
+  RowState<KB> lst;
+  lst.reset();
+  for (int j = lane; j < n; j += 32) {
+    const float* rec = base + j * js;
+    const float mj = rec[0];
+    if (mj != kNegInf) Z += rec[1] * expf(mj - M);
+    for (int i = 0; i < p.k_max; ++i) {
+      const float li = rec[2 + i];
+      const int vi = __float_as_int(rec[2 + p.k_max + i]);
+      if (vi >= 0 && better_lv(li, vi, lst.l[KB - 1], lst.v[KB - 1])) lst.insert(li, vi);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) Z += __shfl_xor_sync(0xffffffffu, Z, o);
+  M_out = M;
+  Z_out = Z;
+  ol = kNegInf;
+  ov = -1;
+  for (int i = 0; i < p.k_max; ++i) {
+    float bl = lst.l[0];
+    int bv = lst.v[0];
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      const float tl = __shfl_xor_sync(0xffffffffu, bl, o);
+      const int tv = __shfl_xor_sync(0xffffffffu, bv, o);
+      if (tv >= 0 && (bv < 0 || better_lv(tl, tv, bl, bv))) {
+        bl = tl;
+        bv = tv;
+      }
+    }
+    if (bv < 0) break;  // warp-uniform: no more candidates
+    if (lst.v[0] == bv) {  // owner pops (token ids are unique within a row)
+#pragma unroll
+      for (int t = 0; t + 1 < KB; ++t) {
+        lst.l[t] = lst.l[t + 1];
+        lst.v[t] = lst.v[t + 1];
+      }
+      lst.l[KB - 1] = kNegInf;
+      lst.v[KB - 1] = -1;
+    }
+    if (lane == i) {
+      ol = bl;
+      ov = bv;
+    }
+  }
+}
+
+template <int KB>
+__global__ void __launch_bounds__(128) merge_rows_kernel(const MergeParams p) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = blockIdx.x * 4 + warp;
+  if (r >= p.N) return;
+  float M, Z, l;
+  int v;
+  merge_row<KB>(p, r, lane, M, Z, l, v);
+  float* rec = p.out_part + (long long)r * p.stride;
+  if (lane == 0) {
+    rec[0] = M;
+    rec[1] = Z;
+  }
+  if (lane < p.k_max) {
+    rec[2 + lane] = l;
+    rec[2 + p.k_max + lane] = __int_as_float(v);
+  }
+}
+
+template <int KB>
+__global__ void __launch_bounds__(128) merge_sentences_kernel(const MergeParams p) {
+  pdl_wait();
+  const int s = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r0 = p.offsets[s], r1 = p.offsets[s + 1];
+  const int ks = p.k_s ? min(p.k_s[s], p.k) : p.k;
+  CandList<KB> cl;
+  cl.reset();
+  for (int r = r0 + warp; r < r1; r += 4) {
+    float M, Z, l;
+    int v;
+    merge_row<KB>(p, r, lane, M, Z, l, v);
+    if (v >= 0) {
+      const float lse = M + logf(Z);
+      cl.insert(Cand{p.prev_cost[r] + (l - lse), l, r, v});
+    }
+  }
+  __shared__ Cand wbest[4];
+  __shared__ Cand winner;
+  for (int i = 0; i < p.k; ++i) {
+    Cand b = cl.c[0];
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      const Cand t = shfl_cand(b, o);
+      if (better_cand(t, b)) b = t;
+    }
+    if (lane == 0) wbest[warp] = b;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      Cand w = wbest[0];
+      for (int q = 1; q < 4; ++q)
+        if (better_cand(wbest[q], w)) w = wbest[q];
+      winner = w;
+      const bool valid = (i < ks) && (w.v >= 0) && (w.v != 0x7fffffff);
+      p.out_idx[(long long)s * p.k + i] = valid ? (long long)w.r * p.V_total + w.v : -1LL;
+      p.out_cost[(long long)s * p.k + i] = valid ? w.cost : kNegInf;
+    }
+    __syncthreads();
+    const Cand w = winner;
+    if (cl.c[0].r == w.r && cl.c[0].v == w.v) cl.pop();
+    __syncthreads();
+  }
+}
+
+}  // namespace amun

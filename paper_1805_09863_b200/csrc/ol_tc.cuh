@@ -1,0 +1,218 @@
+// ol_tc.cuh — fused output layer on the 5th-gen tensor cores (sm_100a).
+//
+// Steps 1-4 of PAPER.md P:81-87 in one persistent, warp-specialised kernel:
+//   warp 0  TMA producer: X tile [128 rows x 64 K] and W tile [256 vocab x 64 K]
+//           per stage (128B swizzle), STAGES-deep mbarrier ring.
+//   warp 1  TMEM allocator + single-thread tcgen05.mma issuer:
+//           D[128 x width] (fp32, TMEM) += X_tile * W_tile^T, K = 16 per MMA.
+//           Two TMEM accumulators (2 x 256 columns = all 512) so the epilogue
+//           of tile t overlaps the MMAs of tile t+1.
+//   warps 2-5  epilogue: thread = hypothesis row (TMEM lane), tcgen05.ld of 32
+//           columns at a time, + bias (step 2), online max/sum-of-exp (step 3,
+//           Alg. 4 with the exp(Delta) rescale of P:193-200) and a register
+//           k-best (step 4). The N x V logits never reach HBM; each
+//           (row, CTA range) emits one partial record {m, s, top-k}
+//           (Alg. 6's per-shard state) for the merge kernel.
+// MODE 1 (test hook) writes the biased logits instead of statistics.
+#pragma once
+#include "epilogue.cuh"
+
+namespace amun {
+
+struct TcParams {
+  int N, V_local, v_offset, n_kblk;
+  Schedule sch;
+  const float* __restrict__ bias;
+  float* __restrict__ part;   // [slots][128][stride]
+  int stride, k_max;
+  float* __restrict__ logits; // MODE 1: [N][V_local]
+};
+
+constexpr int TC_BM = 128;
+constexpr int TC_BN = 256;
+constexpr int TC_BK = 64;
+constexpr int TC_STAGES = 4;
+constexpr int TC_A_BYTES = TC_BM * TC_BK * 2;   // 16 KB
+constexpr int TC_B_BYTES = TC_BN * TC_BK * 2;   // 32 KB
+constexpr int TC_THREADS = 192;
+constexpr int TC_SMEM = TC_STAGES * (TC_A_BYTES + TC_B_BYTES) + 1024 /*align*/ + 256 /*barriers*/;
+
+template <int KB, int MODE>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    ol_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
+                 const TcParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + TC_STAGES * TC_A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + TC_STAGES * TC_B_BYTES);
+  uint64_t* empty = full + TC_STAGES;
+  uint64_t* tfull = empty + TC_STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmX);
+    prefetch_tmap(&tmW);
+    for (int i = 0; i < TC_STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(tmem_holder, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  const long long start = (long long)blockIdx.x * p.sch.C;
+  const long long stop = min(start + p.sch.C, p.sch.total);
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer
+    // The whole warp walks the schedule (keeps it converged); lane 0 issues.
+    const uint64_t pol_x = policy_evict_last();     // X is re-read by every CTA
+    TileIter it{start, stop, p.sch.Vp};
+    int mt, v0, width;
+    bool last;
+    int stage = 0;
+    uint32_t phase = 0;
+    while (it.next(mt, v0, width, last)) {
+      for (int kb = 0; kb < p.n_kblk; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&full[stage], TC_A_BYTES + TC_B_BYTES);
+          tma_load_2d(&tmX, &full[stage], sA + stage * TC_A_BYTES, kb * TC_BK, mt * TC_BM, pol_x);
+          tma_load_2d(&tmW, &full[stage], sB + stage * TC_B_BYTES, kb * TC_BK, v0, 0ull);
+        }
+        __syncwarp();
+        if (++stage == TC_STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer
+    // The whole warp waits; lane 0 issues tcgen05.mma and the commits (a
+    // commit tracks the MMAs issued by the same thread).
+    TileIter it{start, stop, p.sch.Vp};
+    int mt, v0, width;
+    bool last;
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    while (it.next(mt, v0, width, last)) {
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d = tmem_base + acc * TC_BN;
+      const uint32_t idesc = idesc_bf16_f32(TC_BM, width);
+      for (int kb = 0; kb < p.n_kblk; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint64_t ad = sdesc_k_sw128(smem_u32(sA + stage * TC_A_BYTES));
+          const uint64_t bd = sdesc_k_sw128(smem_u32(sB + stage * TC_B_BYTES));
+#pragma unroll
+          for (int k = 0; k < TC_BK / 16; ++k)   // +32 bytes of K per MMA (>>4 = 2)
+            mma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+          mma_commit(&empty[stage]);              // smem slot free once these MMAs finish
+        }
+        __syncwarp();
+        if (++stage == TC_STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      if (lane == 0) mma_commit(&tfull[acc]);     // accumulator ready for the epilogue
+      __syncwarp();
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  } else {
+    // ------------------------------------------------ epilogue (warps 2..5)
+    const int q = warp & 3;                        // TMEM lane quadrant of this warp
+    const int row_local = q * 32 + lane;
+    const uint32_t t_lane = (uint32_t)(q * 32) << 16;
+    RowState<KB> st;
+    st.reset();
+    TileIter it{start, stop, p.sch.Vp};
+    int mt, v0, width;
+    bool last;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    while (it.next(mt, v0, width, last)) {
+      const int row = mt * TC_BM + row_local;
+      const int limit = min(width, p.V_local - v0);
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      for (int c = 0; c < width; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem_base + t_lane + acc * TC_BN + c, r);
+        const int nv = limit - c;
+        float bb[32];
+        if (nv >= 32) {
+          const float4* b4 = reinterpret_cast<const float4*>(p.bias + v0 + c);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float4 t = __ldg(b4 + j);
+            bb[4 * j + 0] = t.x;
+            bb[4 * j + 1] = t.y;
+            bb[4 * j + 2] = t.z;
+            bb[4 * j + 3] = t.w;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) bb[j] = (j < nv) ? __ldg(p.bias + v0 + c + j) : 0.f;
+        }
+        tmem_ld_wait(r);
+        float x[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) x[j] = (j < nv) ? __uint_as_float(r[j]) + bb[j] : kNegInf;
+        if constexpr (MODE == 1) {
+          if (row < p.N) {
+            float* out = p.logits + (long long)row * p.V_local + v0 + c;
+            for (int j = 0; j < 32 && j < nv; ++j) out[j] = x[j];
+          }
+        } else {
+          st.chunk32(x, p.v_offset + v0 + c);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      if (last) {
+        if constexpr (MODE == 0) {
+          if (row < p.N) {
+            const long long slot = (long long)blockIdx.x + mt;
+            st.emit(p.part + (slot * TC_BM + row_local) * p.stride, p.k_max);
+          }
+        }
+        st.reset();
+      }
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, 512);
+  }
+}
+
+}  // namespace amun

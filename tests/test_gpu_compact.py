@@ -1,0 +1,70 @@
+"""GPU compaction (Alg. 2 "Remove h from b") against the oracle: bit-exact
+columns, N', S_alive, new offsets and the row map."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import synth
+
+pytestmark = pytest.mark.gpu
+DEV = torch.device("cuda", 0)
+
+
+def run(N, S_sizes, alive, row_bytes_list, seed=0):
+    import paper_1805_09863_b200 as amun
+    off = torch.tensor(np.concatenate([[0], np.cumsum(S_sizes)]), dtype=torch.int32)
+    assert int(off[-1]) == N
+    cols_h = [synth.gen_bytes(seed + i, synth.S_STATE, N * rb).view(N, rb) if N else
+              torch.empty(0, rb, dtype=torch.uint8) for i, rb in enumerate(row_bytes_list)]
+    cols_d = [(c.to(DEV), torch.full_like(c, 0xAB, device=DEV)) for c in cols_h]
+    n, s_alive, new_off, src_row, counts = amun.compact(cols_d, alive.to(DEV), off.to(DEV))
+    ref_cols, ref_off, ref_src, ref_n, ref_s = O.compact([c.numpy() for c in cols_h],
+                                                          alive.numpy(), off.numpy())
+    assert n == ref_n and s_alive == ref_s
+    assert counts.cpu().tolist() == [ref_n, ref_s]
+    assert np.array_equal(new_off.cpu().numpy(), ref_off)
+    assert np.array_equal(src_row[:n].cpu().numpy(), ref_src)
+    for (src, dst), ref in zip(cols_d, ref_cols):
+        assert np.array_equal(dst[:n].cpu().numpy(), ref)
+        if n < N:   # rows past N' untouched
+            assert (dst[n:].cpu().numpy() == 0xAB).all()
+
+
+@pytest.mark.parametrize("p", [0.0, 0.1, 0.5, 0.9, 0.99, 1.0])
+def test_random_masks(p):
+    N, B = 6400, 5
+    alive = synth.gen_alive(int(p * 100), N, p)
+    run(N, [B] * (N // B), alive, [2048, 8192, 4, 8])
+
+
+def test_cfg4_state_row():
+    """The cfg4 per-hypothesis state: x bf16 [1024] 2048 B + decoder state 2x1024
+    fp32 8192 B + prev_cost 4 B + (sentence, slot) id 8 B = 10,252 B/row."""
+    f = synth.eos_schedule(synth.BASE_SEED + 4, 1280, 5).reshape(-1)
+    for t in [1, 5, 20, 40]:
+        alive = (f > t).to(torch.uint8)
+        run(6400, [5] * 1280, alive, [2048, 8192, 4, 8], seed=t)
+
+
+@pytest.mark.parametrize("N", [0, 1, 31, 33, 257, 1000])
+def test_small_and_ragged(N):
+    rng = np.random.default_rng(N)
+    sizes = []
+    left = N
+    while left > 0:
+        s = int(min(left, rng.integers(0, 7)))
+        sizes.append(s)
+        left -= s
+    sizes.append(0)
+    alive = torch.from_numpy((rng.random(N) < 0.6).astype(np.uint8))
+    run(N, sizes, alive, [16, 4, 48, 20])
+
+
+def test_one_survivor_per_sentence_and_alternating():
+    N, B = 1200, 6
+    alive = torch.zeros(N, dtype=torch.uint8)
+    alive[::B] = 1
+    run(N, [B] * (N // B), alive, [64])
+    alive = torch.tensor([i % 2 for i in range(N)], dtype=torch.uint8)
+    run(N, [B] * (N // B), alive, [64, 12])
