@@ -48,7 +48,7 @@ def load_peaks():
 
 class ClockSampler:
     """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+    Q = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
@@ -71,7 +71,15 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def wait_first(self, timeout=5.0):
+        t0 = time.time()
+        while self.proc and not self.lines and time.time() - t0 < timeout:
+            time.sleep(0.02)
+
+    def mark(self, which):
+        setattr(self, which, time.time())
 
     def __exit__(self, *a):
         if self.proc:
@@ -84,8 +92,12 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
+        t0 = getattr(self, "t_start", 0.0) - 0.15
+        t1 = getattr(self, "t_end", 1e30) + 0.15
+        for ts, ln in self.lines:
+            if not (t0 <= ts <= t1):
+                continue
+            f = [x.strip() for x in ln.split(",")][1:]
             if len(f) < 6:
                 continue
             try:
@@ -172,7 +184,7 @@ def config_of(w, args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="beam", choices=list(synth.CONFIGS))
@@ -224,11 +236,14 @@ def main():
         torch.distributed.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
+        clk.wait_first()
+        clk.mark("t_start")
         start.record()
         for i in range(K):
             idx, cost = step(i, with_events=ev[i])
         end.record()
         torch.cuda.synchronize()
+        clk.mark("t_end")
     if world > 1:
         torch.distributed.barrier()
     ms = start.elapsed_time(end)
