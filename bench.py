@@ -322,7 +322,7 @@ def main():
     cpu = None
     parity = None
     if world == 1 and not args.no_cpu_baseline:
-        n_sent = int(os.environ.get("AMUN_CPU_SENTENCES", "24"))
+        n_sent = int(os.environ.get("AMUN_CPU_SENTENCES", "128"))
         dt, rows, res, logp, pcs = oracle_sample(w, X_h, W_h, b_h, pc_h, n_sent)
         cpu = {"value": rows / dt, "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
                "sample": f"first {n_sent} sentences ({rows} rows) x full V={w.V}, one pass, "
