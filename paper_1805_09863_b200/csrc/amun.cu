@@ -66,7 +66,23 @@ struct MapEntry {
   CUtensorMap map;
 };
 
-inline int kbucket(int k) { return k <= 1 ? 1 : k <= 2 ? 2 : k <= 4 ? 4 : k <= 8 ? 8 : 16; }
+// k-best capacity buckets compiled into the kernels (a row keeps exactly
+// kbucket(k_max) >= k_max entries; smaller = fewer insertions).
+inline int kbucket(int k) {
+  return k <= 6 ? (k < 1 ? 1 : k) : k <= 8 ? 8 : k <= 12 ? 12 : 16;
+}
+#define AMUN_KB_SWITCH(kb, CALL) \
+  switch (kb) {                  \
+    case 1: return CALL(1);      \
+    case 2: return CALL(2);      \
+    case 3: return CALL(3);      \
+    case 4: return CALL(4);      \
+    case 5: return CALL(5);      \
+    case 6: return CALL(6);      \
+    case 8: return CALL(8);      \
+    case 12: return CALL(12);    \
+    default: return CALL(16);    \
+  }
 inline long long cdiv(long long a, long long b) { return (a + b - 1) / b; }
 
 }  // namespace
@@ -179,13 +195,9 @@ amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b
     tp.stride = pl->stride;
     tp.k_max = pl->k_max;
     tp.logits = logits;
-    switch (mode == 1 ? 1 : pl->kb) {
-      case 1: return launch_tc<1>(pl, mx, mw, tp, grid, st, mode);
-      case 2: return launch_tc<2>(pl, mx, mw, tp, grid, st, mode);
-      case 4: return launch_tc<4>(pl, mx, mw, tp, grid, st, mode);
-      case 8: return launch_tc<8>(pl, mx, mw, tp, grid, st, mode);
-      default: return launch_tc<16>(pl, mx, mw, tp, grid, st, mode);
-    }
+#define TC_CALL(K) launch_tc<K>(pl, mx, mw, tp, grid, st, mode)
+    AMUN_KB_SWITCH(mode == 1 ? 1 : pl->kb, TC_CALL)
+#undef TC_CALL
   } else {
     SimtParams sp;
     sp.N = N;
@@ -200,45 +212,38 @@ amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b
     sp.stride = pl->stride;
     sp.k_max = pl->k_max;
     sp.logits = logits;
-    switch (mode == 1 ? 1 : pl->kb) {
-      case 1: return launch_simt<1>(sp, grid, st, mode);
-      case 2: return launch_simt<2>(sp, grid, st, mode);
-      case 4: return launch_simt<4>(sp, grid, st, mode);
-      case 8: return launch_simt<8>(sp, grid, st, mode);
-      default: return launch_simt<16>(sp, grid, st, mode);
-    }
+#define SIMT_CALL(K) launch_simt<K>(sp, grid, st, mode)
+    AMUN_KB_SWITCH(mode == 1 ? 1 : pl->kb, SIMT_CALL)
+#undef SIMT_CALL
   }
 }
 
 template <int KB>
 amun_status launch_merge(const MergeParams& mp, bool rows, int grid, cudaStream_t st) {
   if (grid == 0) return AMUN_OK;
-  if (rows) {
-    merge_rows_kernel<KB><<<grid, 128, 0, st>>>(mp);
-  } else {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(128);
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
+  // Programmatic dependent launch: the merge grid may be scheduled while the
+  // fused kernel still runs; it waits (griddepcontrol.wait) for its results.
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(MG_WARPS * 32);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (rows)
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, merge_rows_kernel<KB>, mp));
+  else
     CUDA_TRY(cudaLaunchKernelEx(&cfg, merge_sentences_kernel<KB>, mp));
-  }
   CUDA_TRY(cudaGetLastError());
   return AMUN_OK;
 }
 
 amun_status run_merge(amun_ol* pl, const MergeParams& mp, bool rows, int grid, cudaStream_t st) {
-  switch (pl->kb) {
-    case 1: return launch_merge<1>(mp, rows, grid, st);
-    case 2: return launch_merge<2>(mp, rows, grid, st);
-    case 4: return launch_merge<4>(mp, rows, grid, st);
-    case 8: return launch_merge<8>(mp, rows, grid, st);
-    default: return launch_merge<16>(mp, rows, grid, st);
-  }
+#define MERGE_CALL(K) launch_merge<K>(mp, rows, grid, st)
+  AMUN_KB_SWITCH(pl->kb, MERGE_CALL)
+#undef MERGE_CALL
 }
 
 amun_status check_select_args(const amun_ol* pl, const float* prev_cost,
@@ -409,7 +414,7 @@ amun_status amun_output_layer_partial(amun_ol* plan, const void* X, const void* 
   mp.sch = make_schedule(plan, N, &grid_unused);
   mp.N = N;
   mp.out_part = partial;
-  return run_merge(plan, mp, true, (int)cdiv(N, 4), static_cast<cudaStream_t>(stream));
+  return run_merge(plan, mp, true, (int)cdiv(N, MG_WARPS), static_cast<cudaStream_t>(stream));
 }
 
 amun_status amun_merge_partials(amun_ol* plan, const float* partials, int G,

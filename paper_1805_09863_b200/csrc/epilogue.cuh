@@ -59,9 +59,33 @@ struct RowState {
     }
   }
 
+  // Insert a NEW element whose token id is larger than every id already in
+  // the list (true inside one ascending scan): ties keep the older entries
+  // ahead. Position p = #entries >= x; all compares are independent, so the
+  // dependency depth is short (no carried compare-swap chain).
+  __device__ __forceinline__ void insert_new(float x, int id) {
+    int p = 0;
+#pragma unroll
+    for (int i = 0; i < KB; ++i) p += (l[i] >= x) ? 1 : 0;
+#pragma unroll
+    for (int i = KB - 1; i >= 1; --i) {
+      const float li = (i > p) ? l[i - 1] : ((i == p) ? x : l[i]);
+      const int vi = (i > p) ? v[i - 1] : ((i == p) ? id : v[i]);
+      l[i] = li;
+      v[i] = vi;
+    }
+    if (p == 0) {
+      l[0] = x;
+      v[0] = id;
+    }
+  }
+
   // Consume 32 biased logits x[j] with token ids vbase + j, in ascending j.
-  // Masked entries must already be -inf.
-  __device__ __forceinline__ void chunk32(const float (&x)[32], int vbase) {
+  // Masked entries must already be -inf. `xs` is this thread's 32-float
+  // shared-memory scratch row (128-byte aligned); its 16-byte chunks are
+  // XOR-swizzled by `sw` (= row & 7) so a warp's stores are conflict-free.
+  // Must be called by all 32 lanes of the warp together (warp-uniform gate).
+  __device__ __forceinline__ void chunk32(const float (&x)[32], int vbase, float* xs, int sw) {
     float t[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) t[j] = fmaxf(x[j], x[j + 16]);
@@ -70,26 +94,60 @@ struct RowState {
 #pragma unroll
       for (int j = 0; j < w; ++j) t[j] = fmaxf(t[j], t[j + w]);
     const float cm = t[0];
-    if (cm == kNegInf) return;  // whole chunk masked: nothing to add (guards -inf - -inf)
-    if (cm > m) {               // Alg. 4: new max -> rescale the sum by e^{Delta}
-      s *= ex2((m - cm) * kLog2e);
-      m = cm;
-    }
-    const float ms = m * kLog2e;
-    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+    if (cm != kNegInf) {        // whole chunk masked: nothing to add (guards -inf - -inf)
+      if (cm > m) {             // Alg. 4: new max -> rescale the sum by e^{Delta}
+        s *= ex2((m - cm) * kLog2e);
+        m = cm;
+      }
+      const float ms = m * kLog2e;
+      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
 #pragma unroll
-    for (int j = 0; j < 32; j += 4) {
-      a0 += ex2(fmaf(x[j + 0], kLog2e, -ms));
-      a1 += ex2(fmaf(x[j + 1], kLog2e, -ms));
-      a2 += ex2(fmaf(x[j + 2], kLog2e, -ms));
-      a3 += ex2(fmaf(x[j + 3], kLog2e, -ms));
+      for (int j = 0; j < 32; j += 4) {
+        a0 += ex2(fmaf(x[j + 0], kLog2e, -ms));
+        a1 += ex2(fmaf(x[j + 1], kLog2e, -ms));
+        a2 += ex2(fmaf(x[j + 2], kLog2e, -ms));
+        a3 += ex2(fmaf(x[j + 3], kLog2e, -ms));
+      }
+      s += (a0 + a1) + (a2 + a3);
     }
-    s += (a0 + a1) + (a2 + a3);
-    if (cm > l[KB - 1]) {  // Alg. 4 "if p' > max ... best <- i", generalised to k
+    // k-best (Alg. 4 "if p' > max ... best <- i", generalised to k): only
+    // elements above the current k-th best can enter. The chunk max gates
+    // the whole path; candidates are found with one bitmask and visited in
+    // ascending j, each read back from shared memory.
+    const float thr = l[KB - 1];
+    const bool need = cm > thr;
+    if (__any_sync(0xffffffffu, need)) {
+      if (need) {
+        float4* xs4 = reinterpret_cast<float4*>(xs);
 #pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (x[j] > l[KB - 1]) insert(x[j], vbase + j);
+        for (int j = 0; j < 8; ++j)
+          xs4[j ^ sw] = make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
+        uint32_t mask = 0;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) mask |= (x[j] > thr) ? (1u << j) : 0u;
+        while (mask) {
+          const int j = __ffs(mask) - 1;
+          mask &= mask - 1;
+          const float xv = xs[(((j >> 2) ^ sw) << 2) | (j & 3)];
+          if (xv > l[KB - 1]) insert_new(xv, vbase + j);
+        }
+      }
+      __syncwarp();
     }
+  }
+
+  // Monoid combine with another partial state over a disjoint column set
+  // (the rescale of P:195-197 and a k-best union with the full tie key).
+  __device__ __forceinline__ void combine(float m2, float s2, const float* l2, const int* v2) {
+    const float mn = fmaxf(m, m2);
+    if (mn != kNegInf) {
+      s = (m == kNegInf ? 0.f : s * ex2((m - mn) * kLog2e)) +
+          (m2 == kNegInf ? 0.f : s2 * ex2((m2 - mn) * kLog2e));
+      m = mn;
+    }
+#pragma unroll
+    for (int i = 0; i < KB; ++i)
+      if (v2[i] >= 0 && better_lv(l2[i], v2[i], l[KB - 1], v[KB - 1])) insert(l2[i], v2[i]);
   }
 
   // Partial record {m, s, l[0..k_max), v[0..k_max)} (see amun.h).

@@ -95,6 +95,8 @@ struct CandList {  // sorted by better_cand, capacity KB
 
 // Row phase for row r, executed by one full warp. Returns lse (all lanes);
 // lane i < k_max receives the i-th best (l, v) of the row in (ol, ov).
+// Lane j takes record j (already sorted by the producer, so it IS the lane's
+// list); records j + 32, j + 64, ... (only with > 32 splits) are inserted.
 template <int KB>
 __device__ __forceinline__ void merge_row(const MergeParams& p, int r, int lane, float& M_out,
                                           float& Z_out, float& ol, int& ov) {
@@ -102,22 +104,38 @@ __device__ __forceinline__ void merge_row(const MergeParams& p, int r, int lane,
   long long js;
   int n;
   row_splits(p, r, base, js, n);
-  float M = kNegInf;
-  for (int j = lane; j < n; j += 32) M = fmaxf(M, base[j * js]);
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-  float Z = 0.f;
   RowState<KB> lst;
   lst.reset();
-  for (int j = lane; j < n; j += 32) {
+  float m0 = kNegInf, s0 = 0.f;
+  if (lane < n) {
+    const float* rec = base + lane * js;
+    m0 = rec[0];
+    s0 = rec[1];
+#pragma unroll
+    for (int i = 0; i < KB; ++i) {
+      if (i < p.k_max) {
+        lst.l[i] = rec[2 + i];
+        lst.v[i] = __float_as_int(rec[2 + p.k_max + i]);
+      }
+    }
+  }
+  float M = m0;
+  for (int j = lane + 32; j < n; j += 32) {
     const float* rec = base + j * js;
-    const float mj = rec[0];
-    if (mj != kNegInf) Z += rec[1] * expf(mj - M);
+    M = fmaxf(M, rec[0]);
     for (int i = 0; i < p.k_max; ++i) {
       const float li = rec[2 + i];
       const int vi = __float_as_int(rec[2 + p.k_max + i]);
       if (vi >= 0 && better_lv(li, vi, lst.l[KB - 1], lst.v[KB - 1])) lst.insert(li, vi);
     }
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+  float Z = (m0 != kNegInf) ? s0 * expf(m0 - M) : 0.f;
+  for (int j = lane + 32; j < n; j += 32) {
+    const float* rec = base + j * js;
+    const float mj = rec[0];
+    if (mj != kNegInf) Z += rec[1] * expf(mj - M);
   }
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) Z += __shfl_xor_sync(0xffffffffu, Z, o);
@@ -154,10 +172,13 @@ __device__ __forceinline__ void merge_row(const MergeParams& p, int r, int lane,
   }
 }
 
+constexpr int MG_WARPS = 8;
+
 template <int KB>
-__global__ void __launch_bounds__(128) merge_rows_kernel(const MergeParams p) {
+__global__ void __launch_bounds__(MG_WARPS * 32) merge_rows_kernel(const MergeParams p) {
+  pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r = blockIdx.x * 4 + warp;
+  const int r = blockIdx.x * MG_WARPS + warp;
   if (r >= p.N) return;
   float M, Z, l;
   int v;
@@ -174,7 +195,7 @@ __global__ void __launch_bounds__(128) merge_rows_kernel(const MergeParams p) {
 }
 
 template <int KB>
-__global__ void __launch_bounds__(128) merge_sentences_kernel(const MergeParams p) {
+__global__ void __launch_bounds__(MG_WARPS * 32) merge_sentences_kernel(const MergeParams p) {
   pdl_wait();
   const int s = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -182,7 +203,7 @@ __global__ void __launch_bounds__(128) merge_sentences_kernel(const MergeParams 
   const int ks = p.k_s ? min(p.k_s[s], p.k) : p.k;
   CandList<KB> cl;
   cl.reset();
-  for (int r = r0 + warp; r < r1; r += 4) {
+  for (int r = r0 + warp; r < r1; r += MG_WARPS) {
     float M, Z, l;
     int v;
     merge_row<KB>(p, r, lane, M, Z, l, v);
@@ -191,7 +212,7 @@ __global__ void __launch_bounds__(128) merge_sentences_kernel(const MergeParams 
       cl.insert(Cand{p.prev_cost[r] + (l - lse), l, r, v});
     }
   }
-  __shared__ Cand wbest[4];
+  __shared__ Cand wbest[MG_WARPS];
   __shared__ Cand winner;
   for (int i = 0; i < p.k; ++i) {
     Cand b = cl.c[0];
@@ -204,7 +225,7 @@ __global__ void __launch_bounds__(128) merge_sentences_kernel(const MergeParams 
     __syncthreads();
     if (threadIdx.x == 0) {
       Cand w = wbest[0];
-      for (int q = 1; q < 4; ++q)
+      for (int q = 1; q < MG_WARPS; ++q)
         if (better_cand(wbest[q], w)) w = wbest[q];
       winner = w;
       const bool valid = (i < ks) && (w.v >= 0) && (w.v != 0x7fffffff);

@@ -21,12 +21,13 @@ struct SimtParams {
   float* __restrict__ logits;    // MODE 1
 };
 
-constexpr int SIMT_KC = 64;
+constexpr int SIMT_KC = 32;
 
 template <int KB, int MODE>
 __global__ void __launch_bounds__(128) ol_simt_kernel(const SimtParams p) {
   __shared__ float xs[128][SIMT_KC + 1];
   __shared__ __align__(16) float ws[32][SIMT_KC];
+  __shared__ __align__(128) float xsc[128 * 32];
   const int tid = threadIdx.x;
   RowState<KB> st;
   st.reset();
@@ -72,7 +73,7 @@ __global__ void __launch_bounds__(128) ol_simt_kernel(const SimtParams p) {
           for (int j = 0; j < 32 && j < nv; ++j) out[j] = x[j];
         }
       } else {
-        st.chunk32(x, p.v_offset + v0 + c);
+        st.chunk32(x, p.v_offset + v0 + c, xsc + tid * 32, tid & 7);
       }
     }
     if (last) {

@@ -7,12 +7,17 @@
 //           D[128 x width] (fp32, TMEM) += X_tile * W_tile^T, K = 16 per MMA.
 //           Two TMEM accumulators (2 x 256 columns = all 512) so the epilogue
 //           of tile t overlaps the MMAs of tile t+1.
-//   warps 2-5  epilogue: thread = hypothesis row (TMEM lane), tcgen05.ld of 32
-//           columns at a time, + bias (step 2), online max/sum-of-exp (step 3,
-//           Alg. 4 with the exp(Delta) rescale of P:193-200) and a register
-//           k-best (step 4). The N x V logits never reach HBM; each
-//           (row, CTA range) emits one partial record {m, s, top-k}
-//           (Alg. 6's per-shard state) for the merge kernel.
+//   warps 2-9  epilogue, two groups of four warps (one warp per TMEM lane
+//           quadrant in each group; group g takes the 32-column chunks
+//           c = g, g+2, ... of every tile, so two warps per SM sub-partition
+//           hide each other's latency). Thread = hypothesis row. Per chunk:
+//           tcgen05.ld of 32 columns, + bias (step 2), online max/sum-of-exp
+//           (step 3, Alg. 4 with the exp(Delta) rescale of P:193-200) and a
+//           register k-best (step 4). The N x V logits never reach
+//           HBM. At the end of a CTA's range in an M-tile the two groups'
+//           states are combined (same monoid as the merge) and one partial
+//           record {m, s, top-k} per (row, CTA range) is written (Alg. 6's
+//           per-shard state).
 // MODE 1 (test hook) writes the biased logits instead of statistics.
 #pragma once
 #include "epilogue.cuh"
@@ -34,8 +39,58 @@ constexpr int TC_BK = 64;
 constexpr int TC_STAGES = 4;
 constexpr int TC_A_BYTES = TC_BM * TC_BK * 2;   // 16 KB
 constexpr int TC_B_BYTES = TC_BN * TC_BK * 2;   // 32 KB
-constexpr int TC_THREADS = 192;
-constexpr int TC_SMEM = TC_STAGES * (TC_A_BYTES + TC_B_BYTES) + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int TC_EPI_GROUPS = 2;
+constexpr int TC_EPI_THREADS = TC_EPI_GROUPS * 128;
+constexpr int TC_THREADS = 64 + TC_EPI_THREADS;  // TMA warp + MMA warp + epilogue
+constexpr int TC_XS_BYTES = TC_EPI_GROUPS * 128 * 32 * 4;   // candidate scratch, 16 KB/group
+constexpr int TC_MS_BYTES = 128 * 2 * 4;                    // group-exchange (m, s)
+constexpr int TC_SMEM = TC_STAGES * (TC_A_BYTES + TC_B_BYTES) + TC_XS_BYTES + TC_MS_BYTES +
+                        1024 /*align*/ + 256 /*barriers*/;
+
+// Bias of columns [v0 + c0, v0 + c0 + 32) (zero past `limit`): eight 16-byte
+// loads whose address is the same for every lane of the warp (broadcast).
+__device__ __forceinline__ void load_bias32(const float* __restrict__ bias, int v0, int c0,
+                                            int limit, float (&bb)[32]) {
+  const int nv = limit - c0;
+  if (nv >= 32) {
+    const float4* b4 = reinterpret_cast<const float4*>(bias + v0 + c0);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float4 t = __ldg(b4 + j);
+      bb[4 * j + 0] = t.x;
+      bb[4 * j + 1] = t.y;
+      bb[4 * j + 2] = t.z;
+      bb[4 * j + 3] = t.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) bb[j] = (j < nv) ? __ldg(bias + v0 + c0 + j) : 0.f;
+  }
+}
+
+// Step 2 (+ bias) and the per-row statistics for one 32-column chunk.
+template <int KB, int MODE>
+__device__ __forceinline__ void consume_chunk(const TcParams& p, RowState<KB>& st,
+                                              const uint32_t (&r)[32], const float (&bb)[32],
+                                              int row, int v0, int c0, int limit, float* xs,
+                                              int sw) {
+  const int nv = limit - c0;
+  float x[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) x[j] = (j < nv) ? __uint_as_float(r[j]) + bb[j] : kNegInf;
+  if constexpr (MODE == 1) {
+    if (row < p.N) {
+      float* out = p.logits + (long long)row * p.V_local + v0 + c0;
+      for (int j = 0; j < 32 && j < nv; ++j) out[j] = x[j];
+    }
+  } else {
+    st.chunk32(x, p.v_offset + v0 + c0, xs, sw);
+  }
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 
 template <int KB, int MODE>
 __global__ void __launch_bounds__(TC_THREADS, 1)
@@ -46,7 +101,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + TC_STAGES * TC_A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB + TC_STAGES * TC_B_BYTES);
+  float* xs_all = reinterpret_cast<float*>(sB + TC_STAGES * TC_B_BYTES);
+  float* ms_x = reinterpret_cast<float*>(sB + TC_STAGES * TC_B_BYTES + TC_XS_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + TC_STAGES * TC_B_BYTES + TC_XS_BYTES +
+                                               TC_MS_BYTES);
   uint64_t* empty = full + TC_STAGES;
   uint64_t* tfull = empty + TC_STAGES;
   uint64_t* tempty = tfull + 2;
@@ -64,7 +122,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 128);
+      mbar_init(&tempty[i], TC_EPI_THREADS);
     }
     fence_barrier_init();
   }
@@ -76,6 +134,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  pdl_trigger();   // let the dependent merge grid get scheduled early (it waits for us)
 
   const long long start = (long long)blockIdx.x * p.sch.C;
   const long long stop = min(start + p.sch.C, p.sch.total);
@@ -143,10 +202,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       if (acc == 0) acc_phase ^= 1;
     }
   } else {
-    // ------------------------------------------------ epilogue (warps 2..5)
+    // ------------------------------------------------ epilogue (warps 2..9)
+    const int e = warp - 2;
+    const int grp = e >> 2;                        // 0 or 1: which chunks
     const int q = warp & 3;                        // TMEM lane quadrant of this warp
     const int row_local = q * 32 + lane;
+    const int sw = row_local & 7;
     const uint32_t t_lane = (uint32_t)(q * 32) << 16;
+    float* xs = xs_all + (grp * 128 + row_local) * 32;
     RowState<KB> st;
     st.reset();
     TileIter it{start, stop, p.sch.Vp};
@@ -154,51 +217,60 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     bool last;
     int acc = 0;
     uint32_t acc_phase = 0;
+    uint32_t r[32];
+    float ba[32], bn[32];
     while (it.next(mt, v0, width, last)) {
       const int row = mt * TC_BM + row_local;
       const int limit = min(width, p.V_local - v0);
+      const int nch = (width + 31) >> 5;
+      // bias of this group's first chunk requested before the accumulator wait
+      if (grp < nch) load_bias32(p.bias, v0, grp * 32, limit, ba);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      for (int c = 0; c < width; c += 32) {
-        uint32_t r[32];
-        tmem_ld32(tmem_base + t_lane + acc * TC_BN + c, r);
-        const int nv = limit - c;
-        float bb[32];
-        if (nv >= 32) {
-          const float4* b4 = reinterpret_cast<const float4*>(p.bias + v0 + c);
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const float4 t = __ldg(b4 + j);
-            bb[4 * j + 0] = t.x;
-            bb[4 * j + 1] = t.y;
-            bb[4 * j + 2] = t.z;
-            bb[4 * j + 3] = t.w;
-          }
-        } else {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) bb[j] = (j < nv) ? __ldg(p.bias + v0 + c + j) : 0.f;
-        }
+      const uint32_t tbase = tmem_base + t_lane + acc * TC_BN;
+      for (int c = grp; c < nch; c += 4) {
+        // chunk c with its bias in ba; the bias of chunk c+2 prefetched into bn
+        tmem_ld32(tbase + c * 32, r);
+        if (c + 2 < nch) load_bias32(p.bias, v0, (c + 2) * 32, limit, bn);
         tmem_ld_wait(r);
-        float x[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) x[j] = (j < nv) ? __uint_as_float(r[j]) + bb[j] : kNegInf;
-        if constexpr (MODE == 1) {
-          if (row < p.N) {
-            float* out = p.logits + (long long)row * p.V_local + v0 + c;
-            for (int j = 0; j < 32 && j < nv; ++j) out[j] = x[j];
-          }
-        } else {
-          st.chunk32(x, p.v_offset + v0 + c);
-        }
+        consume_chunk<KB, MODE>(p, st, r, ba, row, v0, c * 32, limit, xs, sw);
+        if (c + 2 >= nch) break;
+        tmem_ld32(tbase + (c + 2) * 32, r);
+        if (c + 4 < nch) load_bias32(p.bias, v0, (c + 4) * 32, limit, ba);
+        tmem_ld_wait(r);
+        consume_chunk<KB, MODE>(p, st, r, bn, row, v0, (c + 2) * 32, limit, xs, sw);
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
       if (last) {
         if constexpr (MODE == 0) {
-          if (row < p.N) {
-            const long long slot = (long long)blockIdx.x + mt;
-            st.emit(p.part + (slot * TC_BM + row_local) * p.stride, p.k_max);
+          // combine the two groups' states for this row, then emit
+          if (grp == 1) {
+#pragma unroll
+            for (int i = 0; i < KB; ++i) {
+              xs[i] = st.l[i];
+              xs[16 + i] = __int_as_float(st.v[i]);
+            }
+            ms_x[2 * row_local] = st.m;
+            ms_x[2 * row_local + 1] = st.s;
           }
+          named_bar_sync(1 + q, 64);
+          if (grp == 0) {
+            const float* o = xs + 128 * 32;        // the same row of group 1
+            float l2[KB];
+            int v2[KB];
+#pragma unroll
+            for (int i = 0; i < KB; ++i) {
+              l2[i] = o[i];
+              v2[i] = __float_as_int(o[16 + i]);
+            }
+            st.combine(ms_x[2 * row_local], ms_x[2 * row_local + 1], l2, v2);
+            if (row < p.N) {
+              const long long slot = (long long)blockIdx.x + mt;
+              st.emit(p.part + (slot * TC_BM + row_local) * p.stride, p.k_max);
+            }
+          }
+          named_bar_sync(5 + q, 64);   // group 1 may reuse its scratch row after this
         }
         st.reset();
       }
