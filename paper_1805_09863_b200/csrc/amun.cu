@@ -138,12 +138,19 @@ amun_status get_map(amun_ol* pl, MapEntry* cache, int n, int& next, const void* 
 
 Schedule make_schedule(const amun_ol* pl, int N, int* grid) {
   Schedule s;
-  const long long n_mt = cdiv(N, 128);
+  const long long G = pl->num_sms;
+  const long long n_mt = cdiv(N > 0 ? N : 1, 128);
   s.Vp = cdiv(pl->V_local, 16) * 16;
-  s.total = n_mt * s.Vp;
-  s.C = cdiv(cdiv(s.total, pl->num_sms), 16) * 16;
-  if (s.C < 16) s.C = 16;
-  *grid = (int)cdiv(s.total, s.C);
+  const long long splits = G / n_mt;   // aligned mode: vocab splits per M-tile
+  if (splits >= 1 && n_mt * splits * 10 >= G * 9) {
+    s.C = cdiv(cdiv(s.Vp, splits), 16) * 16;
+    s.band = cdiv(s.Vp, s.C) * s.C;
+  } else {
+    s.C = cdiv(cdiv(n_mt * s.Vp, G), 16) * 16;
+    s.band = s.Vp;
+  }
+  s.total = n_mt * s.band;
+  *grid = (int)cdiv((n_mt - 1) * s.band + s.Vp, s.C);
   return s;
 }
 

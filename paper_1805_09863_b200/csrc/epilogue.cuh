@@ -165,28 +165,40 @@ struct RowState {
 };
 
 // Static persistent schedule shared by the fused kernels and the merge.
-// The flattened column space [0, n_mt * Vp) (Vp = V_local rounded up to 16)
-// is cut into equal ranges of C columns (C % 16 == 0), one per CTA; a CTA
-// walks its range in tiles of <= 256 columns; a range may span two M-tiles
-// (segments). CTA c's partial for M-tile mt goes to slot c + mt (unique).
+// The flattened column space has one band of `band` columns per M-tile, of
+// which the first Vp (= V_local rounded up to 16) are real; CTA c owns the
+// flat range [c*C, (c+1)*C) (C % 16 == 0) and walks its real columns in
+// tiles of <= 256 columns; a range may span two M-tiles (segments). CTA c's
+// partial for M-tile mt goes to slot c + mt (unique).
+//   aligned mode: band = s*C with s splits per M-tile, so the CTAs of all
+//     M-tiles start at the same vocab offsets and stream each W tile at the
+//     same time (one HBM read, the other M-tiles hit in L2);
+//   flattened mode: band = Vp, C = total / #SMs (many M-tiles).
 struct Schedule {
-  long long Vp, C, total;
-  __device__ __forceinline__ long long first_cta(int mt) const { return (mt * Vp) / C; }
-  __device__ __forceinline__ long long last_cta(int mt) const { return ((mt + 1) * Vp - 1) / C; }
+  long long band, Vp, C, total;
+  __device__ __forceinline__ long long first_cta(int mt) const { return (mt * band) / C; }
+  __device__ __forceinline__ long long last_cta(int mt) const { return (mt * band + Vp - 1) / C; }
 };
 
 struct TileIter {
-  long long pos, end, Vp;
+  long long pos, end;
+  Schedule sch;
   __device__ __forceinline__ bool next(int& mt, int& v0, int& width, bool& last) {
-    if (pos >= end) return false;
-    mt = (int)(pos / Vp);
-    const long long base = (long long)mt * Vp;
-    v0 = (int)(pos - base);
-    const long long seg_end = min(base + Vp, end) - base;
-    width = (int)min(256LL, seg_end - v0);
-    last = (v0 + width == seg_end);
-    pos += width;
-    return true;
+    for (;;) {
+      if (pos >= end) return false;
+      mt = (int)(pos / sch.band);
+      const long long base = (long long)mt * sch.band;
+      if (pos - base >= sch.Vp) {  // padding of an aligned band: skip to the next band
+        pos = base + sch.band;
+        continue;
+      }
+      v0 = (int)(pos - base);
+      const long long seg_end = min(base + sch.Vp, end) - base;
+      width = (int)min(256LL, seg_end - v0);
+      last = (v0 + width == seg_end);
+      pos += width;
+      return true;
+    }
   }
 };
 

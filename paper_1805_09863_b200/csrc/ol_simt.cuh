@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(128) ol_simt_kernel(const SimtParams p) {
   st.reset();
   const long long start = (long long)blockIdx.x * p.sch.C;
   const long long stop = min(start + p.sch.C, p.sch.total);
-  TileIter it{start, stop, p.sch.Vp};
+  TileIter it{start, stop, p.sch};
   int mt, v0, width;
   bool last;
   while (it.next(mt, v0, width, last)) {

@@ -7,7 +7,8 @@
 //           D[128 x width] (fp32, TMEM) += X_tile * W_tile^T, K = 16 per MMA.
 //           Two TMEM accumulators (2 x 256 columns = all 512) so the epilogue
 //           of tile t overlaps the MMAs of tile t+1.
-//   warps 2-9  epilogue, two groups of four warps (one warp per TMEM lane
+//   warps 2-3  idle (the control warpgroup 0-3 gives its registers away)
+//   warps 4-11 epilogue, two warpgroups of four warps (one warp per TMEM lane
 //           quadrant in each group; group g takes the 32-column chunks
 //           c = g, g+2, ... of every tile, so two warps per SM sub-partition
 //           hide each other's latency). Thread = hypothesis row. Per chunk:
@@ -41,7 +42,9 @@ constexpr int TC_A_BYTES = TC_BM * TC_BK * 2;   // 16 KB
 constexpr int TC_B_BYTES = TC_BN * TC_BK * 2;   // 32 KB
 constexpr int TC_EPI_GROUPS = 2;
 constexpr int TC_EPI_THREADS = TC_EPI_GROUPS * 128;
-constexpr int TC_THREADS = 64 + TC_EPI_THREADS;  // TMA warp + MMA warp + epilogue
+constexpr int TC_THREADS = 128 + TC_EPI_THREADS;  // control warpgroup + epilogue warpgroups
+constexpr int TC_CTRL_REGS = 56;                   // setmaxnreg budgets: 128*56 + 256*224 <= 64K
+constexpr int TC_EPI_REGS = 224;
 constexpr int TC_XS_BYTES = TC_EPI_GROUPS * 128 * 32 * 4;   // candidate scratch, 16 KB/group
 constexpr int TC_MS_BYTES = 128 * 2 * 4;                    // group-exchange (m, s)
 constexpr int TC_SMEM = TC_STAGES * (TC_A_BYTES + TC_B_BYTES) + TC_XS_BYTES + TC_MS_BYTES +
@@ -139,11 +142,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const long long start = (long long)blockIdx.x * p.sch.C;
   const long long stop = min(start + p.sch.C, p.sch.total);
 
+  if (warp < 4) {
+  reg_dealloc<TC_CTRL_REGS>();
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
     // The whole warp walks the schedule (keeps it converged); lane 0 issues.
     const uint64_t pol_x = policy_evict_last();     // X is re-read by every CTA
-    TileIter it{start, stop, p.sch.Vp};
+    TileIter it{start, stop, p.sch};
     int mt, v0, width;
     bool last;
     int stage = 0;
@@ -167,7 +172,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // ------------------------------------------------ MMA issuer
     // The whole warp waits; lane 0 issues tcgen05.mma and the commits (a
     // commit tracks the MMAs issued by the same thread).
-    TileIter it{start, stop, p.sch.Vp};
+    TileIter it{start, stop, p.sch};
     int mt, v0, width;
     bool last;
     int stage = 0;
@@ -201,9 +206,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+  }
   } else {
-    // ------------------------------------------------ epilogue (warps 2..9)
-    const int e = warp - 2;
+    reg_alloc<TC_EPI_REGS>();
+    // ------------------------------------------------ epilogue (warps 4..11)
+    const int e = warp - 4;
     const int grp = e >> 2;                        // 0 or 1: which chunks
     const int q = warp & 3;                        // TMEM lane quadrant of this warp
     const int row_local = q * 32 + lane;
@@ -212,12 +219,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     float* xs = xs_all + (grp * 128 + row_local) * 32;
     RowState<KB> st;
     st.reset();
-    TileIter it{start, stop, p.sch.Vp};
+    TileIter it{start, stop, p.sch};
     int mt, v0, width;
     bool last;
     int acc = 0;
     uint32_t acc_phase = 0;
-    uint32_t r[32];
+    uint32_t ra[32], rb[32];
     float ba[32], bn[32];
     while (it.next(mt, v0, width, last)) {
       const int row = mt * TC_BM + row_local;
@@ -228,17 +235,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tbase = tmem_base + t_lane + acc * TC_BN;
+      if (grp < nch) tmem_ld32(tbase + grp * 32, ra);
+      // software pipeline: TMEM + bias loads of chunk c+2 fly while c is consumed
       for (int c = grp; c < nch; c += 4) {
-        // chunk c with its bias in ba; the bias of chunk c+2 prefetched into bn
-        tmem_ld32(tbase + c * 32, r);
-        if (c + 2 < nch) load_bias32(p.bias, v0, (c + 2) * 32, limit, bn);
-        tmem_ld_wait(r);
-        consume_chunk<KB, MODE>(p, st, r, ba, row, v0, c * 32, limit, xs, sw);
+        tmem_ld_wait(ra);
+        if (c + 2 < nch) {
+          tmem_ld32(tbase + (c + 2) * 32, rb);
+          load_bias32(p.bias, v0, (c + 2) * 32, limit, bn);
+        }
+        consume_chunk<KB, MODE>(p, st, ra, ba, row, v0, c * 32, limit, xs, sw);
         if (c + 2 >= nch) break;
-        tmem_ld32(tbase + (c + 2) * 32, r);
-        if (c + 4 < nch) load_bias32(p.bias, v0, (c + 4) * 32, limit, ba);
-        tmem_ld_wait(r);
-        consume_chunk<KB, MODE>(p, st, r, bn, row, v0, (c + 2) * 32, limit, xs, sw);
+        tmem_ld_wait(rb);
+        if (c + 4 < nch) {
+          tmem_ld32(tbase + (c + 4) * 32, ra);
+          load_bias32(p.bias, v0, (c + 4) * 32, limit, ba);
+        }
+        consume_chunk<KB, MODE>(p, st, rb, bn, row, v0, (c + 2) * 32, limit, xs, sw);
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
