@@ -161,6 +161,12 @@ amun_status launch_tc(amun_ol* pl, const CUtensorMap* mx, const CUtensorMap* mw,
                       const TcParams& tp, int grid, cudaStream_t st, int mode) {
   void (*kern)(const CUtensorMap, const CUtensorMap, const TcParams) =
       mode == 0 ? ol_tc_kernel<KB, 0> : ol_tc_kernel<1, 1>;
+  // the warpgroup register hand-off needs the full launch pool (see TC_LAUNCH_REGS)
+  cudaFuncAttributes fa;
+  CUDA_TRY(cudaFuncGetAttributes(&fa, kern));
+  if (fa.numRegs < TC_LAUNCH_REGS)
+    return fail(AMUN_ECUDA, "fused kernel compiled with %d registers/thread, needs %d for its "
+                "setmaxnreg budget", fa.numRegs, TC_LAUNCH_REGS);
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM));
   kern<<<grid, TC_THREADS, TC_SMEM, st>>>(*mx, *mw, tp);
   CUDA_TRY(cudaGetLastError());

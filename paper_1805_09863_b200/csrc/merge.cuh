@@ -196,20 +196,25 @@ __global__ void __launch_bounds__(MG_WARPS * 32) merge_rows_kernel(const MergePa
 
 template <int KB>
 __global__ void __launch_bounds__(MG_WARPS * 32) merge_sentences_kernel(const MergeParams p) {
-  pdl_wait();
   const int s = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // inputs that do not come from the fused kernel are read before the
+  // programmatic-dependent-launch wait, so their latency overlaps its tail
   const int r0 = p.offsets[s], r1 = p.offsets[s + 1];
   const int ks = p.k_s ? min(p.k_s[s], p.k) : p.k;
+  float pc = 0.f;
+  if (r0 + warp < r1) pc = p.prev_cost[r0 + warp];
+  pdl_wait();
   CandList<KB> cl;
   cl.reset();
   for (int r = r0 + warp; r < r1; r += MG_WARPS) {
     float M, Z, l;
     int v;
     merge_row<KB>(p, r, lane, M, Z, l, v);
+    if (r != r0 + warp) pc = p.prev_cost[r];
     if (v >= 0) {
       const float lse = M + logf(Z);
-      cl.insert(Cand{p.prev_cost[r] + (l - lse), l, r, v});
+      cl.insert(Cand{pc + (l - lse), l, r, v});
     }
   }
   __shared__ Cand wbest[MG_WARPS];
@@ -235,7 +240,6 @@ __global__ void __launch_bounds__(MG_WARPS * 32) merge_sentences_kernel(const Me
     __syncthreads();
     const Cand w = winner;
     if (cl.c[0].r == w.r && cl.c[0].v == w.v) cl.pop();
-    __syncthreads();
   }
 }
 

@@ -43,8 +43,14 @@ constexpr int TC_B_BYTES = TC_BN * TC_BK * 2;   // 32 KB
 constexpr int TC_EPI_GROUPS = 2;
 constexpr int TC_EPI_THREADS = TC_EPI_GROUPS * 128;
 constexpr int TC_THREADS = 128 + TC_EPI_THREADS;  // control warpgroup + epilogue warpgroups
-constexpr int TC_CTRL_REGS = 56;                   // setmaxnreg budgets: 128*56 + 256*224 <= 64K
+// setmaxnreg budgets. They only redistribute the CTA's launch pool
+// (TC_LAUNCH_REGS per thread): a warpgroup can grow only into what the
+// others released, else setmaxnreg.inc blocks forever.
+constexpr int TC_LAUNCH_REGS = 65536 / TC_THREADS / 8 * 8;   // 168
+constexpr int TC_CTRL_REGS = 56;
 constexpr int TC_EPI_REGS = 224;
+static_assert(128 * TC_CTRL_REGS + TC_EPI_THREADS * TC_EPI_REGS <= TC_LAUNCH_REGS * TC_THREADS,
+              "setmaxnreg budget exceeds the launch register pool");
 constexpr int TC_XS_BYTES = TC_EPI_GROUPS * 128 * 32 * 4;   // candidate scratch, 16 KB/group
 constexpr int TC_MS_BYTES = 128 * 2 * 4;                    // group-exchange (m, s)
 constexpr int TC_SMEM = TC_STAGES * (TC_A_BYTES + TC_B_BYTES) + TC_XS_BYTES + TC_MS_BYTES +
