@@ -238,7 +238,7 @@ amun_status launch_merge(const MergeParams& mp, bool rows, int grid, cudaStream_
   // fused kernel still runs; it waits (griddepcontrol.wait) for its results.
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(MG_WARPS * 32);
+  cfg.blockDim = dim3(rows ? MG_WARPS * 32 : MS_WARPS * 32);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;

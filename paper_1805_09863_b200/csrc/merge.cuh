@@ -194,8 +194,27 @@ __global__ void __launch_bounds__(MG_WARPS * 32) merge_rows_kernel(const MergePa
   }
 }
 
+__device__ __forceinline__ Cand shfl_cand_idx(const Cand& c, int src) {
+  Cand o;
+  o.cost = __shfl_sync(0xffffffffu, c.cost, src);
+  o.l = __shfl_sync(0xffffffffu, c.l, src);
+  o.r = __shfl_sync(0xffffffffu, c.r, src);
+  o.v = __shfl_sync(0xffffffffu, c.v, src);
+  return o;
+}
+
+// Sentence phase. CTA = one sentence, warp w takes rows r0+w, r0+w+8, ...
+// Per row: lse from a warp max/sum over the row's partial records, then every
+// lane offers the (l, v) entries of its records, scored
+// cost = prev_cost[r] + (l - lse), to a lane-local sorted list. Each warp
+// extracts its top-KB (KB rounds of warp argmax) into shared memory; after ONE
+// barrier, warp 0 ranks the <= 8*KB survivors by counting better ones and
+// writes rank i to output slot i (ranks are unique: (r, v) pairs are).
+constexpr int MS_WARPS = 8;
+
 template <int KB>
-__global__ void __launch_bounds__(MG_WARPS * 32) merge_sentences_kernel(const MergeParams p) {
+__global__ void __launch_bounds__(MS_WARPS * 32) merge_sentences_kernel(const MergeParams p) {
+  __shared__ Cand pool[MS_WARPS * KB];
   const int s = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // inputs that do not come from the fused kernel are read before the
@@ -207,39 +226,76 @@ __global__ void __launch_bounds__(MG_WARPS * 32) merge_sentences_kernel(const Me
   pdl_wait();
   CandList<KB> cl;
   cl.reset();
-  for (int r = r0 + warp; r < r1; r += MG_WARPS) {
-    float M, Z, l;
-    int v;
-    merge_row<KB>(p, r, lane, M, Z, l, v);
+  for (int r = r0 + warp; r < r1; r += MS_WARPS) {
     if (r != r0 + warp) pc = p.prev_cost[r];
-    if (v >= 0) {
-      const float lse = M + logf(Z);
-      cl.insert(Cand{pc + (l - lse), l, r, v});
+    const float* base;
+    long long js;
+    int n;
+    row_splits(p, r, base, js, n);
+    float M = kNegInf;
+    for (int j = lane; j < n; j += 32) M = fmaxf(M, base[j * js]);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    float Z = 0.f;
+    for (int j = lane; j < n; j += 32) {
+      const float* rec = base + j * js;
+      const float mj = rec[0];
+      if (mj != kNegInf) Z += rec[1] * expf(mj - M);
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) Z += __shfl_xor_sync(0xffffffffu, Z, o);
+    const float lse = M + logf(Z);
+    for (int j = lane; j < n; j += 32) {
+      const float* rec = base + j * js;
+      for (int i = 0; i < p.k_max; ++i) {
+        const int vi = __float_as_int(rec[2 + p.k_max + i]);
+        if (vi < 0) break;
+        const float li = rec[2 + i];
+        const Cand c{pc + (li - lse), li, r, vi};
+        if (!better_cand(c, cl.c[KB - 1])) break;   // entries are sorted: the rest lose too
+        cl.insert(c);
+      }
     }
   }
-  __shared__ Cand wbest[MG_WARPS];
-  __shared__ Cand winner;
-  for (int i = 0; i < p.k; ++i) {
+  // warp top-KB -> shared pool
+  for (int i = 0; i < KB; ++i) {
     Cand b = cl.c[0];
+    int src = lane;
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) {
       const Cand t = shfl_cand(b, o);
-      if (better_cand(t, b)) b = t;
+      const int ts = __shfl_xor_sync(0xffffffffu, src, o);
+      if (better_cand(t, b) || (!better_cand(b, t) && ts < src)) {
+        b = t;
+        src = ts;
+      }
     }
-    if (lane == 0) wbest[warp] = b;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      Cand w = wbest[0];
-      for (int q = 1; q < MG_WARPS; ++q)
-        if (better_cand(wbest[q], w)) w = wbest[q];
-      winner = w;
-      const bool valid = (i < ks) && (w.v >= 0) && (w.v != 0x7fffffff);
-      p.out_idx[(long long)s * p.k + i] = valid ? (long long)w.r * p.V_total + w.v : -1LL;
-      p.out_cost[(long long)s * p.k + i] = valid ? w.cost : kNegInf;
+    if (lane == src) cl.pop();
+    if (lane == 0) pool[warp * KB + i] = b;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    constexpr int NP = MS_WARPS * KB;
+    int nvalid = 0;
+    for (int e = lane; e < NP; e += 32) {
+      const Cand c = pool[e];
+      const bool valid = (c.v >= 0) && (c.v != 0x7fffffff);
+      nvalid += valid;
+      if (!valid) continue;
+      int rank = 0;
+      for (int f = 0; f < NP; ++f) rank += better_cand(pool[f], c) ? 1 : 0;
+      if (rank < ks) {
+        p.out_idx[(long long)s * p.k + rank] = (long long)c.r * p.V_total + c.v;
+        p.out_cost[(long long)s * p.k + rank] = c.cost;
+      }
     }
-    __syncthreads();
-    const Cand w = winner;
-    if (cl.c[0].r == w.r && cl.c[0].v == w.v) cl.pop();
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) nvalid += __shfl_xor_sync(0xffffffffu, nvalid, o);
+    const int filled = min(ks, nvalid);
+    for (int i = filled + lane; i < p.k; i += 32) {
+      p.out_idx[(long long)s * p.k + i] = -1LL;
+      p.out_cost[(long long)s * p.k + i] = kNegInf;
+    }
   }
 }
 

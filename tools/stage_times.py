@@ -1,0 +1,76 @@
+"""Per-stage device times of the output-layer path (CUDA events, warm L2):
+fused kernel alone, select (merge) alone, both, and an empty-launch floor.
+  python tools/stage_times.py [config]"""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import synth  # noqa: E402
+import paper_1805_09863_b200 as amun  # noqa: E402
+
+
+def timeit(fn, iters=200, warm=20):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(iters):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / iters * 1e3
+
+
+def graph_time(fn, reps=20, iters=20):
+    """Pure device time per call: `reps` calls captured in one CUDA graph."""
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            for _ in range(reps):
+                fn()
+    torch.cuda.synchronize()
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(iters):
+        g.replay()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / (iters * reps) * 1e3
+
+
+def main():
+    name = sys.argv[1] if len(sys.argv) > 1 else "beam"
+    w = synth.CONFIGS[name]
+    dev = torch.device("cuda", 0)
+    X, W, b = synth.gen_X(w).to(dev), synth.gen_W(w).to(dev), synth.gen_b(w).to(dev)
+    pc, off = synth.gen_prev_cost(w).to(dev), synth.gen_offsets(w).to(dev)
+    ol = amun.OutputLayer(w.H, w.V, dtype=w.dtype, k_max=w.k, max_rows=w.N, max_sentences=w.S)
+    oi = torch.empty((w.S, w.k), dtype=torch.int64, device=dev)
+    oc = torch.empty((w.S, w.k), dtype=torch.float32, device=dev)
+    ol.scores(X, W, b)
+    t_sel = timeit(lambda: ol.select(w.N, pc, off, w.k, out_idx=oi, out_cost=oc))
+    t_sc = timeit(lambda: ol.scores(X, W, b), iters=50)
+    t_all = timeit(lambda: ol(X, W, b, pc, off, w.k, out_idx=oi, out_cost=oc), iters=50)
+    z = torch.empty(1, device=dev)
+    t_empty = timeit(lambda: z.add_(1.0))
+    print(f"{name}: scores {t_sc:.1f} us | select {t_sel:.1f} us | both {t_all:.1f} us | "
+          f"torch tiny-kernel launch {t_empty:.1f} us  (eager, host-launch bound)")
+    g_sel = graph_time(lambda: ol.select(w.N, pc, off, w.k, out_idx=oi, out_cost=oc))
+    g_sc = graph_time(lambda: ol.scores(X, W, b), reps=5)
+    g_all = graph_time(lambda: ol(X, W, b, pc, off, w.k, out_idx=oi, out_cost=oc), reps=5)
+    g_empty = graph_time(lambda: z.add_(1.0))
+    print(f"{name}: GRAPH scores {g_sc:.1f} us | select {g_sel:.1f} us | both {g_all:.1f} us | "
+          f"tiny kernel {g_empty:.1f} us")
+
+
+if __name__ == "__main__":
+    main()
