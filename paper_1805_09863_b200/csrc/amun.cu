@@ -92,6 +92,9 @@ struct amun_ol {
   amun_dtype dtype;
   int stride;
   size_t ws_bytes;
+  size_t slots_bytes;          // partial-record slots at the start of the workspace
+  const void* hint_ws = nullptr;   // workspace whose hint region is initialised
+  uint32_t gen = 0;                // launch generation of the hint words
   MapEntry xmaps[4];
   MapEntry wmaps[8];
   int xnext = 0, wnext = 0;
@@ -208,6 +211,19 @@ amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b
     tp.stride = pl->stride;
     tp.k_max = pl->k_max;
     tp.logits = logits;
+    tp.hint = reinterpret_cast<unsigned long long*>(static_cast<char*>(workspace) + pl->slots_bytes);
+    if (mode == 0) {
+      // hint words carry a generation tag; zero them once per workspace (and
+      // whenever the 32-bit generation would wrap)
+      if (pl->hint_ws != workspace || pl->gen == 0xffffffffu) {
+        CUDA_TRY(cudaMemsetAsync(tp.hint, 0, (size_t)pl->max_rows * 8, st));
+        pl->hint_ws = workspace;
+        pl->gen = 0;
+      }
+      tp.gen = ++pl->gen;
+    } else {
+      tp.gen = 0;
+    }
 #define TC_CALL(K) launch_tc<K>(pl, mx, mw, tp, grid, st, mode)
     AMUN_KB_SWITCH(mode == 1 ? 1 : pl->kb, TC_CALL)
 #undef TC_CALL
@@ -350,7 +366,8 @@ amun_status amun_ol_create(amun_ol** plan, int H, int V_local, int v_offset, int
   pl->num_sms = prop.multiProcessorCount;
   pl->stride = 2 + 2 * k_max;
   const long long slots = pl->num_sms + cdiv(max_rows > 0 ? max_rows : 1, 128) + 1;
-  pl->ws_bytes = (size_t)cdiv(slots * 128LL * pl->stride * 4, 256) * 256;
+  pl->slots_bytes = (size_t)cdiv(slots * 128LL * pl->stride * 4, 256) * 256;
+  pl->ws_bytes = pl->slots_bytes + (size_t)cdiv((long long)(max_rows > 0 ? max_rows : 1) * 8, 256) * 256;
   *plan = pl;
   return AMUN_OK;
 }

@@ -84,8 +84,12 @@ struct RowState {
   // Masked entries must already be -inf. `xs` is this thread's 32-float
   // shared-memory scratch row (128-byte aligned); its 16-byte chunks are
   // XOR-swizzled by `sw` (= row & 7) so a warp's stores are conflict-free.
+  // `hint` is a proven lower bound for the row's k-th best logit (k entries
+  // >= hint exist elsewhere in the row), so entries below it cannot be in
+  // the row's top-k and are not offered (-inf when unknown).
   // Must be called by all 32 lanes of the warp together (warp-uniform gate).
-  __device__ __forceinline__ void chunk32(const float (&x)[32], int vbase, float* xs, int sw) {
+  __device__ __forceinline__ void chunk32(const float (&x)[32], int vbase, float* xs, int sw,
+                                          float hint = kNegInf) {
     float t[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) t[j] = fmaxf(x[j], x[j + 16]);
@@ -114,8 +118,10 @@ struct RowState {
     // elements above the current k-th best can enter. The chunk max gates
     // the whole path; candidates are found with one bitmask and visited in
     // ascending j, each read back from shared memory.
+    // single-compare gate: x >= tg  <=>  x > l[KB-1] && x >= hint
     const float thr = l[KB - 1];
-    const bool need = cm > thr;
+    const float tg = (hint > thr) ? hint : nextafterf(thr, __int_as_float(0x7f800000));
+    const bool need = cm >= tg;
     if (__any_sync(0xffffffffu, need)) {
       if (need) {
         float4* xs4 = reinterpret_cast<float4*>(xs);
@@ -124,7 +130,7 @@ struct RowState {
           xs4[j ^ sw] = make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
         uint32_t mask = 0;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) mask |= (x[j] > thr) ? (1u << j) : 0u;
+        for (int j = 0; j < 32; ++j) mask |= (x[j] >= tg) ? (1u << j) : 0u;
         while (mask) {
           const int j = __ffs(mask) - 1;
           mask &= mask - 1;
@@ -163,6 +169,25 @@ struct RowState {
     }
   }
 };
+
+// Cross-CTA k-th-best hints: a per-row 64-bit word {generation, ordered float}
+// updated with atomicMax. Any CTA's local k-th best value is a lower bound on
+// the row's global k-th best, so every CTA may skip entries below the largest
+// one published so far. The generation tag makes stale words from earlier
+// launches read as "no hint" without a reset.
+__device__ __forceinline__ uint32_t f2o(float x) {
+  const uint32_t u = __float_as_uint(x);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float o2f(uint32_t o) {
+  return (o & 0x80000000u) ? __uint_as_float(o & 0x7fffffffu) : __uint_as_float(~o);
+}
+__device__ __forceinline__ float hint_decode(unsigned long long h, uint32_t gen) {
+  return ((uint32_t)(h >> 32) == gen) ? o2f((uint32_t)h) : kNegInf;
+}
+__device__ __forceinline__ unsigned long long hint_encode(float x, uint32_t gen) {
+  return ((unsigned long long)gen << 32) | f2o(x);
+}
 
 // Static persistent schedule shared by the fused kernels and the merge.
 // The flattened column space has one band of `band` columns per M-tile, of

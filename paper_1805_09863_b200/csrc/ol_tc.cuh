@@ -32,6 +32,8 @@ struct TcParams {
   float* __restrict__ part;   // [slots][128][stride]
   int stride, k_max;
   float* __restrict__ logits; // MODE 1: [N][V_local]
+  unsigned long long* __restrict__ hint;   // [N] cross-CTA k-th-best hints
+  uint32_t gen;                            // launch generation tag (>= 1)
 };
 
 constexpr int TC_BM = 128;
@@ -82,7 +84,7 @@ template <int KB, int MODE>
 __device__ __forceinline__ void consume_chunk(const TcParams& p, RowState<KB>& st,
                                               const uint32_t (&r)[32], const float (&bb)[32],
                                               int row, int v0, int c0, int limit, float* xs,
-                                              int sw) {
+                                              int sw, float hint) {
   const int nv = limit - c0;
   float x[32];
 #pragma unroll
@@ -93,7 +95,7 @@ __device__ __forceinline__ void consume_chunk(const TcParams& p, RowState<KB>& s
       for (int j = 0; j < 32 && j < nv; ++j) out[j] = x[j];
     }
   } else {
-    st.chunk32(x, p.v_offset + v0 + c0, xs, sw);
+    st.chunk32(x, p.v_offset + v0 + c0, xs, sw, hint);
   }
 }
 
@@ -232,10 +234,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     uint32_t acc_phase = 0;
     uint32_t ra[32], rb[32];
     float ba[32], bn[32];
+    float hintv = kNegInf, published = kNegInf;
     while (it.next(mt, v0, width, last)) {
       const int row = mt * TC_BM + row_local;
       const int limit = min(width, p.V_local - v0);
       const int nch = (width + 31) >> 5;
+      // newest cross-CTA hint for this row (L2, not L1: other SMs update it)
+      if (MODE == 0 && row < p.N) hintv = fmaxf(hintv, hint_decode(__ldcg(p.hint + row), p.gen));
       // bias of this group's first chunk requested before the accumulator wait
       if (grp < nch) load_bias32(p.bias, v0, grp * 32, limit, ba);
       mbar_wait(&tfull[acc], acc_phase);
@@ -249,18 +254,24 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           tmem_ld32(tbase + (c + 2) * 32, rb);
           load_bias32(p.bias, v0, (c + 2) * 32, limit, bn);
         }
-        consume_chunk<KB, MODE>(p, st, ra, ba, row, v0, c * 32, limit, xs, sw);
+        consume_chunk<KB, MODE>(p, st, ra, ba, row, v0, c * 32, limit, xs, sw, hintv);
         if (c + 2 >= nch) break;
         tmem_ld_wait(rb);
         if (c + 4 < nch) {
           tmem_ld32(tbase + (c + 4) * 32, ra);
           load_bias32(p.bias, v0, (c + 4) * 32, limit, ba);
         }
-        consume_chunk<KB, MODE>(p, st, rb, bn, row, v0, (c + 2) * 32, limit, xs, sw);
+        consume_chunk<KB, MODE>(p, st, rb, bn, row, v0, (c + 2) * 32, limit, xs, sw, hintv);
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
+      if (MODE == 0 && row < p.N && st.l[KB - 1] > published) {   // publish our k-th best
+        published = st.l[KB - 1];
+        atomicMax(p.hint + row, hint_encode(published, p.gen));
+      }
       if (last) {
+        hintv = kNegInf;   // next segment is a different M-tile (other rows)
+        published = kNegInf;
         if constexpr (MODE == 0) {
           // combine the two groups' states for this row, then emit
           if (grp == 1) {
