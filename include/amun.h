@@ -157,6 +157,14 @@ amun_status amun_merge_partials(amun_ol* plan, const float* partials, int G,
 amun_status amun_debug_logits(amun_ol* plan, const void* X, const void* W, const float* b, int N,
                               float* logits, void* workspace, void* stream);
 
+/* Benchmark hook (the analogue of the paper's Table 4 breakdown):
+ * the same fused kernel with part of the epilogue compiled out.
+ *   variant 2: bare GEMM, the epilogue only drains the TMEM accumulators;
+ *   variant 3: GEMM + bias + online max/sum-of-exp, no k-best.
+ * Results are meaningless scratch in `workspace`; bf16 plans only. */
+amun_status amun_bench_variant(amun_ol* plan, const void* X, const void* W, const float* b,
+                               int N, int variant, void* workspace, void* stream);
+
 /* Mini-batching (Alg. 2 "Remove h from b"): stable compaction.
  * One column = one per-hypothesis state array of N rows of row_bytes bytes:
  *   src  [N, row_bytes] device, dst [>= N', row_bytes] device (must not

@@ -156,6 +156,12 @@ class OutputLayer:
                                      _ptr(out_idx), _ptr(out_cost), _stream(self.device)))
         return out_idx, out_cost
 
+    def bench_variant(self, X, W, b, variant: int):
+        """Benchmark hook: 2 = bare GEMM, 3 = GEMM + bias + softmax stats (no k-best)."""
+        N = self._check_scores(X, W, b)
+        check(_L.amun_bench_variant(self._h, _ptr(X), _ptr(W), _ptr(b), N, variant,
+                                    _ptr(self.workspace), _stream(self.device)))
+
     def debug_logits(self, X, W, b):
         """Test hook: the biased logits [N, V_local] of the same GEMM."""
         N = self._check_scores(X, W, b)

@@ -163,7 +163,10 @@ template <int KB>
 amun_status launch_tc(amun_ol* pl, const CUtensorMap* mx, const CUtensorMap* mw,
                       const TcParams& tp, int grid, cudaStream_t st, int mode) {
   void (*kern)(const CUtensorMap, const CUtensorMap, const TcParams) =
-      mode == 0 ? ol_tc_kernel<KB, 0> : ol_tc_kernel<1, 1>;
+      mode == 0 ? ol_tc_kernel<KB, 0>
+      : mode == 2 ? ol_tc_kernel<KB, 2>
+      : mode == 3 ? ol_tc_kernel<KB, 3>
+                  : ol_tc_kernel<1, 1>;
   // the warpgroup register hand-off needs the full launch pool (see TC_LAUNCH_REGS)
   cudaFuncAttributes fa;
   CUDA_TRY(cudaFuncGetAttributes(&fa, kern));
@@ -479,6 +482,16 @@ amun_status amun_debug_logits(amun_ol* plan, const void* X, const void* W, const
   if (s != AMUN_OK) return s;
   if (N > 0 && !logits) return fail(AMUN_EINVAL, "NULL logits");
   return run_scores(plan, X, W, b, N, workspace, logits, static_cast<cudaStream_t>(stream), 1);
+}
+
+amun_status amun_bench_variant(amun_ol* plan, const void* X, const void* W, const float* b,
+                               int N, int variant, void* workspace, void* stream) {
+  amun_status s = check_score_args(plan, X, W, b, N, workspace);
+  if (s != AMUN_OK) return s;
+  if (variant != 2 && variant != 3) return fail(AMUN_EINVAL, "variant %d not in {2, 3}", variant);
+  if (plan->dtype != AMUN_BF16) return fail(AMUN_EUNSUPPORTED, "variants exist for bf16 only");
+  return run_scores(plan, X, W, b, N, workspace, nullptr, static_cast<cudaStream_t>(stream),
+                    variant);
 }
 
 amun_status amun_compact(const amun_column* cols, int n_cols, const uint8_t* alive, int N,

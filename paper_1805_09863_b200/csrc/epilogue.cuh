@@ -88,6 +88,7 @@ struct RowState {
   // >= hint exist elsewhere in the row), so entries below it cannot be in
   // the row's top-k and are not offered (-inf when unknown).
   // Must be called by all 32 lanes of the warp together (warp-uniform gate).
+  template <bool TOPK = true>
   __device__ __forceinline__ void chunk32(const float (&x)[32], int vbase, float* xs, int sw,
                                           float hint = kNegInf) {
     float t[16];
@@ -118,6 +119,7 @@ struct RowState {
     // elements above the current k-th best can enter. The chunk max gates
     // the whole path; candidates are found with one bitmask and visited in
     // ascending j, each read back from shared memory.
+    if constexpr (!TOPK) return;
     // single-compare gate: x >= tg  <=>  x > l[KB-1] && x >= hint
     const float thr = l[KB - 1];
     const float tg = (hint > thr) ? hint : nextafterf(thr, __int_as_float(0x7f800000));
@@ -219,7 +221,11 @@ struct TileIter {
       }
       v0 = (int)(pos - base);
       const long long seg_end = min(base + sch.Vp, end) - base;
+#ifdef TC_BN_OVERRIDE
+      width = (int)min((long long)TC_BN_OVERRIDE, seg_end - v0);
+#else
       width = (int)min(256LL, seg_end - v0);
+#endif
       last = (v0 + width == seg_end);
       pos += width;
       return true;

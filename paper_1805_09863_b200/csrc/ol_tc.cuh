@@ -20,6 +20,9 @@
 //           record {m, s, top-k} per (row, CTA range) is written (Alg. 6's
 //           per-shard state).
 // MODE 1 (test hook) writes the biased logits instead of statistics.
+// MODE 2 / 3 (benchmark hooks, the analogue of the paper's Table 4 split):
+// 2 = bare GEMM (the epilogue only drains TMEM), 3 = GEMM + bias + online
+// softmax statistics without the k-best.
 #pragma once
 #include "epilogue.cuh"
 
@@ -37,7 +40,11 @@ struct TcParams {
 };
 
 constexpr int TC_BM = 128;
+#ifndef TC_BN_OVERRIDE
 constexpr int TC_BN = 256;
+#else
+constexpr int TC_BN = TC_BN_OVERRIDE;
+#endif
 constexpr int TC_BK = 64;
 constexpr int TC_STAGES = 4;
 constexpr int TC_A_BYTES = TC_BM * TC_BK * 2;   // 16 KB
@@ -87,13 +94,25 @@ __device__ __forceinline__ void consume_chunk(const TcParams& p, RowState<KB>& s
                                               int sw, float hint) {
   const int nv = limit - c0;
   float x[32];
+  if (nv >= 32) {   // full chunk (all but the vocabulary tail): no masking
 #pragma unroll
-  for (int j = 0; j < 32; ++j) x[j] = (j < nv) ? __uint_as_float(r[j]) + bb[j] : kNegInf;
+    for (int j = 0; j < 32; ++j) x[j] = __uint_as_float(r[j]) + bb[j];
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = (j < nv) ? __uint_as_float(r[j]) + bb[j] : kNegInf;
+  }
   if constexpr (MODE == 1) {
     if (row < p.N) {
       float* out = p.logits + (long long)row * p.V_local + v0 + c0;
       for (int j = 0; j < 32 && j < nv; ++j) out[j] = x[j];
     }
+  } else if constexpr (MODE == 2) {
+    uint32_t acc = 0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) acc ^= r[j];
+    st.s += __uint_as_float(acc & 0x007fffffu);   // keep the loads alive
+  } else if constexpr (MODE == 3) {
+    st.template chunk32<false>(x, p.v_offset + v0 + c0, xs, sw, hint);
   } else {
     st.chunk32(x, p.v_offset + v0 + c0, xs, sw, hint);
   }
@@ -272,7 +291,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       if (last) {
         hintv = kNegInf;   // next segment is a different M-tile (other rows)
         published = kNegInf;
-        if constexpr (MODE == 0) {
+        if constexpr (MODE != 1) {
           // combine the two groups' states for this row, then emit
           if (grp == 1) {
 #pragma unroll

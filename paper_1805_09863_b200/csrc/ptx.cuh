@@ -66,9 +66,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P;\n"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1, %2;\n\t"
       "@!P bra WAIT_%=;\n\t}" ::"r"(addr),
-      "r"(parity)
+      "r"(parity), "r"(0x10000u)   // suspend-time hint (ns): sleep, do not spin
       : "memory");
 }
 #endif

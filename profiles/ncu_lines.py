@@ -32,13 +32,20 @@ for r in rows:
     for i, h in enumerate(hdr):
         if i < 4:
             continue
-        if h == "Warp Stall Sampling (All Samples)" or (h.startswith("stall_") and "Not Issued" not in h):
+        if h in ("Warp Stall Sampling (All Samples)", "Instructions Executed") or (
+                h.startswith("stall_") and "Not Issued" not in h):
             try:
                 agg[line][h] += float(r[i] or 0)
             except ValueError:
                 pass
 tot = sum(v["Warp Stall Sampling (All Samples)"] for v in agg.values())
-print(f"total samples {tot:.0f}")
+itot = sum(v["Instructions Executed"] for v in agg.values())
+print(f"total samples {tot:.0f}, warp-instructions {itot:.3g}")
+if "--inst" in sys.argv:
+    for ln, v in sorted(agg.items(), key=lambda kv: -kv[1]["Instructions Executed"])[:top]:
+        i = v["Instructions Executed"]
+        print(f"{i:11.0f} {100 * i / max(itot, 1):5.1f}% {ln[0]}:{ln[1]:<5} {src.get(ln, '')[:80]}")
+    sys.exit(0)
 for ln, v in sorted(agg.items(), key=lambda kv: -kv[1]["Warp Stall Sampling (All Samples)"])[:top]:
     s = v["Warp Stall Sampling (All Samples)"]
     reasons = sorted(((k, x) for k, x in v.items() if k.startswith("stall_")), key=lambda kv: -kv[1])[:3]

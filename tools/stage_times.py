@@ -68,6 +68,13 @@ def main():
     g_sc = graph_time(lambda: ol.scores(X, W, b), reps=5)
     g_all = graph_time(lambda: ol(X, W, b, pc, off, w.k, out_idx=oi, out_cost=oc), reps=5)
     g_empty = graph_time(lambda: z.add_(1.0))
+    g_v2 = graph_time(lambda: ol.bench_variant(X, W, b, 2), reps=5)
+    g_v3 = graph_time(lambda: ol.bench_variant(X, W, b, 3), reps=5)
+    Wt = W.t()
+    g_cublas = graph_time(lambda: torch.mm(X, Wt), reps=5)
+    print(f"{name}: GRAPH cuBLAS torch.mm bf16 (logits to HBM, no softmax/k-best) {g_cublas:.1f} us")
+    print(f"{name}: GRAPH bare GEMM {g_v2:.1f} us | GEMM+bias+softmax stats {g_v3:.1f} us | "
+          f"+k-best (full fused) {g_sc:.1f} us")
     print(f"{name}: GRAPH scores {g_sc:.1f} us | select {g_sel:.1f} us | both {g_all:.1f} us | "
           f"tiny kernel {g_empty:.1f} us")
 
