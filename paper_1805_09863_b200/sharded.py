@@ -30,9 +30,11 @@ def exchange(partial: torch.Tensor, world: int, group=None) -> torch.Tensor:
     if world == 1:
         return partial.unsqueeze(0)
     import torch.distributed as dist
-    out = torch.empty((world,) + tuple(partial.shape), dtype=partial.dtype, device=partial.device)
+    N = partial.shape[0]
+    out = torch.empty((world * N,) + tuple(partial.shape[1:]), dtype=partial.dtype,
+                      device=partial.device)
     dist.all_gather_into_tensor(out, partial.contiguous(), group=group)
-    return out
+    return out.view((world, N) + tuple(partial.shape[1:]))
 
 
 class ShardedOutputLayer:

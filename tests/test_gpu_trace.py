@@ -1,0 +1,57 @@
+"""Decode trace (Alg. 1 naive vs Alg. 2 dynamic mini-batching) on the GPU:
+every step's output layer matches the oracle, every compaction is bit-exact
+against the oracle's, and the work accounting matches the analytic count
+(S:321-322 style: dynamic rows = sum of per-hypothesis step counts)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import synth
+from tests.compare import compare_kbest
+
+pytestmark = pytest.mark.gpu
+
+
+def test_trace_dynamic_and_naive():
+    from paper_1805_09863_b200.trace import DecodeTrace
+    S, B, H, V = 24, 5, 128, 3000
+    w = synth.Workload("trace-small", H=H, V=V, S=S, B=B, k=B, seed=synth.BASE_SEED + 44)
+    X, W, b, pc = synth.gen_X(w), synth.gen_W(w), synth.gen_b(w), synth.gen_prev_cost(w)
+    f = synth.eos_schedule(w.seed, S, B, p=1 / 3, cap=6)          # short sentences
+    dev = torch.device("cuda", 0)
+    tr = DecodeTrace(H, V, S, B, device=dev)
+    Wd, bd = W.to(dev), b.to(dev)
+    Wo, bo = O.as_f64(W), O.as_f64(b)
+    seen = {"ol": 0, "compact": 0}
+
+    def check(t, inp, out):
+        if inp[0] == "compact":
+            _, src_cols, alive, off = inp
+            dst_cols, new_off, src_row, counts = out
+            ref = O.compact([c.view(torch.uint8).reshape(c.shape[0], -1).cpu().numpy()
+                             for c in src_cols], alive.cpu().numpy(), off.cpu().numpy())
+            rc, ro, rs, rn, rsa = ref
+            assert counts.cpu().tolist() == [rn, rsa]
+            assert np.array_equal(new_off.cpu().numpy(), ro)
+            assert np.array_equal(src_row.cpu().numpy(), rs)
+            for d, r in zip(dst_cols, rc):
+                assert np.array_equal(d.view(torch.uint8).reshape(d.shape[0], -1).cpu().numpy(), r)
+            seen["compact"] += 1
+            return
+        Xs, _, _, prev, off, k_s = inp
+        idx, cost = out
+        logp = O.log_softmax(O.add_bias(O.gemm(O.as_f64(Xs), Wo), bo))
+        prevd = O.as_f64(prev)
+        oi, _, oc64, nxt = O.kbest_sentences(logp, prevd, off.cpu().numpy(), B, k_s.cpu().numpy())
+        compare_kbest(idx.cpu().numpy(), cost.cpu().numpy(), lambda s, r, v: prevd[r] + logp[r, v],
+                      oc64, k_s.cpu().numpy(), "bf16", V, o_next=nxt)
+        seen["ol"] += 1
+
+    dyn = tr.run(X, Wd, bd, pc, f, mode="dynamic", check=check)
+    assert seen["ol"] == dyn.steps and seen["compact"] == dyn.steps
+    assert sum(dyn.rows) == int(f.sum())                     # Alg. 2 work accounting
+    assert dyn.rows == sorted(dyn.rows, reverse=True)        # the batch only shrinks
+    nai = tr.run(X, Wd, bd, pc, f, mode="naive")
+    assert sum(nai.rows) == int(f.max()) * S * B             # Alg. 1 decodes every slot
+    assert nai.steps == dyn.steps == int(f.max())
