@@ -117,7 +117,7 @@ class DecodeTrace:
             e[2].record()
             if mode == "dynamic":
                 alive = (fin[ids] > t + 1).to(torch.uint8)
-                compact(list(zip(cols, spare)), alive, offsets, new_off, src_row, counts,
+                compact([(c[:N], d) for c, d in zip(cols, spare)], alive, offsets, new_off, src_row, counts,
                         sync=False)                                       # Alg. 2 removal
                 e[3].record()
                 n2 = int(counts[0].item())                                # N' to the host

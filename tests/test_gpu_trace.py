@@ -25,18 +25,23 @@ def test_trace_dynamic_and_naive():
     Wo, bo = O.as_f64(W), O.as_f64(b)
     seen = {"ol": 0, "compact": 0}
 
+    def as_bytes(c):
+        rb = c.element_size()
+        for d in c.shape[1:]:
+            rb *= int(d)
+        return c.contiguous().view(torch.uint8).reshape(c.shape[0], rb).cpu().numpy()
+
     def check(t, inp, out):
         if inp[0] == "compact":
             _, src_cols, alive, off = inp
             dst_cols, new_off, src_row, counts = out
-            ref = O.compact([c.view(torch.uint8).reshape(c.shape[0], -1).cpu().numpy()
-                             for c in src_cols], alive.cpu().numpy(), off.cpu().numpy())
+            ref = O.compact([as_bytes(c) for c in src_cols], alive.cpu().numpy(), off.cpu().numpy())
             rc, ro, rs, rn, rsa = ref
             assert counts.cpu().tolist() == [rn, rsa]
             assert np.array_equal(new_off.cpu().numpy(), ro)
             assert np.array_equal(src_row.cpu().numpy(), rs)
             for d, r in zip(dst_cols, rc):
-                assert np.array_equal(d.view(torch.uint8).reshape(d.shape[0], -1).cpu().numpy(), r)
+                assert np.array_equal(as_bytes(d), r)
             seen["compact"] += 1
             return
         Xs, _, _, prev, off, k_s = inp
