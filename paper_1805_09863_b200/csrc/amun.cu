@@ -7,6 +7,7 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -17,6 +18,7 @@
 #include "merge.cuh"
 #include "ol_simt.cuh"
 #include "ol_tc.cuh"
+#include "ol_tc2.cuh"
 
 using namespace amun;
 
@@ -63,6 +65,7 @@ EncodeTiledFn get_encode_fn() {
 struct MapEntry {
   const void* ptr = nullptr;
   long long rows = -1;
+  int box_rows = 0;
   CUtensorMap map;
 };
 
@@ -95,6 +98,7 @@ struct amun_ol {
   size_t slots_bytes;          // partial-record slots at the start of the workspace
   const void* hint_ws = nullptr;   // workspace whose hint region is initialised
   uint32_t gen = 0;                // launch generation of the hint words
+  int pairs_mode = 0;   // env AMUN_PAIRS: 0 auto, 1 never ("off"), 2 always ("force"; tests)
   MapEntry xmaps[4];
   MapEntry wmaps[8];
   int xnext = 0, wnext = 0;
@@ -122,7 +126,7 @@ amun_status encode_map(amun_ol* pl, const void* ptr, long long rows, int box_row
 amun_status get_map(amun_ol* pl, MapEntry* cache, int n, int& next, const void* ptr,
                     long long rows, int box_rows, const CUtensorMap** out) {
   for (int i = 0; i < n; ++i)
-    if (cache[i].ptr == ptr && cache[i].rows == rows) {
+    if (cache[i].ptr == ptr && cache[i].rows == rows && cache[i].box_rows == box_rows) {
       *out = &cache[i].map;
       return AMUN_OK;
     }
@@ -135,14 +139,31 @@ amun_status get_map(amun_ol* pl, MapEntry* cache, int n, int& next, const void* 
   }
   e.ptr = ptr;
   e.rows = rows;
+  e.box_rows = box_rows;
   *out = &e.map;
   return AMUN_OK;
 }
 
+// CTA pairs (tcgen05 cta_group::2) for bf16 when the 128-row M-tiles pair up
+// with little padding: an even count, or >= 9 (<= 1/10 padded). A pair
+// computes 256 rows, so with an odd count one CTA of the last pair computes
+// padding; measured at 5 M-tiles (cfg "beam") the single-CTA kernel wins,
+// at 96 (cfg "shard") pairs are 1.35x faster under the power cap
+// (tools/power_probe.py).
+bool use_pairs(const amun_ol* pl, int N) {
+  if (pl->dtype != AMUN_BF16 || pl->pairs_mode == 1) return false;
+  const long long n_mt = cdiv(N > 0 ? N : 1, 128);
+  if (pl->pairs_mode == 2) return n_mt >= 2;
+  return n_mt >= 2 && (n_mt % 2 == 0 || n_mt >= 9);
+}
+
+// Schedule over "units" of M rows: 128-row M-tiles for single CTAs, 256-row
+// pair tiles for CTA pairs (then *grid counts CTAs = 2 x pairs).
 Schedule make_schedule(const amun_ol* pl, int N, int* grid) {
   Schedule s;
-  const long long G = pl->num_sms;
-  const long long n_mt = cdiv(N > 0 ? N : 1, 128);
+  const bool pairs = use_pairs(pl, N);
+  const long long G = pairs ? pl->num_sms / 2 : pl->num_sms;
+  const long long n_mt = cdiv(N > 0 ? N : 1, pairs ? 256 : 128);
   s.Vp = cdiv(pl->V_local, 16) * 16;
   const long long splits = G / n_mt;   // aligned mode: vocab splits per M-tile
   if (splits >= 1 && n_mt * splits * 10 >= G * 9) {
@@ -153,7 +174,8 @@ Schedule make_schedule(const amun_ol* pl, int N, int* grid) {
     s.band = s.Vp;
   }
   s.total = n_mt * s.band;
-  *grid = (int)cdiv((n_mt - 1) * s.band + s.Vp, s.C);
+  const int units = (int)cdiv((n_mt - 1) * s.band + s.Vp, s.C);
+  *grid = pairs ? 2 * units : units;
   return s;
 }
 
@@ -161,20 +183,27 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 
 
 template <int KB>
 amun_status launch_tc(amun_ol* pl, const CUtensorMap* mx, const CUtensorMap* mw,
-                      const TcParams& tp, int grid, cudaStream_t st, int mode) {
-  void (*kern)(const CUtensorMap, const CUtensorMap, const TcParams) =
-      mode == 0 ? ol_tc_kernel<KB, 0>
-      : mode == 2 ? ol_tc_kernel<KB, 2>
-      : mode == 3 ? ol_tc_kernel<KB, 3>
-                  : ol_tc_kernel<1, 1>;
+                      const TcParams& tp, int grid, cudaStream_t st, int mode, bool pairs) {
+  void (*kern)(const CUtensorMap, const CUtensorMap, const TcParams);
+  if (pairs)
+    kern = mode == 0 ? ol_tc2_kernel<KB, 0>
+         : mode == 2 ? ol_tc2_kernel<KB, 2>
+         : mode == 3 ? ol_tc2_kernel<KB, 3>
+                     : ol_tc2_kernel<1, 1>;
+  else
+    kern = mode == 0 ? ol_tc_kernel<KB, 0>
+         : mode == 2 ? ol_tc_kernel<KB, 2>
+         : mode == 3 ? ol_tc_kernel<KB, 3>
+                     : ol_tc_kernel<1, 1>;
+  const int smem_bytes = pairs ? TC2_SMEM : TC_SMEM;
   // the warpgroup register hand-off needs the full launch pool (see TC_LAUNCH_REGS)
   cudaFuncAttributes fa;
   CUDA_TRY(cudaFuncGetAttributes(&fa, kern));
   if (fa.numRegs < TC_LAUNCH_REGS)
     return fail(AMUN_ECUDA, "fused kernel compiled with %d registers/thread, needs %d for its "
                 "setmaxnreg budget", fa.numRegs, TC_LAUNCH_REGS);
-  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_SMEM));
-  kern<<<grid, TC_THREADS, TC_SMEM, st>>>(*mx, *mw, tp);
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
+  kern<<<grid, TC_THREADS, smem_bytes, st>>>(*mx, *mw, tp);
   CUDA_TRY(cudaGetLastError());
   return AMUN_OK;
 }
@@ -198,10 +227,11 @@ amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b
   int grid;
   Schedule sch = make_schedule(pl, N, &grid);
   if (pl->dtype == AMUN_BF16) {
+    const bool pairs = use_pairs(pl, N);
     const CUtensorMap *mx, *mw;
     amun_status s = get_map(pl, pl->xmaps, 4, pl->xnext, X, N, TC_BM, &mx);
     if (s != AMUN_OK) return s;
-    s = get_map(pl, pl->wmaps, 8, pl->wnext, W, pl->V_local, TC_BN, &mw);
+    s = get_map(pl, pl->wmaps, 8, pl->wnext, W, pl->V_local, pairs ? TC_BN / 2 : TC_BN, &mw);
     if (s != AMUN_OK) return s;
     TcParams tp;
     tp.N = N;
@@ -227,7 +257,7 @@ amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b
     } else {
       tp.gen = 0;
     }
-#define TC_CALL(K) launch_tc<K>(pl, mx, mw, tp, grid, st, mode)
+#define TC_CALL(K) launch_tc<K>(pl, mx, mw, tp, grid, st, mode, pairs)
     AMUN_KB_SWITCH(mode == 1 ? 1 : pl->kb, TC_CALL)
 #undef TC_CALL
   } else {
@@ -368,6 +398,10 @@ amun_status amun_ol_create(amun_ol** plan, int H, int V_local, int v_offset, int
   pl->device = device;
   pl->num_sms = prop.multiProcessorCount;
   pl->stride = 2 + 2 * k_max;
+  {
+    const char* e = getenv("AMUN_PAIRS");
+    pl->pairs_mode = !e ? 0 : (strcmp(e, "off") == 0 ? 1 : (strcmp(e, "force") == 0 ? 2 : 0));
+  }
   const long long slots = pl->num_sms + cdiv(max_rows > 0 ? max_rows : 1, 128) + 1;
   pl->slots_bytes = (size_t)cdiv(slots * 128LL * pl->stride * 4, 256) * 256;
   pl->ws_bytes = pl->slots_bytes + (size_t)cdiv((long long)(max_rows > 0 ? max_rows : 1) * 8, 256) * 256;
@@ -404,7 +438,7 @@ amun_status amun_ol_select(amun_ol* plan, const void* workspace, const float* pr
   MergeParams mp = base_merge(plan);
   int grid_unused;
   mp.part = static_cast<const float*>(workspace);
-  mp.layout = 0;
+  mp.layout = use_pairs(plan, N > 0 ? N : 1) ? 2 : 0;
   mp.sch = make_schedule(plan, N > 0 ? N : 1, &grid_unused);
   mp.N = N;
   mp.S = S;
@@ -443,7 +477,7 @@ amun_status amun_output_layer_partial(amun_ol* plan, const void* X, const void* 
   MergeParams mp = base_merge(plan);
   int grid_unused;
   mp.part = static_cast<const float*>(workspace);
-  mp.layout = 0;
+  mp.layout = use_pairs(plan, N) ? 2 : 0;
   mp.sch = make_schedule(plan, N, &grid_unused);
   mp.N = N;
   mp.out_part = partial;

@@ -20,7 +20,8 @@ namespace amun {
 
 struct MergeParams {
   // partial locator: layout 0 = fused-kernel slots [slot][128][stride] with
-  // the Schedule; layout 1 = external [G][N][stride]
+  // the Schedule; layout 2 = the same for CTA pairs; layout 1 = external
+  // [G][N][stride]
   const float* __restrict__ part;
   int stride, k_max, layout, G;
   Schedule sch;
@@ -42,6 +43,13 @@ __device__ __forceinline__ void row_splits(const MergeParams& p, int r, const fl
     const long long c0 = p.sch.first_cta(mt), c1 = p.sch.last_cta(mt);
     base = p.part + ((c0 + mt) * 128 + (r & 127)) * (long long)p.stride;
     jstride = 128LL * p.stride;
+    n = (int)(c1 - c0 + 1);
+  } else if (p.layout == 2) {
+    // CTA pairs: slot (pair + mp) * 2 + rank holds M-tile 2 mp + rank
+    const int mt = r >> 7, mp = mt >> 1, rk = mt & 1;
+    const long long c0 = p.sch.first_cta(mp), c1 = p.sch.last_cta(mp);
+    base = p.part + (((c0 + mp) * 2 + rk) * 128 + (r & 127)) * (long long)p.stride;
+    jstride = 2LL * 128 * p.stride;
     n = (int)(c1 - c0 + 1);
   } else {
     base = p.part + (long long)r * p.stride;

@@ -291,3 +291,24 @@ def test_invalid_k_rejected():
     b = torch.zeros(100, device=DEV)
     with pytest.raises(amun().AmunError):
         ol(X, W, b, torch.zeros(2, device=DEV), torch.tensor([0, 2], dtype=torch.int32, device=DEV), 3)
+
+
+# ------------------------------------------------------------------ CTA-pair kernel
+@pytest.mark.parametrize("N,V,H,k", [(300, 4099, 128, 5), (640, 9000, 256, 5), (130, 1000, 64, 3)])
+def test_pair_kernel_forced(N, V, H, k, monkeypatch):
+    """The tcgen05 cta_group::2 kernel on odd M-tile counts (a padded pair) and
+    small cases, forced with AMUN_PAIRS=force (read at plan creation)."""
+    monkeypatch.setenv("AMUN_PAIRS", "force")
+    S = N // 5 if N % 5 == 0 else N
+    B = N // S
+    w = synth.Workload("pairs", H=H, V=V, S=S, B=B, k=k, seed=synth.BASE_SEED + N)
+    run_case(w)
+    # integer regime bit-exact through the pair kernel
+    rng = np.random.default_rng(N)
+    X = torch.from_numpy(rng.integers(-8, 9, (N, H)).astype(np.float32)).to(torch.bfloat16)
+    W = torch.from_numpy(rng.integers(-8, 9, (V, H)).astype(np.float32)).to(torch.bfloat16)
+    b = torch.from_numpy(rng.integers(-4, 5, V).astype(np.float32))
+    ol = amun().OutputLayer(H, V, k_max=4, max_rows=N, max_sentences=N)
+    L = ol.debug_logits(X.to(DEV), W.to(DEV), b.to(DEV)).cpu().numpy()
+    ref = O.add_bias(O.gemm(O.as_f64(X), O.as_f64(W)), O.as_f64(b))
+    assert np.array_equal(L.astype(np.float64), ref)
