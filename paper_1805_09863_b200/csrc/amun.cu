@@ -96,8 +96,9 @@ struct amun_ol {
   int stride;
   size_t ws_bytes;
   size_t slots_bytes;          // partial-record slots at the start of the workspace
+  size_t hint_bytes;               // per-row hint words after the slots, then 2 x u32
+                                   // {generation, CTAs done} (device-side counters)
   const void* hint_ws = nullptr;   // workspace whose hint region is initialised
-  uint32_t gen = 0;                // launch generation of the hint words
   int pairs_mode = 0;   // env AMUN_PAIRS: 0 auto, 1 never ("off"), 2 always ("force"; tests)
   MapEntry xmaps[4];
   MapEntry wmaps[8];
@@ -245,17 +246,13 @@ amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b
     tp.k_max = pl->k_max;
     tp.logits = logits;
     tp.hint = reinterpret_cast<unsigned long long*>(static_cast<char*>(workspace) + pl->slots_bytes);
-    if (mode == 0) {
-      // hint words carry a generation tag; zero them once per workspace (and
-      // whenever the 32-bit generation would wrap)
-      if (pl->hint_ws != workspace || pl->gen == 0xffffffffu) {
-        CUDA_TRY(cudaMemsetAsync(tp.hint, 0, (size_t)pl->max_rows * 8, st));
-        pl->hint_ws = workspace;
-        pl->gen = 0;
-      }
-      tp.gen = ++pl->gen;
-    } else {
-      tp.gen = 0;
+    tp.gen_ctr = reinterpret_cast<unsigned int*>(static_cast<char*>(workspace) + pl->slots_bytes +
+                                                 pl->hint_bytes);
+    if (mode == 0 && pl->hint_ws != workspace) {
+      // hint words carry the launch generation (advanced on the device by the
+      // kernel itself); zero words + counters once per workspace
+      CUDA_TRY(cudaMemsetAsync(tp.hint, 0, pl->hint_bytes + 256, st));
+      pl->hint_ws = workspace;
     }
 #define TC_CALL(K) launch_tc<K>(pl, mx, mw, tp, grid, st, mode, pairs)
     AMUN_KB_SWITCH(mode == 1 ? 1 : pl->kb, TC_CALL)
@@ -404,7 +401,8 @@ amun_status amun_ol_create(amun_ol** plan, int H, int V_local, int v_offset, int
   }
   const long long slots = pl->num_sms + cdiv(max_rows > 0 ? max_rows : 1, 128) + 1;
   pl->slots_bytes = (size_t)cdiv(slots * 128LL * pl->stride * 4, 256) * 256;
-  pl->ws_bytes = pl->slots_bytes + (size_t)cdiv((long long)(max_rows > 0 ? max_rows : 1) * 8, 256) * 256;
+  pl->hint_bytes = (size_t)cdiv((long long)(max_rows > 0 ? max_rows : 1) * 8, 256) * 256;
+  pl->ws_bytes = pl->slots_bytes + pl->hint_bytes + 256;
   *plan = pl;
   return AMUN_OK;
 }

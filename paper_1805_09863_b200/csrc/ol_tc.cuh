@@ -36,8 +36,24 @@ struct TcParams {
   int stride, k_max;
   float* __restrict__ logits; // MODE 1: [N][V_local]
   unsigned long long* __restrict__ hint;   // [N] cross-CTA k-th-best hints
-  uint32_t gen;                            // launch generation tag (>= 1)
+  unsigned int* __restrict__ gen_ctr;      // {generation, CTAs done}: device-side, so every
+                                           // launch (graph replays too) gets a fresh tag
 };
+
+// Read the launch generation (all CTAs, before any of them finishes).
+__device__ __forceinline__ uint32_t read_generation(const unsigned int* gen_ctr) {
+  return 1u + *reinterpret_cast<const volatile unsigned int*>(gen_ctr);
+}
+// Called once per CTA after all its work: the last CTA advances the generation.
+__device__ __forceinline__ void finish_generation(unsigned int* gen_ctr) {
+  __threadfence();
+  const unsigned int prev = atomicAdd(gen_ctr + 1, 1u);
+  if (prev == gridDim.x - 1) {   // every CTA has read the generation and finished
+    gen_ctr[1] = 0u;
+    atomicAdd(gen_ctr, 1u);
+    __threadfence();
+  }
+}
 
 constexpr int TC_BM = 128;
 #ifndef TC_BN_OVERRIDE
@@ -139,6 +155,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint64_t* tfull = empty + TC_STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint32_t* gen_smem = tmem_holder + 1;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -155,6 +172,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_init(&tempty[i], TC_EPI_THREADS);
     }
     fence_barrier_init();
+    *gen_smem = (MODE == 0) ? read_generation(p.gen_ctr) : 0u;
   }
   if (warp == 1) {
     tmem_alloc(tmem_holder, 512);
@@ -164,6 +182,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  const uint32_t gen = *gen_smem;   // this launch's hint tag
   pdl_trigger();   // let the dependent merge grid get scheduled early (it waits for us)
 
   const long long start = (long long)blockIdx.x * p.sch.C;
@@ -259,7 +278,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int limit = min(width, p.V_local - v0);
       const int nch = (width + 31) >> 5;
       // newest cross-CTA hint for this row (L2, not L1: other SMs update it)
-      if (MODE == 0 && row < p.N) hintv = fmaxf(hintv, hint_decode(__ldcg(p.hint + row), p.gen));
+      if (MODE == 0 && row < p.N) hintv = fmaxf(hintv, hint_decode(__ldcg(p.hint + row), gen));
       // bias of this group's first chunk requested before the accumulator wait
       if (grp < nch) load_bias32(p.bias, v0, grp * 32, limit, ba);
       mbar_wait(&tfull[acc], acc_phase);
@@ -286,7 +305,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_arrive(&tempty[acc]);
       if (MODE == 0 && row < p.N && st.l[KB - 1] > published) {   // publish our k-th best
         published = st.l[KB - 1];
-        atomicMax(p.hint + row, hint_encode(published, p.gen));
+        atomicMax(p.hint + row, hint_encode(published, gen));
       }
       if (last) {
         hintv = kNegInf;   // next segment is a different M-tile (other rows)
@@ -333,6 +352,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_fence_after();
     tmem_dealloc(tmem_base, 512);
   }
+  if (MODE == 0 && threadIdx.x == 0) finish_generation(p.gen_ctr);
 }
 
 }  // namespace amun

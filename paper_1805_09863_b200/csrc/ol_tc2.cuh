@@ -44,6 +44,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
   uint64_t* tfull = empty + TC2_STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint32_t* gen_smem = tmem_holder + 1;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -62,6 +63,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       mbar_init(&tempty[i], 2 * TC2_EPI_WARPS);   // one arrival per epilogue warp of the pair
     }
     fence_barrier_init();
+    *gen_smem = (MODE == 0) ? read_generation(p.gen_ctr) : 0u;
   }
   if (warp == 1) {
     tmem_alloc_2sm(tmem_holder, 512);
@@ -71,6 +73,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
   cluster_sync();      // barriers of both CTAs initialised before any remote use
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  const uint32_t gen = *gen_smem;   // this launch's hint tag
   pdl_trigger();
 
   const long long start = (long long)pair * p.sch.C;
@@ -169,7 +172,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       const bool live = mt * TC_BM < p.N;            // warp-uniform: padding M-tile of a pair
       const int limit = min(width, p.V_local - v0);
       const int nch = (width + 31) >> 5;
-      if (MODE == 0 && row < p.N) hintv = fmaxf(hintv, hint_decode(__ldcg(p.hint + row), p.gen));
+      if (MODE == 0 && row < p.N) hintv = fmaxf(hintv, hint_decode(__ldcg(p.hint + row), gen));
       if (live && grp < nch) load_bias32(p.bias, v0, grp * 32, limit, ba);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
@@ -197,7 +200,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       if (lane == 0) mbar_arrive_cluster(tempty_leader[acc]);
       if (MODE == 0 && row < p.N && st.l[KB - 1] > published) {
         published = st.l[KB - 1];
-        atomicMax(p.hint + row, hint_encode(published, p.gen));
+        atomicMax(p.hint + row, hint_encode(published, gen));
       }
       if (last) {
         hintv = kNegInf;
@@ -244,6 +247,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     tc_fence_after();
     tmem_dealloc_2sm(tmem_base, 512);
   }
+  if (MODE == 0 && threadIdx.x == 0) finish_generation(p.gen_ctr);
 }
 
 }  // namespace amun

@@ -312,3 +312,41 @@ def test_pair_kernel_forced(N, V, H, k, monkeypatch):
     L = ol.debug_logits(X.to(DEV), W.to(DEV), b.to(DEV)).cpu().numpy()
     ref = O.add_bias(O.gemm(O.as_f64(X), O.as_f64(W)), O.as_f64(b))
     assert np.array_equal(L.astype(np.float64), ref)
+
+
+# ------------------------------------------------------------------ CUDA graphs
+@pytest.mark.parametrize("N", [640, 250])
+def test_graph_replay_with_new_inputs(N):
+    """The path is CUDA-graph capturable; each replay must see fresh cross-CTA
+    k-th-best hints (a device-side launch generation), so replaying the same
+    graph on NEW X contents stays exact."""
+    H, V, B, k = 256, 20000, 5, 5
+    S = N // B
+    dev = DEV
+    ol = amun().OutputLayer(H, V, k_max=k, max_rows=N, max_sentences=S)
+    base = synth.Workload("g", H=H, V=V, S=S, B=B, k=k, seed=synth.BASE_SEED + 500)
+    W, b = synth.gen_W(base).to(dev), synth.gen_b(base).to(dev)
+    pc, off = synth.gen_prev_cost(base).to(dev), synth.gen_offsets(base).to(dev)
+    Xbuf = torch.empty(N, H, dtype=torch.bfloat16, device=dev)
+    oi = torch.empty(S, k, dtype=torch.int64, device=dev)
+    oc = torch.empty(S, k, dtype=torch.float32, device=dev)
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        Xbuf.copy_(synth.gen_X(base).to(dev))
+        ol(Xbuf, W, b, pc, off, k, out_idx=oi, out_cost=oc)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            ol(Xbuf, W, b, pc, off, k, out_idx=oi, out_cost=oc)
+    Wo, bo = O.as_f64(synth.gen_W(base)), O.as_f64(synth.gen_b(base))
+    pcd = O.as_f64(synth.gen_prev_cost(base))
+    for rep in range(3):
+        w = synth.Workload("g", H=H, V=V, S=S, B=B, k=k, seed=synth.BASE_SEED + 600 + rep)
+        Xh = synth.gen_X(w)
+        Xbuf.copy_(Xh.to(dev))
+        g.replay()
+        torch.cuda.synchronize()
+        logp = O.log_softmax(O.add_bias(O.gemm(O.as_f64(Xh), Wo), bo))
+        _, _, oc64, nxt = O.kbest_sentences(logp, pcd, off.cpu().numpy(), k)
+        compare_kbest(oi.cpu().numpy(), oc.cpu().numpy(), lambda s, r, v: pcd[r] + logp[r, v],
+                      oc64, np.full(S, k), "bf16", V, o_next=nxt)
