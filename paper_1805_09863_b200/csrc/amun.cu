@@ -284,7 +284,7 @@ amun_status launch_merge(const MergeParams& mp, bool rows, int grid, cudaStream_
   // fused kernel still runs; it waits (griddepcontrol.wait) for its results.
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(rows ? MG_WARPS * 32 : MS_WARPS * 32);
+  cfg.blockDim = dim3(MS_WARPS * 32);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -479,7 +479,7 @@ amun_status amun_output_layer_partial(amun_ol* plan, const void* X, const void* 
   mp.sch = make_schedule(plan, N, &grid_unused);
   mp.N = N;
   mp.out_part = partial;
-  return run_merge(plan, mp, true, (int)cdiv(N, MG_WARPS), static_cast<cudaStream_t>(stream));
+  return run_merge(plan, mp, true, (int)cdiv(N, MS_WARPS), static_cast<cudaStream_t>(stream));
 }
 
 amun_status amun_merge_partials(amun_ol* plan, const float* partials, int G,

@@ -101,21 +101,34 @@ struct CandList {  // sorted by better_cand, capacity KB
   }
 };
 
-// Row phase for row r, executed by one full warp. Returns lse (all lanes);
-// lane i < k_max receives the i-th best (l, v) of the row in (ol, ov).
-// Lane j takes record j (already sorted by the producer, so it IS the lane's
-// list); records j + 32, j + 64, ... (only with > 32 splits) are inserted.
+// ---------------------------------------------------------------- row phase v3
+// 64-bit sort key of a row entry: ordered logit in the high word, inverted
+// token id in the low word, so a plain max picks (l desc, v asc); 0 = empty.
+__device__ __forceinline__ unsigned long long lv_key(float l, int v) {
+  return v < 0 ? 0ull : (((unsigned long long)f2o(l) << 32) | (uint32_t)(0x7fffffff - v));
+}
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long x) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {
+    const unsigned long long y = __shfl_xor_sync(0xffffffffu, x, o);
+    x = y > x ? y : x;
+  }
+  return x;
+}
+
+// Row r, one full warp: lse_r = M + log Z over the row's partial records and
+// the row's top-k_max (l, v). Lane i < k_max receives entry i (v = -1 if none).
 template <int KB>
-__device__ __forceinline__ void merge_row(const MergeParams& p, int r, int lane, float& M_out,
-                                          float& Z_out, float& ol, int& ov) {
+__device__ __forceinline__ void row_topk(const MergeParams& p, int r, int lane, float& lse,
+                                         float& M_out, float& Z_out, float& ol, int& ov) {
   const float* base;
   long long js;
   int n;
   row_splits(p, r, base, js, n);
-  RowState<KB> lst;
+  RowState<KB> lst;      // lane-local sorted list (l desc, v asc)
   lst.reset();
   float m0 = kNegInf, s0 = 0.f;
-  if (lane < n) {
+  if (lane < n) {        // record `lane` is already sorted: it is the lane's list
     const float* rec = base + lane * js;
     m0 = rec[0];
     s0 = rec[1];
@@ -128,13 +141,15 @@ __device__ __forceinline__ void merge_row(const MergeParams& p, int r, int lane,
     }
   }
   float M = m0;
-  for (int j = lane + 32; j < n; j += 32) {
+  for (int j = lane + 32; j < n; j += 32) {   // > 32 records: fold the extra ones in
     const float* rec = base + j * js;
     M = fmaxf(M, rec[0]);
     for (int i = 0; i < p.k_max; ++i) {
-      const float li = rec[2 + i];
       const int vi = __float_as_int(rec[2 + p.k_max + i]);
-      if (vi >= 0 && better_lv(li, vi, lst.l[KB - 1], lst.v[KB - 1])) lst.insert(li, vi);
+      if (vi < 0) break;
+      const float li = rec[2 + i];
+      if (!better_lv(li, vi, lst.l[KB - 1], lst.v[KB - 1])) break;
+      lst.insert(li, vi);
     }
   }
 #pragma unroll
@@ -149,22 +164,14 @@ __device__ __forceinline__ void merge_row(const MergeParams& p, int r, int lane,
   for (int o = 16; o >= 1; o >>= 1) Z += __shfl_xor_sync(0xffffffffu, Z, o);
   M_out = M;
   Z_out = Z;
+  lse = M + logf(Z);
   ol = kNegInf;
   ov = -1;
   for (int i = 0; i < p.k_max; ++i) {
-    float bl = lst.l[0];
-    int bv = lst.v[0];
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-      const float tl = __shfl_xor_sync(0xffffffffu, bl, o);
-      const int tv = __shfl_xor_sync(0xffffffffu, bv, o);
-      if (tv >= 0 && (bv < 0 || better_lv(tl, tv, bl, bv))) {
-        bl = tl;
-        bv = tv;
-      }
-    }
-    if (bv < 0) break;  // warp-uniform: no more candidates
-    if (lst.v[0] == bv) {  // owner pops (token ids are unique within a row)
+    const unsigned long long head = lv_key(lst.l[0], lst.v[0]);
+    const unsigned long long best = warp_max_u64(head);
+    if (best == 0ull) break;                  // warp-uniform: no more entries
+    if (head == best) {                       // unique (token ids are unique in a row)
 #pragma unroll
       for (int t = 0; t + 1 < KB; ++t) {
         lst.l[t] = lst.l[t + 1];
@@ -173,24 +180,25 @@ __device__ __forceinline__ void merge_row(const MergeParams& p, int r, int lane,
       lst.l[KB - 1] = kNegInf;
       lst.v[KB - 1] = -1;
     }
-    if (lane == i) {
-      ol = bl;
-      ov = bv;
+    if (lane == i) {                          // the key carries the winner exactly
+      ov = 0x7fffffff - (int)(uint32_t)best;
+      ol = o2f((uint32_t)(best >> 32));
     }
   }
 }
 
-constexpr int MG_WARPS = 8;
+constexpr int MS_WARPS = 8;
+constexpr int MS_CAP = 256;   // candidates ranked per batch of rows
 
 template <int KB>
-__global__ void __launch_bounds__(MG_WARPS * 32) merge_rows_kernel(const MergeParams p) {
+__global__ void __launch_bounds__(MS_WARPS * 32) merge_rows_kernel(const MergeParams p) {
   pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r = blockIdx.x * MG_WARPS + warp;
+  const int r = blockIdx.x * MS_WARPS + warp;
   if (r >= p.N) return;
-  float M, Z, l;
+  float lse, M, Z, l;
   int v;
-  merge_row<KB>(p, r, lane, M, Z, l, v);
+  row_topk<KB>(p, r, lane, lse, M, Z, l, v);
   float* rec = p.out_part + (long long)r * p.stride;
   if (lane == 0) {
     rec[0] = M;
@@ -202,108 +210,64 @@ __global__ void __launch_bounds__(MG_WARPS * 32) merge_rows_kernel(const MergePa
   }
 }
 
-__device__ __forceinline__ Cand shfl_cand_idx(const Cand& c, int src) {
-  Cand o;
-  o.cost = __shfl_sync(0xffffffffu, c.cost, src);
-  o.l = __shfl_sync(0xffffffffu, c.l, src);
-  o.r = __shfl_sync(0xffffffffu, c.r, src);
-  o.v = __shfl_sync(0xffffffffu, c.v, src);
-  return o;
-}
-
-// Sentence phase. CTA = one sentence, warp w takes rows r0+w, r0+w+8, ...
-// Per row: lse from a warp max/sum over the row's partial records, then every
-// lane offers the (l, v) entries of its records, scored
-// cost = prev_cost[r] + (l - lse), to a lane-local sorted list. Each warp
-// extracts its top-KB (KB rounds of warp argmax) into shared memory; after ONE
-// barrier, warp 0 ranks the <= 8*KB survivors by counting better ones and
-// writes rank i to output slot i (ranks are unique: (r, v) pairs are).
-constexpr int MS_WARPS = 8;
-
+// Sentence phase. CTA = one sentence. Warps take rows; each row's top-k_max
+// (already scored cost = prev_cost + l - lse: only the winners are
+// normalised) goes to shared memory; the carried best-k plus a batch of
+// rows' candidates are ranked by counting better ones (ranks are unique), and
+// the best k stay at the front for the next batch.
 template <int KB>
 __global__ void __launch_bounds__(MS_WARPS * 32) merge_sentences_kernel(const MergeParams p) {
-  __shared__ Cand pool[MS_WARPS * KB];
+  __shared__ Cand pool[KB + MS_CAP];
+  __shared__ Cand best[KB];
+  __shared__ int s_valid;
   const int s = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // inputs that do not come from the fused kernel are read before the
-  // programmatic-dependent-launch wait, so their latency overlaps its tail
   const int r0 = p.offsets[s], r1 = p.offsets[s + 1];
   const int ks = p.k_s ? min(p.k_s[s], p.k) : p.k;
   float pc = 0.f;
-  if (r0 + warp < r1) pc = p.prev_cost[r0 + warp];
+  if (r0 + warp < r1) pc = p.prev_cost[r0 + warp];   // before the PDL wait
   pdl_wait();
-  CandList<KB> cl;
-  cl.reset();
-  for (int r = r0 + warp; r < r1; r += MS_WARPS) {
-    if (r != r0 + warp) pc = p.prev_cost[r];
-    const float* base;
-    long long js;
-    int n;
-    row_splits(p, r, base, js, n);
-    float M = kNegInf;
-    for (int j = lane; j < n; j += 32) M = fmaxf(M, base[j * js]);
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-    float Z = 0.f;
-    for (int j = lane; j < n; j += 32) {
-      const float* rec = base + j * js;
-      const float mj = rec[0];
-      if (mj != kNegInf) Z += rec[1] * expf(mj - M);
-    }
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) Z += __shfl_xor_sync(0xffffffffu, Z, o);
-    const float lse = M + logf(Z);
-    for (int j = lane; j < n; j += 32) {
-      const float* rec = base + j * js;
-      for (int i = 0; i < p.k_max; ++i) {
-        const int vi = __float_as_int(rec[2 + p.k_max + i]);
-        if (vi < 0) break;
-        const float li = rec[2 + i];
-        const Cand c{pc + (li - lse), li, r, vi};
-        if (!better_cand(c, cl.c[KB - 1])) break;   // entries are sorted: the rest lose too
-        cl.insert(c);
+  const int nrows = r1 - r0;
+  const int rows_per_batch = max(1, MS_CAP / p.k_max);
+  int keep = 0;
+  for (int rb = 0; rb < nrows || (rb == 0 && nrows == 0); rb += rows_per_batch) {
+    const int re = min(nrows, rb + rows_per_batch);
+    for (int rr = rb + warp; rr < re; rr += MS_WARPS) {
+      const int r = r0 + rr;
+      if (rr != warp) pc = p.prev_cost[r];
+      float lse, M, Z, l;
+      int v;
+      row_topk<KB>(p, r, lane, lse, M, Z, l, v);
+      if (lane < p.k_max) {
+        Cand c = (v >= 0) ? Cand{pc + (l - lse), l, r, v}
+                          : Cand{kNegInf, kNegInf, 0x7fffffff, 0x7fffffff};
+        pool[keep + (rr - rb) * p.k_max + lane] = c;
       }
     }
-  }
-  // warp top-KB -> shared pool
-  for (int i = 0; i < KB; ++i) {
-    Cand b = cl.c[0];
-    int src = lane;
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-      const Cand t = shfl_cand(b, o);
-      const int ts = __shfl_xor_sync(0xffffffffu, src, o);
-      if (better_cand(t, b) || (!better_cand(b, t) && ts < src)) {
-        b = t;
-        src = ts;
-      }
-    }
-    if (lane == src) cl.pop();
-    if (lane == 0) pool[warp * KB + i] = b;
-  }
-  __syncthreads();
-  if (warp == 0) {
-    constexpr int NP = MS_WARPS * KB;
-    int nvalid = 0;
-    for (int e = lane; e < NP; e += 32) {
+    if (threadIdx.x == 0) s_valid = 0;
+    __syncthreads();
+    const int n = keep + (re - rb) * p.k_max;
+    int valid = 0;
+    for (int e = threadIdx.x; e < n; e += MS_WARPS * 32) {
       const Cand c = pool[e];
-      const bool valid = (c.v >= 0) && (c.v != 0x7fffffff);
-      nvalid += valid;
-      if (!valid) continue;
+      if (c.v == 0x7fffffff) continue;
+      ++valid;
       int rank = 0;
-      for (int f = 0; f < NP; ++f) rank += better_cand(pool[f], c) ? 1 : 0;
-      if (rank < ks) {
-        p.out_idx[(long long)s * p.k + rank] = (long long)c.r * p.V_total + c.v;
-        p.out_cost[(long long)s * p.k + rank] = c.cost;
-      }
+      for (int f = 0; f < n; ++f) rank += better_cand(pool[f], c) ? 1 : 0;
+      if (rank < p.k) best[rank] = c;
     }
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) nvalid += __shfl_xor_sync(0xffffffffu, nvalid, o);
-    const int filled = min(ks, nvalid);
-    for (int i = filled + lane; i < p.k; i += 32) {
-      p.out_idx[(long long)s * p.k + i] = -1LL;
-      p.out_cost[(long long)s * p.k + i] = kNegInf;
-    }
+    if (valid) atomicAdd(&s_valid, valid);
+    __syncthreads();
+    keep = min(s_valid, p.k);
+    if (threadIdx.x < keep) pool[threadIdx.x] = best[threadIdx.x];
+    __syncthreads();
+    if (nrows == 0) break;
+  }
+  if (threadIdx.x < p.k) {
+    const int i = threadIdx.x;
+    const bool ok = i < keep && i < ks;
+    p.out_idx[(long long)s * p.k + i] = ok ? (long long)pool[i].r * p.V_total + pool[i].v : -1LL;
+    p.out_cost[(long long)s * p.k + i] = ok ? pool[i].cost : kNegInf;
   }
 }
 
