@@ -91,13 +91,16 @@ struct RowState {
   template <bool TOPK = true>
   __device__ __forceinline__ void chunk32(const float (&x)[32], int vbase, float* xs, int sw,
                                           float hint = kNegInf) {
+    // max tree; g[j] = max(x[j], x[j+8], x[j+16], x[j+24]) (the group maxima)
     float t[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) t[j] = fmaxf(x[j], x[j + 16]);
+    float g[8];
 #pragma unroll
-    for (int w = 8; w >= 1; w >>= 1)
+    for (int j = 0; j < 8; ++j) g[j] = fmaxf(t[j], t[j + 8]);
 #pragma unroll
-      for (int j = 0; j < w; ++j) t[j] = fmaxf(t[j], t[j + w]);
+    for (int j = 0; j < 4; ++j) t[j] = fmaxf(g[j], g[j + 4]);
+    t[0] = fmaxf(fmaxf(t[0], t[2]), fmaxf(t[1], t[3]));
     const float cm = t[0];
     if (cm != kNegInf) {        // whole chunk masked: nothing to add (guards -inf - -inf)
       if (cm > m) {             // Alg. 4: new max -> rescale the sum by e^{Delta}
@@ -122,7 +125,28 @@ struct RowState {
     if constexpr (!TOPK) return;
     // single-compare gate: x >= tg  <=>  x > l[KB-1] && x >= hint
     const float thr = l[KB - 1];
-    const float tg = (hint > thr) ? hint : nextafterf(thr, __int_as_float(0x7f800000));
+    float tg = (hint > thr) ? hint : nextafterf(thr, __int_as_float(0x7f800000));
+    if constexpr (KB <= 8) {
+      // list still filling (start of a CTA range): the KB-th largest group
+      // maximum is a lower bound on the chunk's KB-th best (KB distinct
+      // elements reach it), so nothing below it can enter the row's top-KB
+      if (__any_sync(0xffffffffu, thr == kNegInf)) {
+        float q[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) q[j] = g[j];
+        // sorting network for 8 (19 comparators), descending
+#define AMUN_CS(a, b) { const float hi = fmaxf(q[a], q[b]); q[b] = fminf(q[a], q[b]); q[a] = hi; }
+        AMUN_CS(0, 1) AMUN_CS(2, 3) AMUN_CS(4, 5) AMUN_CS(6, 7)
+        AMUN_CS(0, 2) AMUN_CS(1, 3) AMUN_CS(4, 6) AMUN_CS(5, 7)
+        AMUN_CS(1, 2) AMUN_CS(5, 6) AMUN_CS(0, 4) AMUN_CS(3, 7)
+        AMUN_CS(1, 5) AMUN_CS(2, 6)
+        AMUN_CS(1, 4) AMUN_CS(3, 6)
+        AMUN_CS(2, 4) AMUN_CS(3, 5)
+        AMUN_CS(3, 4)
+#undef AMUN_CS
+        if (q[KB - 1] > tg) tg = q[KB - 1];
+      }
+    }
     const bool need = cm >= tg;
     if (__any_sync(0xffffffffu, need)) {
       if (need) {
