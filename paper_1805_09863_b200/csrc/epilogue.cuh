@@ -150,17 +150,25 @@ struct RowState {
     const bool need = cm >= tg;
     if (__any_sync(0xffffffffu, need)) {
       if (need) {
+        // stage the chunk group-transposed: slot j holds (x[j], x[j+8], x[j+16],
+        // x[j+24]), 16-byte slots XOR-swizzled by `sw`
         float4* xs4 = reinterpret_cast<float4*>(xs);
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          xs4[j ^ sw] = make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
+        for (int j = 0; j < 8; ++j) xs4[j ^ sw] = make_float4(x[j], x[j + 8], x[j + 16], x[j + 24]);
+        // candidate groups first (8 compares), then only their 4 values
         uint32_t mask = 0;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) mask |= (x[j] >= tg) ? (1u << j) : 0u;
-        while (mask) {
+        for (int j = 0; j < 8; ++j) {
+          if (g[j] >= tg) {
+            const float4 q = xs4[j ^ sw];
+            mask |= (q.x >= tg ? (1u << j) : 0u) | (q.y >= tg ? (1u << (j + 8)) : 0u) |
+                    (q.z >= tg ? (1u << (j + 16)) : 0u) | (q.w >= tg ? (1u << (j + 24)) : 0u);
+          }
+        }
+        while (mask) {   // ascending token id, so ties keep the earlier entries ahead
           const int j = __ffs(mask) - 1;
           mask &= mask - 1;
-          const float xv = xs[(((j >> 2) ^ sw) << 2) | (j & 3)];
+          const float xv = xs[(((j & 7) ^ sw) << 2) | (j >> 3)];
           if (xv > l[KB - 1]) insert_new(xv, vbase + j);
         }
       }
