@@ -108,15 +108,16 @@ struct RowState {
         m = cm;
       }
       const float ms = m * kLog2e;
-      float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+      // 8 independent chains so MUFU latency overlaps (one warp per SMSP
+      // per group cannot hide it with other warps alone)
+      float a[8];
 #pragma unroll
-      for (int j = 0; j < 32; j += 4) {
-        a0 += ex2(fmaf(x[j + 0], kLog2e, -ms));
-        a1 += ex2(fmaf(x[j + 1], kLog2e, -ms));
-        a2 += ex2(fmaf(x[j + 2], kLog2e, -ms));
-        a3 += ex2(fmaf(x[j + 3], kLog2e, -ms));
-      }
-      s += (a0 + a1) + (a2 + a3);
+      for (int u = 0; u < 8; ++u) a[u] = ex2(fmaf(x[u], kLog2e, -ms));
+#pragma unroll
+      for (int j = 8; j < 32; j += 8)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a[u] += ex2(fmaf(x[j + u], kLog2e, -ms));
+      s += ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
     }
     // k-best (Alg. 4 "if p' > max ... best <- i", generalised to k): only
     // elements above the current k-th best can enter. The chunk max gates

@@ -62,7 +62,11 @@ constexpr int TC_BN = 256;
 constexpr int TC_BN = TC_BN_OVERRIDE;
 #endif
 constexpr int TC_BK = 64;
+#ifdef TC_STAGES_OVERRIDE
+constexpr int TC_STAGES = TC_STAGES_OVERRIDE;
+#else
 constexpr int TC_STAGES = 4;
+#endif
 constexpr int TC_A_BYTES = TC_BM * TC_BK * 2;   // 16 KB
 constexpr int TC_B_BYTES = TC_BN * TC_BK * 2;   // 32 KB
 constexpr int TC_EPI_GROUPS = 2;

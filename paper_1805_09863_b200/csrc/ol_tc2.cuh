@@ -20,7 +20,11 @@
 
 namespace amun {
 
+#ifdef TC2_STAGES_OVERRIDE
+constexpr int TC2_STAGES = TC2_STAGES_OVERRIDE;
+#else
 constexpr int TC2_STAGES = 6;
+#endif
 constexpr int TC2_A_BYTES = TC_BM * TC_BK * 2;          // 16 KB: this CTA's 128 rows of X
 constexpr int TC2_B_BYTES = (TC_BN / 2) * TC_BK * 2;    // 16 KB: this CTA's half of the W tile
 constexpr int TC2_SMEM = TC2_STAGES * (TC2_A_BYTES + TC2_B_BYTES) + TC_XS_BYTES + TC_MS_BYTES +

@@ -50,6 +50,10 @@ def graph_time(fn, reps=20, iters=20):
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "beam"
     w = synth.CONFIGS[name]
+    if os.environ.get("AMUN_SENTENCES"):   # same config with another batch size
+        import dataclasses
+        w = dataclasses.replace(w, S=int(os.environ["AMUN_SENTENCES"]))
+        name = f"{name}(S={w.S})"
     dev = torch.device("cuda", 0)
     X, W, b = synth.gen_X(w).to(dev), synth.gen_W(w).to(dev), synth.gen_b(w).to(dev)
     pc, off = synth.gen_prev_cost(w).to(dev), synth.gen_offsets(w).to(dev)
