@@ -282,7 +282,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int limit = min(width, p.V_local - v0);
       const int nch = (width + 31) >> 5;
       // newest cross-CTA hint for this row (L2, not L1: other SMs update it)
-      if (MODE == 0 && row < p.N) hintv = fmaxf(hintv, hint_decode(__ldcg(p.hint + row), gen));
       // bias of this group's first chunk requested before the accumulator wait
       if (grp < nch) load_bias32(p.bias, v0, grp * 32, limit, ba);
       mbar_wait(&tfull[acc], acc_phase);
@@ -307,9 +306,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
-      if (MODE == 0 && row < p.N && st.l[KB - 1] > published) {   // publish our k-th best
-        published = st.l[KB - 1];
-        atomicMax(p.hint + row, hint_encode(published, gen));
+      if (MODE == 0 && row < p.N) {
+        if (st.l[KB - 1] > published) {   // publish our k-th best
+          published = st.l[KB - 1];
+          atomicMax(p.hint + row, hint_encode(published, gen));
+        }
+        // newest cross-CTA hint for the next tile (L2, not L1: other SMs
+        // update it); its latency overlaps the next accumulator wait
+        hintv = fmaxf(hintv, hint_decode(__ldcg(p.hint + row), gen));
       }
       if (last) {
         hintv = kNegInf;   // next segment is a different M-tile (other rows)

@@ -176,7 +176,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       const bool live = mt * TC_BM < p.N;            // warp-uniform: padding M-tile of a pair
       const int limit = min(width, p.V_local - v0);
       const int nch = (width + 31) >> 5;
-      if (MODE == 0 && row < p.N) hintv = fmaxf(hintv, hint_decode(__ldcg(p.hint + row), gen));
       if (live && grp < nch) load_bias32(p.bias, v0, grp * 32, limit, ba);
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
@@ -202,9 +201,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(tempty_leader[acc]);
-      if (MODE == 0 && row < p.N && st.l[KB - 1] > published) {
-        published = st.l[KB - 1];
-        atomicMax(p.hint + row, hint_encode(published, gen));
+      if (MODE == 0 && row < p.N) {
+        if (st.l[KB - 1] > published) {
+          published = st.l[KB - 1];
+          atomicMax(p.hint + row, hint_encode(published, gen));
+        }
+        hintv = fmaxf(hintv, hint_decode(__ldcg(p.hint + row), gen));
       }
       if (last) {
         hintv = kNegInf;

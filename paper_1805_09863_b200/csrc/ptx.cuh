@@ -220,8 +220,11 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t local_smem_addr, uint32
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_smem_addr), "r"(rank));
   return r;
 }
+// Relaxed: the arrival hands over no memory (the TMEM reads it orders are
+// completed by tcgen05.wait::ld and tcgen05.fence::before_thread_sync); a
+// release at cluster scope would cost a cluster-wide memory barrier per call.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
                : "memory");
 }
 // 2-D TMA load whose completion is signalled on the pair leader's mbarrier.
