@@ -99,6 +99,7 @@ struct amun_ol {
   size_t hint_bytes;               // per-row hint words after the slots, then 2 x u32
                                    // {generation, CTAs done} (device-side counters)
   const void* hint_ws = nullptr;   // workspace whose hint region is initialised
+  int ng_override = 0;  // env AMUN_NG: 2 or 4 epilogue warpgroups (experiments)
   int pairs_mode = 0;   // env AMUN_PAIRS: 0 auto, 1 never ("off"), 2 always ("force"; tests)
   MapEntry xmaps[4];
   MapEntry wmaps[8];
@@ -182,31 +183,41 @@ Schedule make_schedule(const amun_ol* pl, int N, int* grid) {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+template <int KB, int NG>
+amun_status launch_tc_ng(const CUtensorMap* mx, const CUtensorMap* mw, const TcParams& tp,
+                         int grid, cudaStream_t st, int mode, bool pairs) {
+  void (*kern)(const CUtensorMap, const CUtensorMap, const TcParams);
+  if (pairs)
+    kern = mode == 0 ? ol_tc2_kernel<KB, 0, NG>
+         : mode == 2 ? ol_tc2_kernel<KB, 2, NG>
+         : mode == 3 ? ol_tc2_kernel<KB, 3, NG>
+                     : ol_tc2_kernel<1, 1, NG>;
+  else
+    kern = mode == 0 ? ol_tc_kernel<KB, 0, NG>
+         : mode == 2 ? ol_tc_kernel<KB, 2, NG>
+         : mode == 3 ? ol_tc_kernel<KB, 3, NG>
+                     : ol_tc_kernel<1, 1, NG>;
+  const int smem_bytes = pairs ? TC2_SMEM : TC_SMEM;
+  // the warpgroup register hand-off needs the full launch pool (see TcCfg)
+  cudaFuncAttributes fa;
+  CUDA_TRY(cudaFuncGetAttributes(&fa, kern));
+  if (fa.numRegs < TcCfg<NG>::kLaunchRegs)
+    return fail(AMUN_ECUDA, "fused kernel compiled with %d registers/thread, needs %d for its "
+                "setmaxnreg budget", fa.numRegs, TcCfg<NG>::kLaunchRegs);
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
+  kern<<<grid, TcCfg<NG>::kThreads, smem_bytes, st>>>(*mx, *mw, tp);
+  CUDA_TRY(cudaGetLastError());
+  return AMUN_OK;
+}
+
+// Epilogue warpgroups: NG = 4 for k-best lists up to 8 (more latency hiding),
+// 2 beyond (more registers per thread). AMUN_NG=2|4 overrides (experiments).
 template <int KB>
 amun_status launch_tc(amun_ol* pl, const CUtensorMap* mx, const CUtensorMap* mw,
                       const TcParams& tp, int grid, cudaStream_t st, int mode, bool pairs) {
-  void (*kern)(const CUtensorMap, const CUtensorMap, const TcParams);
-  if (pairs)
-    kern = mode == 0 ? ol_tc2_kernel<KB, 0>
-         : mode == 2 ? ol_tc2_kernel<KB, 2>
-         : mode == 3 ? ol_tc2_kernel<KB, 3>
-                     : ol_tc2_kernel<1, 1>;
-  else
-    kern = mode == 0 ? ol_tc_kernel<KB, 0>
-         : mode == 2 ? ol_tc_kernel<KB, 2>
-         : mode == 3 ? ol_tc_kernel<KB, 3>
-                     : ol_tc_kernel<1, 1>;
-  const int smem_bytes = pairs ? TC2_SMEM : TC_SMEM;
-  // the warpgroup register hand-off needs the full launch pool (see TC_LAUNCH_REGS)
-  cudaFuncAttributes fa;
-  CUDA_TRY(cudaFuncGetAttributes(&fa, kern));
-  if (fa.numRegs < TC_LAUNCH_REGS)
-    return fail(AMUN_ECUDA, "fused kernel compiled with %d registers/thread, needs %d for its "
-                "setmaxnreg budget", fa.numRegs, TC_LAUNCH_REGS);
-  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
-  kern<<<grid, TC_THREADS, smem_bytes, st>>>(*mx, *mw, tp);
-  CUDA_TRY(cudaGetLastError());
-  return AMUN_OK;
+  const int ng = pl->ng_override ? pl->ng_override : 2;
+  if (ng == 4) return launch_tc_ng<KB, 4>(mx, mw, tp, grid, st, mode, pairs);
+  return launch_tc_ng<KB, 2>(mx, mw, tp, grid, st, mode, pairs);
 }
 
 template <int KB>
@@ -395,6 +406,11 @@ amun_status amun_ol_create(amun_ol** plan, int H, int V_local, int v_offset, int
   pl->device = device;
   pl->num_sms = prop.multiProcessorCount;
   pl->stride = 2 + 2 * k_max;
+  {
+    const char* g = getenv("AMUN_NG");
+    pl->ng_override = g ? atoi(g) : 0;
+    if (pl->ng_override != 2 && pl->ng_override != 4) pl->ng_override = 0;
+  }
   {
     const char* e = getenv("AMUN_PAIRS");
     pl->pairs_mode = !e ? 0 : (strcmp(e, "off") == 0 ? 1 : (strcmp(e, "force") == 0 ? 2 : 0));

@@ -80,6 +80,102 @@ struct RowState {
     }
   }
 
+  // Insert (x, id) ranking before the current KB-th entry, ids in any order:
+  // position p = #entries ranking before it under the full key (l desc, v
+  // asc); all compares are independent (short dependency depth).
+  __device__ __forceinline__ void insert_pos(float x, int id) {
+    int p = 0;
+#pragma unroll
+    for (int i = 0; i < KB; ++i) p += better_lv(l[i], v[i], x, id) ? 1 : 0;
+#pragma unroll
+    for (int i = KB - 1; i >= 1; --i) {
+      const float li = (i > p) ? l[i - 1] : ((i == p) ? x : l[i]);
+      const int vi = (i > p) ? v[i - 1] : ((i == p) ? id : v[i]);
+      l[i] = li;
+      v[i] = vi;
+    }
+    if (p == 0) {
+      l[0] = x;
+      v[0] = id;
+    }
+  }
+
+  // Register-only variant of chunk32 (no shared-memory staging): the same
+  // statistics and gate; a candidate group's four values (x[g], x[g+8],
+  // x[g+16], x[g+24]) are selected from registers by a 3-level select tree
+  // and offered with the full tie key (ids arrive out of order).
+  template <bool TOPK = true>
+  __device__ __forceinline__ void chunk32r(const float (&x)[32], int vbase, float hint) {
+    float t[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) t[j] = fmaxf(x[j], x[j + 16]);
+    float g[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) g[j] = fmaxf(t[j], t[j + 8]);
+    const float cm = fmaxf(fmaxf(fmaxf(g[0], g[4]), fmaxf(g[1], g[5])),
+                           fmaxf(fmaxf(g[2], g[6]), fmaxf(g[3], g[7])));
+    if (cm != kNegInf) {
+      if (cm > m) {
+        s *= ex2((m - cm) * kLog2e);
+        m = cm;
+      }
+      const float ms = m * kLog2e;
+      float a[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] = ex2(fmaf(x[u], kLog2e, -ms));
+#pragma unroll
+      for (int j = 8; j < 32; j += 8)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a[u] += ex2(fmaf(x[j + u], kLog2e, -ms));
+      s += ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+    }
+    if constexpr (!TOPK) return;
+    const float thr = l[KB - 1];
+    float tg = (hint > thr) ? hint : thr;     // candidates: x >= tg (full key decides ties)
+    if constexpr (KB <= 8) {
+      if (__any_sync(0xffffffffu, thr == kNegInf)) {   // list filling: KB-th group maximum
+        float q[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) q[j] = g[j];
+#define AMUN_CS(a, b) { const float hi = fmaxf(q[a], q[b]); q[b] = fminf(q[a], q[b]); q[a] = hi; }
+        AMUN_CS(0, 1) AMUN_CS(2, 3) AMUN_CS(4, 5) AMUN_CS(6, 7)
+        AMUN_CS(0, 2) AMUN_CS(1, 3) AMUN_CS(4, 6) AMUN_CS(5, 7)
+        AMUN_CS(1, 2) AMUN_CS(5, 6) AMUN_CS(0, 4) AMUN_CS(3, 7)
+        AMUN_CS(1, 5) AMUN_CS(2, 6)
+        AMUN_CS(1, 4) AMUN_CS(3, 6)
+        AMUN_CS(2, 4) AMUN_CS(3, 5)
+        AMUN_CS(3, 4)
+#undef AMUN_CS
+        if (q[KB - 1] > tg) tg = q[KB - 1];
+      }
+    }
+    const bool need = cm >= tg && cm != kNegInf;
+    if (__any_sync(0xffffffffu, need)) {
+      uint32_t gm = 0;
+      if (need) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) gm |= (g[j] >= tg) ? (1u << j) : 0u;
+      }
+      while (gm) {
+        const int gi = __ffs(gm) - 1;
+        gm &= gm - 1;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int b = 8 * u;
+          const float s01 = (gi & 1) ? x[b + 1] : x[b + 0];
+          const float s23 = (gi & 1) ? x[b + 3] : x[b + 2];
+          const float s45 = (gi & 1) ? x[b + 5] : x[b + 4];
+          const float s67 = (gi & 1) ? x[b + 7] : x[b + 6];
+          const float s03 = (gi & 2) ? s23 : s01;
+          const float s47 = (gi & 2) ? s67 : s45;
+          const float xv = (gi & 4) ? s47 : s03;
+          const int id = vbase + gi + b;
+          if (xv >= hint && better_lv(xv, id, l[KB - 1], v[KB - 1])) insert_pos(xv, id);
+        }
+      }
+    }
+  }
+
   // Consume 32 biased logits x[j] with token ids vbase + j, in ascending j.
   // Masked entries must already be -inf. `xs` is this thread's 32-float
   // shared-memory scratch row (128-byte aligned); its 16-byte chunks are

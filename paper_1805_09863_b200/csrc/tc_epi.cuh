@@ -1,0 +1,228 @@
+// tc_epi.cuh — the epilogue of the fused tcgen05 kernels (steps 2-4 on the
+// TMEM accumulator), shared by the single-CTA and the CTA-pair kernels.
+//
+// NG epilogue warpgroups; warp (grp, q) owns TMEM lane quadrant q (rows
+// 32q..32q+31 of the CTA's M-tile) and the 32-column chunks c = grp,
+// grp + NG, ... of every tile. Thread = hypothesis row. Per chunk:
+// tcgen05.ld of 32 fp32 columns, + bias (from the shared-memory ring the TMA
+// producer fills), online max / sum-of-exp (Alg. 4 with the exp(Delta)
+// rescale), and the gated register k-best (RowState::chunk32r).
+// After each tile: publish / refresh the cross-CTA k-th-best hint. At the end
+// of a CTA's range in an M-tile the NG groups' states are combined in NG-1
+// rounds through one exchange area and group 0 writes the partial record.
+#pragma once
+#include "epilogue.cuh"
+
+namespace amun {
+
+struct TcParams {
+  int N, V_local, v_offset, n_kblk;
+  Schedule sch;
+  const float* __restrict__ bias;
+  float* __restrict__ part;   // [slots][128][stride]
+  int stride, k_max;
+  float* __restrict__ logits; // MODE 1: [N][V_local]
+  unsigned long long* __restrict__ hint;   // [N] cross-CTA k-th-best hints
+  unsigned int* __restrict__ gen_ctr;      // {generation, CTAs done}: device-side, so every
+                                           // launch (graph replays too) gets a fresh tag
+};
+
+constexpr int TC_BM = 128;
+#ifndef TC_BN_OVERRIDE
+constexpr int TC_BN = 256;
+#else
+constexpr int TC_BN = TC_BN_OVERRIDE;
+#endif
+constexpr int TC_BK = 64;
+constexpr int TC_NBIAS = 8;                          // bias ring slots (see producer bound)
+constexpr int TC_BIAS_BYTES = TC_NBIAS * TC_BN * 4;
+constexpr int TC_XCH_FLOATS = 2 + 2 * 16;            // one row's state in the exchange area
+constexpr int TC_XCH_BYTES = 128 * TC_XCH_FLOATS * 4;
+
+// Launch configuration of NG epilogue warpgroups (warps 0 .. 4NG-1) + the
+// control warpgroup (TMA producer warp, MMA warp, 2 idle warps), and the setmaxnreg budget,
+// which only redistributes the CTA's launch register pool (a warpgroup can
+// grow only into what the others released, else setmaxnreg.inc blocks).
+template <int NG>
+struct TcCfg {
+  static constexpr int kEpiThreads = NG * 128;
+  static constexpr int kThreads = 128 + kEpiThreads;
+  static constexpr int kLaunchRegs = 65536 / kThreads / 8 * 8 > 248 ? 248 : 65536 / kThreads / 8 * 8;
+  static constexpr int kCtrlRegs = NG >= 4 ? 32 : 56;
+  static constexpr int kEpiRegs0 = (kLaunchRegs * kThreads - 128 * kCtrlRegs) / kEpiThreads / 8 * 8;
+  static constexpr int kEpiRegs = kEpiRegs0 > 248 ? 248 : kEpiRegs0;
+  static_assert(128 * kCtrlRegs + kEpiThreads * kEpiRegs <= kLaunchRegs * kThreads,
+                "setmaxnreg budget exceeds the launch register pool");
+};
+
+// Read the launch generation (all CTAs, before any of them finishes).
+__device__ __forceinline__ uint32_t read_generation(const unsigned int* gen_ctr) {
+  return 1u + *reinterpret_cast<const volatile unsigned int*>(gen_ctr);
+}
+// Called once per CTA after all its work: the last CTA advances the generation.
+__device__ __forceinline__ void finish_generation(unsigned int* gen_ctr) {
+  __threadfence();
+  const unsigned int prev = atomicAdd(gen_ctr + 1, 1u);
+  if (prev == gridDim.x - 1) {   // every CTA has read the generation and finished
+    gen_ctr[1] = 0u;
+    atomicAdd(gen_ctr, 1u);
+    __threadfence();
+  }
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Producer side of the bias ring: slot (tile % TC_NBIAS) receives the tile's
+// bias (its 16-byte-aligned part; a <= 3-float tail is read from global).
+// The producer runs at most 2 + ceil(STAGES / n_kblk) - 1 <= 2 + STAGES tiles
+// ahead of the slowest epilogue warp (the MMA cannot start tile t+2 before
+// every epilogue warp released tile t), so TC_NBIAS >= 2 + STAGES suffices.
+__device__ __forceinline__ void bias_ring_load(const TcParams& p, float* sbias, uint64_t* bfull,
+                                               int tile, int v0, int width) {
+  const int slot = tile % TC_NBIAS;
+  const int limit = min(width, p.V_local - v0);
+  const uint32_t bytes = (uint32_t)(limit & ~3) * 4u;
+  mbar_arrive_expect_tx(&bfull[slot], bytes);
+  if (bytes) bulk_load(sbias + slot * TC_BN, p.bias + v0, bytes, &bfull[slot]);
+}
+
+// The epilogue. PAIR: the CTA is rank `rank` of a CTA pair (its M-tile is
+// 2 mp + rank of the pair schedule; TMEM-empty arrivals go to the leader).
+template <int KB, int MODE, int NG, bool PAIR>
+__device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_base, long long start,
+                                            long long stop, uint64_t* tfull, uint64_t* tempty,
+                                            uint64_t* bfull, const float* sbias, float* xch,
+                                            uint32_t gen, int warp, int lane, uint32_t rank,
+                                            long long slot_base) {
+  const int grp = warp >> 2;                       // epilogue warps are 0 .. 4NG-1
+  const int q = warp & 3;                          // TMEM lane quadrant of this warp
+  const int row_local = q * 32 + lane;
+  const uint32_t t_lane = (uint32_t)(q * 32) << 16;
+  uint32_t tempty_addr[2];
+  if constexpr (PAIR) {
+    tempty_addr[0] = mapa_shared(smem_u32(&tempty[0]), 0);
+    tempty_addr[1] = mapa_shared(smem_u32(&tempty[1]), 0);
+  }
+  RowState<KB> st;
+  st.reset();
+  TileIter it{start, stop, p.sch};
+  int unit, v0, width;
+  bool last;
+  int acc = 0, tile = 0;
+  uint32_t acc_phase = 0;
+  float hintv = kNegInf, published = kNegInf;
+  while (it.next(unit, v0, width, last)) {
+    const int mt = PAIR ? 2 * unit + (int)rank : unit;
+    const int row = mt * TC_BM + row_local;
+    const bool live = mt * TC_BM < p.N;            // warp-uniform (padding M-tile of a pair)
+    const int limit = min(width, p.V_local - v0);
+    const int nch = (width + 31) >> 5;
+    const float* bsl = sbias + (tile % TC_NBIAS) * TC_BN;
+    mbar_wait(&bfull[tile % TC_NBIAS], (uint32_t)(tile / TC_NBIAS) & 1u);
+    mbar_wait(&tfull[acc], acc_phase);
+    tc_fence_after();
+    const uint32_t tbase = tmem_base + t_lane + acc * TC_BN;
+    if (live) {
+      for (int c = grp; c < nch; c += NG) {
+        uint32_t r[32];
+        tmem_ld32(tbase + c * 32, r);
+        const int c0 = c * 32;
+        const int nv = limit - c0;
+        float x[32];
+        tmem_ld_wait(r);
+        if (nv >= 32) {   // full chunk: bias from the ring (same address in all lanes)
+          const float4* b4 = reinterpret_cast<const float4*>(bsl + c0);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float4 bq = b4[j];
+            x[4 * j + 0] = __uint_as_float(r[4 * j + 0]) + bq.x;
+            x[4 * j + 1] = __uint_as_float(r[4 * j + 1]) + bq.y;
+            x[4 * j + 2] = __uint_as_float(r[4 * j + 2]) + bq.z;
+            x[4 * j + 3] = __uint_as_float(r[4 * j + 3]) + bq.w;
+          }
+        } else {          // vocabulary tail: mask, and the unstaged <= 3-float bias tail
+          const int nv4 = (limit & ~3) - c0;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float bj = (j < nv4) ? bsl[c0 + j] : ((j < nv) ? __ldg(p.bias + v0 + c0 + j) : 0.f);
+            x[j] = (j < nv) ? __uint_as_float(r[j]) + bj : kNegInf;
+          }
+        }
+        if constexpr (MODE == 1) {
+          if (row < p.N) {
+            float* out = p.logits + (long long)row * p.V_local + v0 + c0;
+            for (int j = 0; j < 32 && j < nv; ++j) out[j] = x[j];
+          }
+        } else if constexpr (MODE == 2) {
+          uint32_t a = 0;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) a ^= r[j];
+          st.s += __uint_as_float(a & 0x007fffffu);   // keep the loads alive
+        } else if constexpr (MODE == 3) {
+          st.template chunk32r<false>(x, p.v_offset + v0 + c0, hintv);
+        } else {
+          st.chunk32r(x, p.v_offset + v0 + c0, hintv);
+        }
+      }
+    }
+    tc_fence_before();
+    if constexpr (PAIR) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_addr[acc]);
+    } else {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+    if (MODE == 0 && row < p.N) {
+      if (st.l[KB - 1] > published) {   // publish our k-th best
+        published = st.l[KB - 1];
+        atomicMax(p.hint + row, hint_encode(published, gen));
+      }
+      // newest cross-CTA hint for the next tile (L2, not L1: other SMs update
+      // it); its latency overlaps the next accumulator wait
+      hintv = fmaxf(hintv, hint_decode(__ldcg(p.hint + row), gen));
+    }
+    if (last) {
+      hintv = kNegInf;   // the next segment is another M-tile (other rows)
+      published = kNegInf;
+      if constexpr (MODE != 1) {
+        float* xr = xch + row_local * TC_XCH_FLOATS;
+        for (int g = 1; g < NG; ++g) {
+          if (grp == g) {
+            xr[0] = st.m;
+            xr[1] = st.s;
+#pragma unroll
+            for (int i = 0; i < KB; ++i) {
+              xr[2 + i] = st.l[i];
+              xr[2 + 16 + i] = __int_as_float(st.v[i]);
+            }
+          }
+          named_bar_sync(1 + q, NG * 32);
+          if (grp == 0) {
+            float l2[KB];
+            int v2[KB];
+#pragma unroll
+            for (int i = 0; i < KB; ++i) {
+              l2[i] = xr[2 + i];
+              v2[i] = __float_as_int(xr[2 + 16 + i]);
+            }
+            st.combine(xr[0], xr[1], l2, v2);
+          }
+          named_bar_sync(5 + q, NG * 32);
+        }
+        if (grp == 0 && row < p.N) {
+          const long long slot = PAIR ? (slot_base + unit) * 2 + rank : slot_base + unit;
+          st.emit(p.part + (slot * TC_BM + row_local) * p.stride, p.k_max);
+        }
+      }
+      st.reset();
+    }
+    acc ^= 1;
+    if (acc == 0) acc_phase ^= 1;
+    ++tile;
+  }
+}
+
+}  // namespace amun
