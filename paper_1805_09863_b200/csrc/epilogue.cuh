@@ -159,6 +159,7 @@ struct RowState {
       while (gm) {
         const int gi = __ffs(gm) - 1;
         gm &= gm - 1;
+        float q[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           const int b = 8 * u;
@@ -168,8 +169,16 @@ struct RowState {
           const float s67 = (gi & 1) ? x[b + 7] : x[b + 6];
           const float s03 = (gi & 2) ? s23 : s01;
           const float s47 = (gi & 2) ? s67 : s45;
-          const float xv = (gi & 4) ? s47 : s03;
-          const int id = vbase + gi + b;
+          q[u] = (gi & 4) ? s47 : s03;
+        }
+        // pre-check the 4 values; only qualifying ones (usually 1) are offered
+        uint32_t em = (q[0] >= tg ? 1u : 0u) | (q[1] >= tg ? 2u : 0u) | (q[2] >= tg ? 4u : 0u) |
+                      (q[3] >= tg ? 8u : 0u);
+        while (em) {
+          const int u = __ffs(em) - 1;
+          em &= em - 1;
+          const float xv = (u & 2) ? ((u & 1) ? q[3] : q[2]) : ((u & 1) ? q[1] : q[0]);
+          const int id = vbase + gi + 8 * u;
           if (xv >= hint && better_lv(xv, id, l[KB - 1], v[KB - 1])) insert_pos(xv, id);
         }
       }

@@ -31,7 +31,7 @@ constexpr int TC_STAGES = 4;
 constexpr int TC_A_BYTES = TC_BM * TC_BK * 2;   // 16 KB
 constexpr int TC_B_BYTES = TC_BN * TC_BK * 2;   // 32 KB
 constexpr int TC_SMEM = TC_STAGES * (TC_A_BYTES + TC_B_BYTES) + TC_BIAS_BYTES + TC_XCH_BYTES +
-                        1024 /*align*/ + 512 /*barriers*/;
+                        TC_THRX_BYTES + 1024 /*align*/ + 512 /*barriers*/;
 static_assert(TC_NBIAS >= 2 + TC_STAGES, "bias ring too small for the producer's lead");
 
 template <int KB, int MODE, int NG>
@@ -46,7 +46,8 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
   uint8_t* sB = sA + TC_STAGES * TC_A_BYTES;
   float* sbias = reinterpret_cast<float*>(sB + TC_STAGES * TC_B_BYTES);
   float* xch = sbias + TC_NBIAS * TC_BN;
-  uint64_t* full = reinterpret_cast<uint64_t*>(xch + 128 * TC_XCH_FLOATS);
+  unsigned long long* thr_x = reinterpret_cast<unsigned long long*>(xch + 128 * TC_XCH_FLOATS);
+  uint64_t* full = reinterpret_cast<uint64_t*>(thr_x + 4 * 128);
   uint64_t* empty = full + TC_STAGES;
   uint64_t* tfull = empty + TC_STAGES;
   uint64_t* tempty = tfull + 2;
@@ -63,6 +64,7 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
   constexpr int kCtrl = 4 * NG;                    // first control warp
   const int role = warp - kCtrl;                   // 0 = TMA, 1 = MMA, 2-3 idle, < 0 epilogue
 
+  for (int i = threadIdx.x; i < 4 * 128; i += blockDim.x) thr_x[i] = 0ull;   // no stale tags
   if (role == 0 && lane == 0) {
     prefetch_tmap(&tmX);
     prefetch_tmap(&tmW);
@@ -162,7 +164,7 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
   } else {
     reg_alloc<Cfg::kEpiRegs>();
     tc_epilogue<KB, MODE, NG, false>(p, tmem_base, start, stop, tfull, tempty, bfull, sbias, xch,
-                                     gen, warp, lane, 0u, (long long)blockIdx.x);
+                                     thr_x, gen, warp, lane, 0u, (long long)blockIdx.x);
   }
 
   tc_fence_before();

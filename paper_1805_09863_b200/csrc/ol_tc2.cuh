@@ -27,7 +27,7 @@ constexpr int TC2_STAGES = 6;
 constexpr int TC2_A_BYTES = TC_BM * TC_BK * 2;          // 16 KB: this CTA's 128 rows of X
 constexpr int TC2_B_BYTES = (TC_BN / 2) * TC_BK * 2;    // 16 KB: this CTA's half of the W tile
 constexpr int TC2_SMEM = TC2_STAGES * (TC2_A_BYTES + TC2_B_BYTES) + TC_BIAS_BYTES + TC_XCH_BYTES +
-                         1024 /*align*/ + 512 /*barriers*/;
+                         TC_THRX_BYTES + 1024 /*align*/ + 512 /*barriers*/;
 static_assert(TC_NBIAS >= 2 + TC2_STAGES, "bias ring too small for the producer's lead");
 
 template <int KB, int MODE, int NG>
@@ -42,7 +42,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<NG>::kThreads,
   uint8_t* sB = sA + TC2_STAGES * TC2_A_BYTES;
   float* sbias = reinterpret_cast<float*>(sB + TC2_STAGES * TC2_B_BYTES);
   float* xch = sbias + TC_NBIAS * TC_BN;
-  uint64_t* full = reinterpret_cast<uint64_t*>(xch + 128 * TC_XCH_FLOATS);
+  unsigned long long* thr_x = reinterpret_cast<unsigned long long*>(xch + 128 * TC_XCH_FLOATS);
+  uint64_t* full = reinterpret_cast<uint64_t*>(thr_x + 4 * 128);
   uint64_t* empty = full + TC2_STAGES;
   uint64_t* tfull = empty + TC2_STAGES;
   uint64_t* tempty = tfull + 2;
@@ -61,6 +62,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<NG>::kThreads,
   const uint32_t rank = cluster_ctarank();          // 0 = leader, 1 = peer
   const int pair = blockIdx.x >> 1;
 
+  for (int i = threadIdx.x; i < 4 * 128; i += blockDim.x) thr_x[i] = 0ull;   // no stale tags
   if (role == 0 && lane == 0) {
     prefetch_tmap(&tmX);
     prefetch_tmap(&tmW);
@@ -160,7 +162,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<NG>::kThreads,
   } else {
     reg_alloc<Cfg::kEpiRegs>();
     tc_epilogue<KB, MODE, NG, true>(p, tmem_base, start, stop, tfull, tempty, bfull, sbias, xch,
-                                    gen, warp, lane, rank, (long long)pair);
+                                    thr_x, gen, warp, lane, rank, (long long)pair);
   }
 
   tc_fence_before();

@@ -38,6 +38,7 @@ constexpr int TC_NBIAS = 8;                          // bias ring slots (see pro
 constexpr int TC_BIAS_BYTES = TC_NBIAS * TC_BN * 4;
 constexpr int TC_XCH_FLOATS = 2 + 2 * 16;            // one row's state in the exchange area
 constexpr int TC_XCH_BYTES = 128 * TC_XCH_FLOATS * 4;
+constexpr int TC_THRX_BYTES = 4 * 128 * 8;           // per-(group, row) k-th-best words (NG <= 4)
 
 // Launch configuration of NG epilogue warpgroups (warps 0 .. 4NG-1) + the
 // control warpgroup (TMA producer warp, MMA warp, 2 idle warps), and the setmaxnreg budget,
@@ -94,8 +95,8 @@ template <int KB, int MODE, int NG, bool PAIR>
 __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_base, long long start,
                                             long long stop, uint64_t* tfull, uint64_t* tempty,
                                             uint64_t* bfull, const float* sbias, float* xch,
-                                            uint32_t gen, int warp, int lane, uint32_t rank,
-                                            long long slot_base) {
+                                            unsigned long long* thr_x, uint32_t gen, int warp,
+                                            int lane, uint32_t rank, long long slot_base) {
   const int grp = warp >> 2;                       // epilogue warps are 0 .. 4NG-1
   const int q = warp & 3;                          // TMEM lane quadrant of this warp
   const int row_local = q * 32 + lane;
@@ -113,8 +114,14 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
   int acc = 0, tile = 0;
   uint32_t acc_phase = 0;
   float hintv = kNegInf, published = kNegInf;
+  // The groups of a CTA hold disjoint chunks of the same rows: each publishes
+  // its k-th best in shared memory (tagged with the M-tile, so a word from an
+  // earlier segment is never used) and gates with the best of all groups.
+  unsigned long long* my_thr = thr_x + grp * 128 + row_local;
+  float shared_kth = kNegInf;
   while (it.next(unit, v0, width, last)) {
     const int mt = PAIR ? 2 * unit + (int)rank : unit;
+    const uint32_t tag = (uint32_t)mt + 1u;
     const int row = mt * TC_BM + row_local;
     const bool live = mt * TC_BM < p.N;            // warp-uniform (padding M-tile of a pair)
     const int limit = min(width, p.V_local - v0);
@@ -163,7 +170,16 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
         } else if constexpr (MODE == 3) {
           st.template chunk32r<false>(x, p.v_offset + v0 + c0, hintv);
         } else {
-          st.chunk32r(x, p.v_offset + v0 + c0, hintv);
+#pragma unroll
+          for (int g2 = 0; g2 < NG; ++g2) {
+            if (g2 != grp) {
+              const unsigned long long w = thr_x[g2 * 128 + row_local];
+              if ((uint32_t)(w >> 32) == tag) shared_kth = fmaxf(shared_kth, o2f((uint32_t)w));
+            }
+          }
+          const float before = st.l[KB - 1];
+          st.chunk32r(x, p.v_offset + v0 + c0, fmaxf(hintv, shared_kth));
+          if (st.l[KB - 1] > before) *my_thr = ((unsigned long long)tag << 32) | f2o(st.l[KB - 1]);
         }
       }
     }
@@ -187,6 +203,7 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
     if (last) {
       hintv = kNegInf;   // the next segment is another M-tile (other rows)
       published = kNegInf;
+      shared_kth = kNegInf;
       if constexpr (MODE != 1) {
         float* xr = xch + row_local * TC_XCH_FLOATS;
         for (int g = 1; g < NG; ++g) {
