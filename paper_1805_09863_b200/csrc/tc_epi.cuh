@@ -192,7 +192,10 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
       if (lane == 0) mbar_arrive(&tempty[acc]);
     }
     if (MODE == 0 && row < p.N) {
-      if (st.l[KB - 1] > published) {   // publish our k-th best
+      // publish our k-th best only if it beats what is already known (with
+      // many CTAs per row, e.g. one M-tile over 148 CTAs, unconditional
+      // atomics would serialise on the row's word)
+      if (st.l[KB - 1] > published && st.l[KB - 1] > hintv) {
         published = st.l[KB - 1];
         atomicMax(p.hint + row, hint_encode(published, gen));
       }
