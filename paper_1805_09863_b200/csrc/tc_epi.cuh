@@ -127,6 +127,10 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
     const int limit = min(width, p.V_local - v0);
     const int nch = (width + 31) >> 5;
     const float* bsl = sbias + (tile % TC_NBIAS) * TC_BN;
+    // request the newest cross-CTA hint now (L2, not L1: other SMs update it);
+    // it is folded in after this tile's chunks, for the next tile of the segment
+    unsigned long long hraw = 0ull;
+    if (MODE == 0 && row < p.N && !last) hraw = __ldcg(p.hint + row);
     mbar_wait(&bfull[tile % TC_NBIAS], (uint32_t)(tile / TC_NBIAS) & 1u);
     mbar_wait(&tfull[acc], acc_phase);
     tc_fence_after();
@@ -199,9 +203,7 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
         published = st.l[KB - 1];
         atomicMax(p.hint + row, hint_encode(published, gen));
       }
-      // newest cross-CTA hint for the next tile (L2, not L1: other SMs update
-      // it); its latency overlaps the next accumulator wait
-      hintv = fmaxf(hintv, hint_decode(__ldcg(p.hint + row), gen));
+      hintv = fmaxf(hintv, hint_decode(hraw, gen));   // 0 (no hint) when `last`
     }
     if (last) {
       hintv = kNegInf;   // the next segment is another M-tile (other rows)
