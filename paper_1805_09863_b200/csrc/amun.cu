@@ -210,13 +210,17 @@ amun_status launch_tc_ng(const CUtensorMap* mx, const CUtensorMap* mw, const TcP
   return AMUN_OK;
 }
 
-// Epilogue warpgroups: NG = 4 for k-best lists up to 8 (more latency hiding),
-// 2 beyond (more registers per thread). AMUN_NG=2|4 overrides (experiments).
+// Two epilogue warpgroups: measured faster than four at every config tried
+// (four warps per sub-partition cost issue slots and registers).
+// Building with -DAMUN_WITH_NG4 adds the 4-group kernels (env AMUN_NG=4).
 template <int KB>
 amun_status launch_tc(amun_ol* pl, const CUtensorMap* mx, const CUtensorMap* mw,
                       const TcParams& tp, int grid, cudaStream_t st, int mode, bool pairs) {
-  const int ng = pl->ng_override ? pl->ng_override : 2;
-  if (ng == 4) return launch_tc_ng<KB, 4>(mx, mw, tp, grid, st, mode, pairs);
+#ifdef AMUN_WITH_NG4
+  if (pl->ng_override == 4) return launch_tc_ng<KB, 4>(mx, mw, tp, grid, st, mode, pairs);
+#else
+  (void)pl;
+#endif
   return launch_tc_ng<KB, 2>(mx, mw, tp, grid, st, mode, pairs);
 }
 

@@ -350,3 +350,62 @@ def test_graph_replay_with_new_inputs(N):
         _, _, oc64, nxt = O.kbest_sentences(logp, pcd, off.cpu().numpy(), k)
         compare_kbest(oi.cpu().numpy(), oc.cpu().numpy(), lambda s, r, v: pcd[r] + logp[r, v],
                       oc64, np.full(S, k), "bf16", V, o_next=nxt)
+
+
+# ------------------------------------------------------------------ full-size sampled parity
+def _sampled_oracle_check(w, idx, cost, sentences, V_total):
+    """Oracle on the sampled sentences only (all their rows, full vocabulary)."""
+    Xh, pch, offh = synth.gen_X(w), synth.gen_prev_cost(w), synth.gen_offsets(w)
+    rows = np.concatenate([np.arange(int(offh[s]), int(offh[s + 1])) for s in sentences])
+    Wo, bo = O.as_f64(synth.gen_W(w)), O.as_f64(synth.gen_b(w))
+    L = O.add_bias(O.gemm(O.as_f64(Xh[torch.from_numpy(rows)]), Wo), bo)
+    logp = O.log_softmax(L)
+    pcs = O.as_f64(pch)[rows]
+    sub_off = np.concatenate([[0], np.cumsum([int(offh[s + 1] - offh[s]) for s in sentences])])
+    _, _, oc64, nxt = O.kbest_sentences(logp, pcs, sub_off, w.k)
+    pos = {int(r): i for i, r in enumerate(rows)}
+    gi = idx.cpu().numpy()[sentences]
+    gc = cost.cpu().numpy()[sentences]
+    # GPU indices are r * V_total + v with global r; the oracle sees the sampled rows
+    return compare_kbest(gi, gc, lambda s, r, v: pcs[pos[r]] + logp[pos[r], v], oc64,
+                         np.full(len(sentences), w.k), "bf16", V_total, o_next=nxt)
+
+
+@pytest.mark.slow
+def test_cfg_shard_full_size_sampled():
+    """BASELINE cfg 'shard' at full size on one GPU (H=1024, V=256000, 1024 x 12,
+    k=12; 96 M-tiles -> the CTA-pair kernel): every 64th sentence (16 sentences,
+    192 rows, full vocabulary) against the oracle."""
+    w = synth.CONFIGS["shard"]
+    dev = DEV
+    ol = amun().OutputLayer(w.H, w.V, k_max=w.k, max_rows=w.N, max_sentences=w.S)
+    X, W, b = synth.gen_X(w).to(dev), synth.gen_W(w).to(dev), synth.gen_b(w).to(dev)
+    pc, off = synth.gen_prev_cost(w).to(dev), synth.gen_offsets(w).to(dev)
+    idx, cost = ol(X, W, b, pc, off, w.k)
+    torch.cuda.synchronize()
+    del W
+    rep = _sampled_oracle_check(w, idx, cost, list(range(0, w.S, 64)), w.V)
+    assert rep["sentences_checked"] == 16
+
+
+@pytest.mark.slow
+def test_cfg_shard_vocab_sharded_8_sampled():
+    """The 8-way vocab-sharded path at cfg 'shard' size, emulated on one GPU:
+    8 plans over V/8 slices (partial records), stacked like the all-gather,
+    exact merge; every 128th sentence against the oracle."""
+    from paper_1805_09863_b200.sharded import shard_range
+    w = synth.CONFIGS["shard"]
+    dev = DEV
+    X, pc, off = synth.gen_X(w).to(dev), synth.gen_prev_cost(w).to(dev), synth.gen_offsets(w).to(dev)
+    parts, plans = [], []
+    for g in range(8):
+        v0, v1 = shard_range(w.V, 8, g)
+        ol = amun().OutputLayer(w.H, v1 - v0, v_offset=v0, V_total=w.V, k_max=w.k,
+                                max_rows=w.N, max_sentences=w.S)
+        plans.append(ol)
+        parts.append(ol.partial(X, synth.gen_W(w, v0, v1 - v0).to(dev),
+                                synth.gen_b(w, v0, v1 - v0).to(dev)))
+    idx, cost = plans[0].merge(torch.stack(parts), pc, off, w.k)
+    torch.cuda.synchronize()
+    rep = _sampled_oracle_check(w, idx, cost, list(range(0, w.S, 128)), w.V)
+    assert rep["sentences_checked"] == 8

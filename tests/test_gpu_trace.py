@@ -60,3 +60,61 @@ def test_trace_dynamic_and_naive():
     nai = tr.run(X, Wd, bd, pc, f, mode="naive")
     assert sum(nai.rows) == int(f.max()) * S * B             # Alg. 1 decodes every slot
     assert nai.steps == dyn.steps == int(f.max())
+
+
+@pytest.mark.slow
+def test_trace_full_size_sampled():
+    """BASELINE cfg 'trace' at full size (1280 sentences x beam 5, V = 90000,
+    H = 1024): compaction bit-exact against the oracle at EVERY step; the output
+    layer against the oracle on 16 sampled sentences at 4 sampled steps."""
+    from paper_1805_09863_b200.trace import DecodeTrace
+    w = synth.CONFIGS["trace"]
+    S, B, H, V = w.S, w.B, w.H, w.V
+    X, W, b, pc = synth.gen_X(w), synth.gen_W(w), synth.gen_b(w), synth.gen_prev_cost(w)
+    f = synth.eos_schedule(w.seed, S, B)
+    dev = torch.device("cuda", 0)
+    tr = DecodeTrace(H, V, S, B, device=dev)
+    Wo, bo = O.as_f64(W), O.as_f64(b)
+    steps_checked = {0, 5, 20, 40}
+    seen = {"compact": 0, "ol": 0}
+
+    def as_bytes(c):
+        rb = c.element_size()
+        for d in c.shape[1:]:
+            rb *= int(d)
+        return c.contiguous().view(torch.uint8).reshape(c.shape[0], rb).cpu().numpy()
+
+    def check(t, inp, out):
+        if inp[0] == "compact":
+            _, src_cols, alive, off = inp
+            dst_cols, new_off, src_row, counts = out
+            rc, ro, rs, rn, rsa = O.compact([as_bytes(c) for c in src_cols], alive.cpu().numpy(),
+                                            off.cpu().numpy())
+            assert counts.cpu().tolist() == [rn, rsa]
+            assert np.array_equal(new_off.cpu().numpy(), ro)
+            assert np.array_equal(src_row.cpu().numpy(), rs)
+            for d, r in zip(dst_cols, rc):
+                assert np.array_equal(as_bytes(d), r)
+            seen["compact"] += 1
+            return
+        if t not in steps_checked:
+            return
+        Xs, _, _, prev, off, k_s = inp
+        idx, cost = out
+        offn, ksn = off.cpu().numpy(), k_s.cpu().numpy()
+        live = [s for s in range(S) if offn[s + 1] > offn[s]]
+        sent = live[:: max(1, len(live) // 16)][:16]
+        rows = np.concatenate([np.arange(offn[s], offn[s + 1]) for s in sent])
+        logp = O.log_softmax(O.add_bias(O.gemm(O.as_f64(Xs[torch.from_numpy(rows).to(Xs.device)]), Wo), bo))
+        prevd = O.as_f64(prev)[rows]
+        sub_off = np.concatenate([[0], np.cumsum([offn[s + 1] - offn[s] for s in sent])])
+        _, _, oc64, nxt = O.kbest_sentences(logp, prevd, sub_off, B, ksn[sent])
+        pos = {int(r): i for i, r in enumerate(rows)}
+        compare_kbest(idx.cpu().numpy()[sent], cost.cpu().numpy()[sent],
+                      lambda s, r, v: prevd[pos[r]] + logp[pos[r], v], oc64, ksn[sent], "bf16", V,
+                      o_next=nxt)
+        seen["ol"] += 1
+
+    dyn = tr.run(X, W.to(dev), b.to(dev), pc, f, mode="dynamic", check=check)
+    assert seen["compact"] == dyn.steps and seen["ol"] == 4
+    assert sum(dyn.rows) == int(f.sum())
