@@ -5,6 +5,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -582,7 +583,9 @@ amun_status amun_compact(const amun_column* cols, int n_cols, const uint8_t* ali
   cp.src_row = src_row;
   cp.counts = counts;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int grid = N > 0 ? (int)cdiv(N, CP_ROWS) : 1;
+  cp.per = (int)cdiv(cdiv(N > 0 ? N : 1, CP_THREADS), 16) * 16;
+  const int grid = (int)std::max<long long>(
+      1, std::max<long long>(cdiv(N, CP_ROWS), cdiv((long long)S + 1, CP_THREADS)));
   compact_kernel<<<grid, CP_THREADS, 0, st>>>(cp);
   CUDA_TRY(cudaGetLastError());
   if (counts_host) {

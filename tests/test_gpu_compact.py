@@ -11,14 +11,19 @@ pytestmark = pytest.mark.gpu
 DEV = torch.device("cuda", 0)
 
 
-def run(N, S_sizes, alive, row_bytes_list, seed=0):
+def run(N, S_sizes, alive, row_bytes_list, seed=0, alive_shift=0):
     import paper_1805_09863_b200 as amun
     off = torch.tensor(np.concatenate([[0], np.cumsum(S_sizes)]), dtype=torch.int32)
     assert int(off[-1]) == N
     cols_h = [synth.gen_bytes(seed + i, synth.S_STATE, N * rb).view(N, rb) if N else
               torch.empty(0, rb, dtype=torch.uint8) for i, rb in enumerate(row_bytes_list)]
     cols_d = [(c.to(DEV), torch.full_like(c, 0xAB, device=DEV)) for c in cols_h]
-    n, s_alive, new_off, src_row, counts = amun.compact(cols_d, alive.to(DEV), off.to(DEV))
+    alive_d = alive.to(DEV)
+    if alive_shift:   # flags at a non-16-byte-aligned address (byte path)
+        buf = torch.zeros(N + alive_shift, dtype=torch.uint8, device=DEV)
+        buf[alive_shift:] = alive_d
+        alive_d = buf[alive_shift:]
+    n, s_alive, new_off, src_row, counts = amun.compact(cols_d, alive_d, off.to(DEV))
     ref_cols, ref_off, ref_src, ref_n, ref_s = O.compact([c.numpy() for c in cols_h],
                                                           alive.numpy(), off.numpy())
     assert n == ref_n and s_alive == ref_s
@@ -68,3 +73,21 @@ def test_one_survivor_per_sentence_and_alternating():
     run(N, [B] * (N // B), alive, [64])
     alive = torch.tensor([i % 2 for i in range(N)], dtype=torch.uint8)
     run(N, [B] * (N // B), alive, [64, 12])
+
+
+@pytest.mark.parametrize("shift", [1, 3, 8])
+def test_unaligned_flags(shift):
+    N = 1001
+    rng = np.random.default_rng(shift)
+    alive = torch.from_numpy((rng.random(N) < 0.5).astype(np.uint8))
+    run(N, [7] * 143, alive, [32, 4], alive_shift=shift)
+
+
+@pytest.mark.parametrize("N,B", [(70001, 1), (65536, 12), (16389, 3)])
+def test_large_ragged(N, B):
+    """Several 16-byte flag words per scan thread, S > 256 * grid-limit cases,
+    flag counts that end mid-word (masked-tail path)."""
+    rng = np.random.default_rng(N)
+    sizes = [B] * (N // B) + ([N % B] if N % B else [])
+    alive = torch.from_numpy((rng.random(N) < 0.3).astype(np.uint8))
+    run(N, sizes, alive, [16, 4])
