@@ -74,7 +74,7 @@ class OutputLayer:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and _L is not None:   # (_L is None at interpreter exit)
             _L.amun_ol_destroy(h)
             self._h = None
 

@@ -219,9 +219,11 @@ amun_status launch_tc(amun_ol* pl, const CUtensorMap* mx, const CUtensorMap* mw,
                       const TcParams& tp, int grid, cudaStream_t st, int mode, bool pairs) {
 #ifdef AMUN_WITH_NG4
   if (pl->ng_override == 4) return launch_tc_ng<KB, 4>(mx, mw, tp, grid, st, mode, pairs);
-#else
-  (void)pl;
 #endif
+#ifdef AMUN_WITH_NG3
+  if (pl->ng_override == 3) return launch_tc_ng<KB, 3>(mx, mw, tp, grid, st, mode, pairs);
+#endif
+  (void)pl;
   return launch_tc_ng<KB, 2>(mx, mw, tp, grid, st, mode, pairs);
 }
 
@@ -414,7 +416,7 @@ amun_status amun_ol_create(amun_ol** plan, int H, int V_local, int v_offset, int
   {
     const char* g = getenv("AMUN_NG");
     pl->ng_override = g ? atoi(g) : 0;
-    if (pl->ng_override != 2 && pl->ng_override != 4) pl->ng_override = 0;
+    if (pl->ng_override < 2 || pl->ng_override > 4) pl->ng_override = 0;
   }
   {
     const char* e = getenv("AMUN_PAIRS");
@@ -594,5 +596,16 @@ amun_status amun_compact(const amun_column* cols, int n_cols, const uint8_t* ali
   }
   return AMUN_OK;
 }
+
+#if AMUN_EXP == 4
+amun_status amun_debug_counters(unsigned long long* host8, int reset) {
+  cudaMemcpyFromSymbol(host8, amun::amun_dbg, 8 * sizeof(unsigned long long));
+  if (reset) {
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(amun::amun_dbg, z, sizeof(z));
+  }
+  return AMUN_OK;
+}
+#endif
 
 }  // extern "C"

@@ -15,7 +15,16 @@
 #include <math_constants.h>
 #include "ptx.cuh"
 
+#ifndef AMUN_EXP
+#define AMUN_EXP 0
+#endif
 namespace amun {
+#if AMUN_EXP == 4
+// instrumentation build only: [0] row-chunks, [1] row-chunks with a candidate,
+// [2] insertions, [3] insertions into a filling list, [4] warp-chunks with a candidate
+__device__ unsigned long long amun_dbg[8];
+#define AMUN_DBG(i, n) atomicAdd(&amun_dbg[i], (unsigned long long)(n))
+#endif
 
 constexpr float kLog2e = 1.4426950408889634f;
 constexpr float kNegInf = -__builtin_huge_valf();
@@ -61,43 +70,41 @@ struct RowState {
 
   // Insert a NEW element whose token id is larger than every id already in
   // the list (true inside one ascending scan): ties keep the older entries
-  // ahead. Position p = #entries >= x; all compares are independent, so the
-  // dependency depth is short (no carried compare-swap chain).
+  // ahead. All compares are independent and each slot is one select pair,
+  // so the dependency depth is short (no carried compare-swap chain).
   __device__ __forceinline__ void insert_new(float x, int id) {
-    int p = 0;
+    bool b[KB];   // b[i]: entry i stays ahead of x; a prefix, since l is sorted
 #pragma unroll
-    for (int i = 0; i < KB; ++i) p += (l[i] >= x) ? 1 : 0;
+    for (int i = 0; i < KB; ++i) b[i] = l[i] >= x;
+    shift_in(b, x, id);
+  }
+
+  // Slot i keeps its entry if it ranks ahead of the new one, else takes the
+  // new one (first slot behind it) or its predecessor's entry.
+  __device__ __forceinline__ void shift_in(const bool (&b)[KB], float x, int id) {
 #pragma unroll
     for (int i = KB - 1; i >= 1; --i) {
-      const float li = (i > p) ? l[i - 1] : ((i == p) ? x : l[i]);
-      const int vi = (i > p) ? v[i - 1] : ((i == p) ? id : v[i]);
-      l[i] = li;
-      v[i] = vi;
+      l[i] = b[i] ? l[i] : (b[i - 1] ? x : l[i - 1]);
+      v[i] = b[i] ? v[i] : (b[i - 1] ? id : v[i - 1]);
     }
-    if (p == 0) {
-      l[0] = x;
-      v[0] = id;
-    }
+    l[0] = b[0] ? l[0] : x;
+    v[0] = b[0] ? v[0] : id;
   }
 
   // Insert (x, id) ranking before the current KB-th entry, ids in any order:
-  // position p = #entries ranking before it under the full key (l desc, v
-  // asc); all compares are independent (short dependency depth).
+  // entries ranking ahead of it under the full key (l desc, v asc) stay.
   __device__ __forceinline__ void insert_pos(float x, int id) {
-    int p = 0;
+#if AMUN_EXP == 1
+    l[KB - 1] = x; v[KB - 1] = id; return;
+#endif
+#if AMUN_EXP == 4
+    AMUN_DBG(2, 1);
+    if (l[KB - 1] == kNegInf) AMUN_DBG(3, 1);
+#endif
+    bool b[KB];
 #pragma unroll
-    for (int i = 0; i < KB; ++i) p += better_lv(l[i], v[i], x, id) ? 1 : 0;
-#pragma unroll
-    for (int i = KB - 1; i >= 1; --i) {
-      const float li = (i > p) ? l[i - 1] : ((i == p) ? x : l[i]);
-      const int vi = (i > p) ? v[i - 1] : ((i == p) ? id : v[i]);
-      l[i] = li;
-      v[i] = vi;
-    }
-    if (p == 0) {
-      l[0] = x;
-      v[0] = id;
-    }
+    for (int i = 0; i < KB; ++i) b[i] = better_lv(l[i], v[i], x, id);
+    shift_in(b, x, id);
   }
 
   // Register-only variant of chunk32 (no shared-memory staging): the same
@@ -120,13 +127,21 @@ struct RowState {
         m = cm;
       }
       const float ms = m * kLog2e;
+      // exp2 arguments and the 8 running sums on packed fp32 pairs (same
+      // association as the scalar form: a[u] = e[u] + e[u+8] + e[u+16] + e[u+24])
+      float e[32];
+#pragma unroll
+      for (int u = 0; u < 32; u += 2)
+        ffma2(e[u], e[u + 1], x[u], x[u + 1], kLog2e, kLog2e, -ms, -ms);
+#pragma unroll
+      for (int u = 0; u < 32; ++u) e[u] = ex2(e[u]);
       float a[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) a[u] = ex2(fmaf(x[u], kLog2e, -ms));
+      for (int u = 0; u < 8; ++u) a[u] = e[u];
 #pragma unroll
       for (int j = 8; j < 32; j += 8)
 #pragma unroll
-        for (int u = 0; u < 8; ++u) a[u] += ex2(fmaf(x[j + u], kLog2e, -ms));
+        for (int u = 0; u < 8; u += 2) fadd2(a[u], a[u + 1], a[u], a[u + 1], e[j + u], e[j + u + 1]);
       s += ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
     }
     if constexpr (!TOPK) return;
@@ -150,6 +165,18 @@ struct RowState {
       }
     }
     const bool need = cm >= tg && cm != kNegInf;
+#if AMUN_EXP == 4
+    if ((threadIdx.x & 31) == 0) {
+      AMUN_DBG(0, __popc(__ballot_sync(0xffffffffu, cm != kNegInf)));
+      AMUN_DBG(1, __popc(__ballot_sync(0xffffffffu, need)));
+      if (__any_sync(0xffffffffu, need)) AMUN_DBG(4, 1);
+    } else {
+      __ballot_sync(0xffffffffu, cm != kNegInf); __ballot_sync(0xffffffffu, need); __any_sync(0xffffffffu, need);
+    }
+#endif
+#if AMUN_EXP == 2
+    if (__any_sync(0xffffffffu, need)) { if (need) { l[KB - 1] = cm; v[KB - 1] = vbase; } return; }
+#endif
     if (__any_sync(0xffffffffu, need)) {
       uint32_t gm = 0;
       if (need) {

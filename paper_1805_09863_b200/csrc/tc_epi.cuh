@@ -129,6 +129,8 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
     const float* bsl = sbias + (tile % TC_NBIAS) * TC_BN;
     // request the newest cross-CTA hint now (L2, not L1: other SMs update it);
     // it is folded in after this tile's chunks, for the next tile of the segment
+    // (per-chunk exchange halves the insertions but its loads and atomics cost
+    // as much as it saves: DESIGN.md §6.1)
     unsigned long long hraw = 0ull;
     if (MODE == 0 && row < p.N && !last) hraw = __ldcg(p.hint + row);
     mbar_wait(&bfull[tile % TC_NBIAS], (uint32_t)(tile / TC_NBIAS) & 1u);
@@ -144,14 +146,14 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
         float x[32];
         tmem_ld_wait(r);
         if (nv >= 32) {   // full chunk: bias from the ring (same address in all lanes)
-          const float4* b4 = reinterpret_cast<const float4*>(bsl + c0);
+          const uint32_t b4 = smem_u32(bsl + c0);
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            const float4 bq = b4[j];
-            x[4 * j + 0] = __uint_as_float(r[4 * j + 0]) + bq.x;
-            x[4 * j + 1] = __uint_as_float(r[4 * j + 1]) + bq.y;
-            x[4 * j + 2] = __uint_as_float(r[4 * j + 2]) + bq.z;
-            x[4 * j + 3] = __uint_as_float(r[4 * j + 3]) + bq.w;
+            const float4 bq = lds128(b4 + 16 * j);
+            fadd2(x[4 * j + 0], x[4 * j + 1], __uint_as_float(r[4 * j + 0]), __uint_as_float(r[4 * j + 1]),
+                  bq.x, bq.y);
+            fadd2(x[4 * j + 2], x[4 * j + 3], __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]),
+                  bq.z, bq.w);
           }
         } else {          // vocabulary tail: mask, and the unstaged <= 3-float bias tail
           const int nv4 = (limit & ~3) - c0;
@@ -176,14 +178,14 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
         } else {
 #pragma unroll
           for (int g2 = 0; g2 < NG; ++g2) {
-            if (g2 != grp) {
+            if (g2 != grp && AMUN_EXP != 3) {
               const unsigned long long w = thr_x[g2 * 128 + row_local];
               if ((uint32_t)(w >> 32) == tag) shared_kth = fmaxf(shared_kth, o2f((uint32_t)w));
             }
           }
           const float before = st.l[KB - 1];
           st.chunk32r(x, p.v_offset + v0 + c0, fmaxf(hintv, shared_kth));
-          if (st.l[KB - 1] > before) *my_thr = ((unsigned long long)tag << 32) | f2o(st.l[KB - 1]);
+          if (AMUN_EXP != 3 && st.l[KB - 1] > before) *my_thr = ((unsigned long long)tag << 32) | f2o(st.l[KB - 1]);
         }
       }
     }
@@ -199,7 +201,7 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
       // publish our k-th best only if it beats what is already known (with
       // many CTAs per row, e.g. one M-tile over 148 CTAs, unconditional
       // atomics would serialise on the row's word)
-      if (st.l[KB - 1] > published && st.l[KB - 1] > hintv) {
+      if (AMUN_EXP != 3 && st.l[KB - 1] > published && st.l[KB - 1] > hintv) {
         published = st.l[KB - 1];
         atomicMax(p.hint + row, hint_encode(published, gen));
       }
