@@ -266,6 +266,10 @@ amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b
     tp.hint = reinterpret_cast<unsigned long long*>(static_cast<char*>(workspace) + pl->slots_bytes);
     tp.gen_ctr = reinterpret_cast<unsigned int*>(static_cast<char*>(workspace) + pl->slots_bytes +
                                                  pl->hint_bytes);
+    // cross-CTA hints pay off only when a CTA's range holds several tiles: with
+    // ~2 (cfg greedy) they arrive too late and their atomics contend (148
+    // publishers per row word)
+    tp.use_hint = sch.C >= 4 * TC_BN ? 1 : 0;
     if (mode == 0 && pl->hint_ws != workspace) {
       // hint words carry the launch generation (advanced on the device by the
       // kernel itself); zero words + counters once per workspace

@@ -145,6 +145,22 @@ struct RowState {
       s += ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
     }
     if constexpr (!TOPK) return;
+    if constexpr (KB == 1) {
+      // Alg. 4 / Alg. 5 "if p' > max: best <- i", per chunk: only the chunk
+      // maximum can replace the best; its token is the lowest index holding
+      // it. Entries below the hint (a proven lower bound) are not offered.
+      if (cm != kNegInf && cm >= hint && cm >= l[0]) {
+        uint32_t msk = 0;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) msk |= (x[j] == cm) ? (1u << j) : 0u;
+        const int id = vbase + __ffs(msk) - 1;
+        if (better_lv(cm, id, l[0], v[0])) {
+          l[0] = cm;
+          v[0] = id;
+        }
+      }
+      return;
+    }
     const float thr = l[KB - 1];
     float tg = (hint > thr) ? hint : thr;     // candidates: x >= tg (full key decides ties)
     if constexpr (KB <= 8) {

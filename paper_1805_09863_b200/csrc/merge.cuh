@@ -140,25 +140,37 @@ __device__ __forceinline__ void row_topk(const MergeParams& p, int r, int lane, 
       }
     }
   }
+  // records beyond the first 32 (many vocab splits per row, e.g. one M-tile
+  // over 148 CTAs): all of a record's fields are loaded before its entries
+  // are offered, so the loads of successive records do not wait on the
+  // insertions (no data-dependent early exit between loads)
   float M = m0;
-  for (int j = lane + 32; j < n; j += 32) {   // > 32 records: fold the extra ones in
+#pragma unroll 2
+  for (int j = lane + 32; j < n; j += 32) {
     const float* rec = base + j * js;
     M = fmaxf(M, rec[0]);
-    for (int i = 0; i < p.k_max; ++i) {
-      const int vi = __float_as_int(rec[2 + p.k_max + i]);
-      if (vi < 0) break;
-      const float li = rec[2 + i];
-      if (!better_lv(li, vi, lst.l[KB - 1], lst.v[KB - 1])) break;
-      lst.insert(li, vi);
+    float rl[KB];
+    int rv[KB];
+#pragma unroll
+    for (int i = 0; i < KB; ++i) {
+      rl[i] = i < p.k_max ? rec[2 + i] : kNegInf;
+      rv[i] = i < p.k_max ? __float_as_int(rec[2 + p.k_max + i]) : -1;
+    }
+#pragma unroll
+    for (int i = 0; i < KB; ++i) {   // a record is sorted: stop at its first loser
+      if (rv[i] < 0 || !better_lv(rl[i], rv[i], lst.l[KB - 1], lst.v[KB - 1])) break;
+      lst.insert(rl[i], rv[i]);
     }
   }
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
   float Z = (m0 != kNegInf) ? s0 * expf(m0 - M) : 0.f;
+#pragma unroll 4
   for (int j = lane + 32; j < n; j += 32) {
     const float* rec = base + j * js;
     const float mj = rec[0];
-    if (mj != kNegInf) Z += rec[1] * expf(mj - M);
+    const float sj = rec[1];
+    if (mj != kNegInf) Z += sj * expf(mj - M);
   }
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) Z += __shfl_xor_sync(0xffffffffu, Z, o);

@@ -23,6 +23,7 @@ struct TcParams {
   int stride, k_max;
   float* __restrict__ logits; // MODE 1: [N][V_local]
   unsigned long long* __restrict__ hint;   // [N] cross-CTA k-th-best hints
+  int use_hint;                            // 0: CTA ranges too short to profit from them
   unsigned int* __restrict__ gen_ctr;      // {generation, CTAs done}: device-side, so every
                                            // launch (graph replays too) gets a fresh tag
 };
@@ -132,7 +133,7 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
     // (per-chunk exchange halves the insertions but its loads and atomics cost
     // as much as it saves: DESIGN.md §6.1)
     unsigned long long hraw = 0ull;
-    if (MODE == 0 && row < p.N && !last) hraw = __ldcg(p.hint + row);
+    if (MODE == 0 && p.use_hint && row < p.N && !last) hraw = __ldcg(p.hint + row);
     mbar_wait(&bfull[tile % TC_NBIAS], (uint32_t)(tile / TC_NBIAS) & 1u);
     mbar_wait(&tfull[acc], acc_phase);
     tc_fence_after();
@@ -197,10 +198,11 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
     }
-    if (MODE == 0 && row < p.N) {
+    if (MODE == 0 && p.use_hint && row < p.N && !last) {
       // publish our k-th best only if it beats what is already known (with
       // many CTAs per row, e.g. one M-tile over 148 CTAs, unconditional
-      // atomics would serialise on the row's word)
+      // atomics would serialise on the row's word); never after the segment's
+      // last tile (the other CTAs of the row are finishing too)
       if (AMUN_EXP != 3 && st.l[KB - 1] > published && st.l[KB - 1] > hintv) {
         published = st.l[KB - 1];
         atomicMax(p.hint + row, hint_encode(published, gen));
