@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
       while (it.next(mt, v0, width, last)) {
         if (lane == 0) bias_ring_load(p, sbias, bfull, tile, v0, width);
         for (int kb = 0; kb < p.n_kblk; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_wait_spin(&empty[stage], phase ^ 1);
           if (lane == 0) {
             mbar_arrive_expect_tx(&full[stage], TC_A_BYTES + TC_B_BYTES);
             tma_load_2d(&tmX, &full[stage], sA + stage * TC_A_BYTES, kb * TC_BK, mt * TC_BM, pol_x);
@@ -134,12 +134,12 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
       int acc = 0;
       uint32_t acc_phase = 0;
       while (it.next(mt, v0, width, last)) {
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        mbar_wait_spin(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + acc * TC_BN;
         const uint32_t idesc = idesc_bf16_f32(TC_BM, width);
         for (int kb = 0; kb < p.n_kblk; ++kb) {
-          mbar_wait(&full[stage], phase);
+          mbar_wait_spin(&full[stage], phase);
           tc_fence_after();
           if (lane == 0) {
             const uint64_t ad = sdesc_k_sw128(smem_u32(sA + stage * TC_A_BYTES));

@@ -107,7 +107,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<NG>::kThreads,
         const int vb = v0 + (int)rank * (width >> 1);   // this CTA's half of the B tile
         if (lane == 0) bias_ring_load(p, sbias, bfull, tile, v0, width);
         for (int kb = 0; kb < p.n_kblk; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_wait_spin(&empty[stage], phase ^ 1);
           if (lane == 0) {
             if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * (TC2_A_BYTES + TC2_B_BYTES));
             const uint32_t lb = mapa_shared(smem_u32(&full[stage]), 0);
@@ -132,12 +132,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<NG>::kThreads,
       int acc = 0;
       uint32_t acc_phase = 0;
       while (it.next(mp, v0, width, last)) {
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        mbar_wait_spin(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + acc * TC_BN;
         const uint32_t idesc = idesc_bf16_f32(2 * TC_BM, width);
         for (int kb = 0; kb < p.n_kblk; ++kb) {
-          mbar_wait(&full[stage], phase);
+          mbar_wait_spin(&full[stage], phase);
           tc_fence_after();
           if (lane == 0) {
             const uint64_t ad = sdesc_k_sw128(smem_u32(sA + stage * TC2_A_BYTES));

@@ -72,6 +72,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 #endif
+// Spin variant for the single-thread pipeline roles (TMA producer, MMA
+// issuer): no suspend-time hint, so the next copy / MMA issues as soon as
+// the phase completes.
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+#ifdef AMUN_NO_SPIN
+  mbar_wait(bar, parity);
+#else
+  uint32_t addr = smem_u32(bar);
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "WAITS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra WAITS_%=;\n\t}" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+#endif
+}
 
 // ------------------------------------------------------------- TMA
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* m) {
