@@ -151,6 +151,20 @@ amun_status amun_merge_partials(amun_ol* plan, const float* partials, int G,
                                 const int32_t* k_per_sentence, int k, int64_t* out_idx,
                                 float* out_cost, void* stream);
 
+/* Greedy decoding, Alg. 5 "argmax_1best": for every
+ * row, the token with the largest biased logit, WITHOUT the softmax (it is
+ * monotone, so the argmax needs no exp; observation 1). Ties go to
+ * the lowest token id (reading G3).
+ *   X, W, b      as amun_output_layer (single GPU: v_offset = 0 plans only
+ *                give global ids when V_local = V_total).
+ *   out_token    [N] int64: the winning token id (v_offset + v).
+ *   out_logit    [N] fp32: its biased logit (W x + b)[token] (NOT a log-prob).
+ * Same fused kernel with the softmax statistics compiled out and k = 1,
+ * then a per-row argmax over the vocab-split records. Enqueues 2 kernels.
+ * Errors: EINVAL for N < 0, N > max_rows or NULL outputs with N > 0. */
+amun_status amun_argmax(amun_ol* plan, const void* X, const void* W, const float* b, int N,
+                        int64_t* out_token, float* out_logit, void* workspace, void* stream);
+
 /* Test hook: steps 1-2 only. Writes the biased logits of the same tcgen05
  * (bf16) or SIMT (f32) GEMM to logits [N, V_local] fp32 (these never reach
  * HBM on the real path). For bit-exact GEMM checks in the integer regime. */
@@ -160,7 +174,8 @@ amun_status amun_debug_logits(amun_ol* plan, const void* X, const void* W, const
 /* Benchmark hook (the analogue of the paper's Table 4 breakdown):
  * the same fused kernel with part of the epilogue compiled out.
  *   variant 2: bare GEMM, the epilogue only drains the TMEM accumulators;
- *   variant 3: GEMM + bias + online max/sum-of-exp, no k-best.
+ *   variant 3: GEMM + bias + online max/sum-of-exp, no k-best;
+ *   variant 4: the first kernel of amun_argmax alone (k = 1, no exp).
  * Results are meaningless scratch in `workspace`; bf16 plans only. */
 amun_status amun_bench_variant(amun_ol* plan, const void* X, const void* W, const float* b,
                                int N, int variant, void* workspace, void* stream);

@@ -157,10 +157,24 @@ class OutputLayer:
         return out_idx, out_cost
 
     def bench_variant(self, X, W, b, variant: int):
-        """Benchmark hook: 2 = bare GEMM, 3 = GEMM + bias + softmax stats (no k-best)."""
+        """Benchmark hook: 2 = bare GEMM, 3 = GEMM + bias + softmax stats (no k-best),
+        4 = the argmax (Alg. 5) fused kernel alone."""
         N = self._check_scores(X, W, b)
         check(_L.amun_bench_variant(self._h, _ptr(X), _ptr(W), _ptr(b), N, variant,
                                     _ptr(self.workspace), _stream(self.device)))
+
+    def argmax(self, X, W, b, out_token=None, out_logit=None):
+        """Greedy decoding, Alg. 5: per row the token with the
+        largest biased logit (lowest id on ties), no softmax. Returns
+        (token [N] int64, logit [N] fp32 = (W x + b)[token])."""
+        N = self._check_scores(X, W, b)
+        if out_token is None:
+            out_token = torch.empty(N, dtype=torch.int64, device=self.device)
+        if out_logit is None:
+            out_logit = torch.empty(N, dtype=torch.float32, device=self.device)
+        check(_L.amun_argmax(self._h, _ptr(X), _ptr(W), _ptr(b), N, _ptr(out_token),
+                             _ptr(out_logit), _ptr(self.workspace), _stream(self.device)))
+        return out_token, out_logit
 
     def debug_logits(self, X, W, b):
         """Test hook: the biased logits [N, V_local] of the same GEMM."""

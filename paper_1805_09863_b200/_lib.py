@@ -21,7 +21,7 @@ EXPORTS = [
     "amun_abi_version", "amun_last_error", "amun_status_string", "amun_ol_create",
     "amun_ol_destroy", "amun_ol_workspace_bytes", "amun_ol_partial_stride",
     "amun_output_layer", "amun_ol_scores", "amun_ol_select", "amun_output_layer_partial",
-    "amun_merge_partials", "amun_debug_logits", "amun_bench_variant", "amun_compact",
+    "amun_merge_partials", "amun_argmax", "amun_debug_logits", "amun_bench_variant", "amun_compact",
 ]
 
 
@@ -62,6 +62,7 @@ def load() -> ctypes.CDLL:
         "amun_ol_select": (st, [vp, vp, vp, vp, i32, i32, vp, i32, vp, vp, vp]),
         "amun_output_layer_partial": (st, [vp, vp, vp, vp, i32, vp, vp, vp]),
         "amun_merge_partials": (st, [vp, vp, i32, vp, vp, i32, i32, vp, i32, vp, vp, vp]),
+        "amun_argmax": (st, [vp, vp, vp, vp, i32, vp, vp, vp, vp]),
         "amun_debug_logits": (st, [vp, vp, vp, vp, i32, vp, vp, vp]),
         "amun_bench_variant": (st, [vp, vp, vp, vp, i32, i32, vp, vp]),
         "amun_compact": (st, [ctypes.POINTER(amun_column), i32, vp, i32, vp, i32, vp, vp, vp, vp, vp]),

@@ -192,11 +192,13 @@ amun_status launch_tc_ng(const CUtensorMap* mx, const CUtensorMap* mw, const TcP
     kern = mode == 0 ? ol_tc2_kernel<KB, 0, NG>
          : mode == 2 ? ol_tc2_kernel<KB, 2, NG>
          : mode == 3 ? ol_tc2_kernel<KB, 3, NG>
+         : mode == 4 ? ol_tc2_kernel<1, 4, NG>
                      : ol_tc2_kernel<1, 1, NG>;
   else
     kern = mode == 0 ? ol_tc_kernel<KB, 0, NG>
          : mode == 2 ? ol_tc_kernel<KB, 2, NG>
          : mode == 3 ? ol_tc_kernel<KB, 3, NG>
+         : mode == 4 ? ol_tc_kernel<1, 4, NG>
                      : ol_tc_kernel<1, 1, NG>;
   const int smem_bytes = pairs ? TC2_SMEM : TC_SMEM;
   // the warpgroup register hand-off needs the full launch pool (see TcCfg)
@@ -270,14 +272,14 @@ amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b
     // ~2 (cfg greedy) they arrive too late and their atomics contend (148
     // publishers per row word)
     tp.use_hint = sch.C >= 4 * TC_BN ? 1 : 0;
-    if (mode == 0 && pl->hint_ws != workspace) {
+    if ((mode == 0 || mode == 4) && pl->hint_ws != workspace) {
       // hint words carry the launch generation (advanced on the device by the
       // kernel itself); zero words + counters once per workspace
       CUDA_TRY(cudaMemsetAsync(tp.hint, 0, pl->hint_bytes + 256, st));
       pl->hint_ws = workspace;
     }
 #define TC_CALL(K) launch_tc<K>(pl, mx, mw, tp, grid, st, mode, pairs)
-    AMUN_KB_SWITCH(mode == 1 ? 1 : pl->kb, TC_CALL)
+    AMUN_KB_SWITCH(mode == 1 || mode == 4 ? 1 : pl->kb, TC_CALL)
 #undef TC_CALL
   } else {
     SimtParams sp;
@@ -293,6 +295,7 @@ amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b
     sp.stride = pl->stride;
     sp.k_max = pl->k_max;
     sp.logits = logits;
+    if (mode == 4) return launch_simt<1>(sp, grid, st, 0);   // argmax: the k = 1 records
 #define SIMT_CALL(K) launch_simt<K>(sp, grid, st, mode)
     AMUN_KB_SWITCH(mode == 1 ? 1 : pl->kb, SIMT_CALL)
 #undef SIMT_CALL
@@ -302,21 +305,14 @@ amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b
 template <int KB>
 amun_status launch_merge(const MergeParams& mp, bool rows, int grid, cudaStream_t st) {
   if (grid == 0) return AMUN_OK;
-  // Programmatic dependent launch: the merge grid may be scheduled while the
-  // fused kernel still runs; it waits (griddepcontrol.wait) for its results.
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(MS_WARPS * 32);
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  // Plain stream-ordered launch. Programmatic dependent launch (scheduling
+  // this grid early, waiting in griddepcontrol.wait) measured slower inside
+  // CUDA graphs: cfg beam 108.5 vs 107.0 us, greedy 20.5 vs 19.8 us
+  // (DESIGN.md §6.2).
   if (rows)
-    CUDA_TRY(cudaLaunchKernelEx(&cfg, merge_rows_kernel<KB>, mp));
+    merge_rows_kernel<KB><<<grid, MS_WARPS * 32, 0, st>>>(mp);
   else
-    CUDA_TRY(cudaLaunchKernelEx(&cfg, merge_sentences_kernel<KB>, mp));
+    merge_sentences_kernel<KB><<<grid, MS_WARPS * 32, 0, st>>>(mp);
   CUDA_TRY(cudaGetLastError());
   return AMUN_OK;
 }
@@ -543,11 +539,33 @@ amun_status amun_debug_logits(amun_ol* plan, const void* X, const void* W, const
   return run_scores(plan, X, W, b, N, workspace, logits, static_cast<cudaStream_t>(stream), 1);
 }
 
+amun_status amun_argmax(amun_ol* plan, const void* X, const void* W, const float* b, int N,
+                        int64_t* out_token, float* out_logit, void* workspace, void* stream) {
+  amun_status s = check_score_args(plan, X, W, b, N, workspace);
+  if (s != AMUN_OK) return s;
+  if (N > 0 && (!out_token || !out_logit)) return fail(AMUN_EINVAL, "NULL out_token / out_logit");
+  if (N == 0) return AMUN_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  s = run_scores(plan, X, W, b, N, workspace, nullptr, st, 4);
+  if (s != AMUN_OK) return s;
+  MergeParams mp = base_merge(plan);
+  int grid_unused;
+  mp.part = static_cast<const float*>(workspace);
+  mp.layout = use_pairs(plan, N) ? 2 : 0;
+  mp.sch = make_schedule(plan, N, &grid_unused);
+  mp.N = N;
+  // one warp per row (more CTAs spread the latency-bound reduction)
+  argmax_rows_kernel<<<(unsigned)N, 32, 0, st>>>(mp, reinterpret_cast<long long*>(out_token),
+                                                 out_logit);
+  CUDA_TRY(cudaGetLastError());
+  return AMUN_OK;
+}
+
 amun_status amun_bench_variant(amun_ol* plan, const void* X, const void* W, const float* b,
                                int N, int variant, void* workspace, void* stream) {
   amun_status s = check_score_args(plan, X, W, b, N, workspace);
   if (s != AMUN_OK) return s;
-  if (variant != 2 && variant != 3) return fail(AMUN_EINVAL, "variant %d not in {2, 3}", variant);
+  if (variant < 2 || variant > 4) return fail(AMUN_EINVAL, "variant %d not in {2, 3, 4}", variant);
   if (plan->dtype != AMUN_BF16) return fail(AMUN_EUNSUPPORTED, "variants exist for bf16 only");
   return run_scores(plan, X, W, b, N, workspace, nullptr, static_cast<cudaStream_t>(stream),
                     variant);

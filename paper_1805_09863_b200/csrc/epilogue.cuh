@@ -111,7 +111,7 @@ struct RowState {
   // statistics and gate; a candidate group's four values (x[g], x[g+8],
   // x[g+16], x[g+24]) are selected from registers by a 3-level select tree
   // and offered with the full tie key (ids arrive out of order).
-  template <bool TOPK = true>
+  template <bool TOPK = true, bool STATS = true>
   __device__ __forceinline__ void chunk32r(const float (&x)[32], int vbase, float hint) {
     float t[16];
 #pragma unroll
@@ -121,7 +121,7 @@ struct RowState {
     for (int j = 0; j < 8; ++j) g[j] = fmaxf(t[j], t[j + 8]);
     const float cm = fmaxf(fmaxf(fmaxf(g[0], g[4]), fmaxf(g[1], g[5])),
                            fmaxf(fmaxf(g[2], g[6]), fmaxf(g[3], g[7])));
-    if (cm != kNegInf) {
+    if (STATS && cm != kNegInf) {   // (STATS = false: Alg. 5 argmax only, no exp)
       if (cm > m) {
         s *= ex2((m - cm) * kLog2e);
         m = cm;

@@ -204,7 +204,6 @@ constexpr int MS_CAP = 256;   // candidates ranked per batch of rows
 
 template <int KB>
 __global__ void __launch_bounds__(MS_WARPS * 32) merge_rows_kernel(const MergeParams p) {
-  pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = blockIdx.x * MS_WARPS + warp;
   if (r >= p.N) return;
@@ -219,6 +218,48 @@ __global__ void __launch_bounds__(MS_WARPS * 32) merge_rows_kernel(const MergePa
   if (lane < p.k_max) {
     rec[2 + lane] = l;
     rec[2 + p.k_max + lane] = __int_as_float(v);
+  }
+}
+
+// Alg. 5 reduce (P:244-251 with k = 1, no normalisation): one warp per row,
+// the best (l desc, v asc) entry 0 over the row's vocab-split records.
+__global__ void __launch_bounds__(32) argmax_rows_kernel(const MergeParams p,
+                                                                    long long* __restrict__ tok,
+                                                                    float* __restrict__ logit) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (r >= p.N) return;
+  const float* base;
+  long long js;
+  int n;
+  row_splits(p, r, base, js, n);
+  // up to 8 records per lane are loaded before any is reduced (independent
+  // loads in flight; the row's records are 128 * stride floats apart)
+  unsigned long long best = 0ull;
+  for (int j0 = 0; j0 < n; j0 += 8 * 32) {
+    float l[8];
+    int v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int j = j0 + u * 32 + lane;
+      l[u] = kNegInf;
+      v[u] = -1;
+      if (j < n) {
+        const float* rec = base + j * js;
+        l[u] = __ldcg(rec + 2);
+        v[u] = __float_as_int(__ldcg(rec + 2 + p.k_max));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const unsigned long long key = lv_key(l[u], v[u]);
+      best = key > best ? key : best;
+    }
+  }
+  best = warp_max_u64(best);
+  if (lane == 0) {
+    tok[r] = best ? (long long)(0x7fffffff - (int)(uint32_t)best) : -1LL;
+    logit[r] = best ? o2f((uint32_t)(best >> 32)) : kNegInf;
   }
 }
 
@@ -237,8 +278,7 @@ __global__ void __launch_bounds__(MS_WARPS * 32) merge_sentences_kernel(const Me
   const int r0 = p.offsets[s], r1 = p.offsets[s + 1];
   const int ks = p.k_s ? min(p.k_s[s], p.k) : p.k;
   float pc = 0.f;
-  if (r0 + warp < r1) pc = p.prev_cost[r0 + warp];   // before the PDL wait
-  pdl_wait();
+  if (r0 + warp < r1) pc = p.prev_cost[r0 + warp];
   const int nrows = r1 - r0;
   const int rows_per_batch = max(1, MS_CAP / p.k_max);
   int keep = 0;

@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
     }
     for (int i = 0; i < TC_NBIAS; ++i) mbar_init(&bfull[i], 1);
     fence_barrier_init();
-    *gen_smem = (MODE == 0) ? read_generation(p.gen_ctr) : 0u;
+    *gen_smem = (MODE == 0 || MODE == 4) ? read_generation(p.gen_ctr) : 0u;
   }
   if (role == 1) {
     tmem_alloc(tmem_holder, 512);
@@ -89,7 +89,6 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
   const uint32_t gen = *gen_smem;   // this launch's hint tag
-  pdl_trigger();   // let the dependent merge grid get scheduled early (it waits for us)
 
   const long long start = (long long)blockIdx.x * p.sch.C;
   const long long stop = min(start + p.sch.C, p.sch.total);
@@ -173,7 +172,7 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
     tc_fence_after();
     tmem_dealloc(tmem_base, 512);
   }
-  if (MODE == 0 && threadIdx.x == 0) finish_generation(p.gen_ctr);
+  if ((MODE == 0 || MODE == 4) && threadIdx.x == 0) finish_generation(p.gen_ctr);
 }
 
 }  // namespace amun

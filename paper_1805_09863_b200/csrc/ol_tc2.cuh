@@ -76,7 +76,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<NG>::kThreads,
     }
     for (int i = 0; i < TC_NBIAS; ++i) mbar_init(&bfull[i], 1);
     fence_barrier_init();
-    *gen_smem = (MODE == 0) ? read_generation(p.gen_ctr) : 0u;
+    *gen_smem = (MODE == 0 || MODE == 4) ? read_generation(p.gen_ctr) : 0u;
   }
   if (role == 1) {
     tmem_alloc_2sm(tmem_holder, 512);
@@ -87,7 +87,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<NG>::kThreads,
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
   const uint32_t gen = *gen_smem;
-  pdl_trigger();
 
   const long long start = (long long)pair * p.sch.C;
   const long long stop = min(start + p.sch.C, p.sch.total);
@@ -171,7 +170,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<NG>::kThreads,
     tc_fence_after();
     tmem_dealloc_2sm(tmem_base, 512);
   }
-  if (MODE == 0 && threadIdx.x == 0) finish_generation(p.gen_ctr);
+  if ((MODE == 0 || MODE == 4) && threadIdx.x == 0) finish_generation(p.gen_ctr);
 }
 
 }  // namespace amun

@@ -133,7 +133,7 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
     // (per-chunk exchange halves the insertions but its loads and atomics cost
     // as much as it saves: DESIGN.md §6.1)
     unsigned long long hraw = 0ull;
-    if (MODE == 0 && p.use_hint && row < p.N && !last) hraw = __ldcg(p.hint + row);
+    if ((MODE == 0 || MODE == 4) && p.use_hint && row < p.N && !last) hraw = __ldcg(p.hint + row);
     mbar_wait(&bfull[tile % TC_NBIAS], (uint32_t)(tile / TC_NBIAS) & 1u);
     mbar_wait(&tfull[acc], acc_phase);
     tc_fence_after();
@@ -185,7 +185,7 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
             }
           }
           const float before = st.l[KB - 1];
-          st.chunk32r(x, p.v_offset + v0 + c0, fmaxf(hintv, shared_kth));
+          st.template chunk32r<true, MODE != 4>(x, p.v_offset + v0 + c0, fmaxf(hintv, shared_kth));
           if (AMUN_EXP != 3 && st.l[KB - 1] > before) *my_thr = ((unsigned long long)tag << 32) | f2o(st.l[KB - 1]);
         }
       }
@@ -198,7 +198,7 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
     }
-    if (MODE == 0 && p.use_hint && row < p.N && !last) {
+    if ((MODE == 0 || MODE == 4) && p.use_hint && row < p.N && !last) {
       // publish our k-th best only if it beats what is already known (with
       // many CTAs per row, e.g. one M-tile over 148 CTAs, unconditional
       // atomics would serialise on the row's word); never after the segment's

@@ -91,4 +91,5 @@ def test_null_plan_calls(lib):
     assert lib.amun_ol_workspace_bytes(None) == 0
     assert lib.amun_ol_partial_stride(None) == 0
     assert lib.amun_ol_scores(None, None, None, None, 1, None, None) == 1
+    assert lib.amun_argmax(None, None, None, None, 1, None, None, None, None) == 1
     assert lib.amun_merge_partials(None, None, 1, None, None, 0, 0, None, 1, None, None, None) == 1

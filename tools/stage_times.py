@@ -81,6 +81,13 @@ def main():
           f"+k-best (full fused) {g_sc:.1f} us")
     print(f"{name}: GRAPH scores {g_sc:.1f} us | select {g_sel:.1f} us | both {g_all:.1f} us | "
           f"tiny kernel {g_empty:.1f} us")
+    if w.dtype == "bf16":
+        ot = torch.empty(w.N, dtype=torch.int64, device=dev)
+        ob = torch.empty(w.N, dtype=torch.float32, device=dev)
+        g_am = graph_time(lambda: ol.argmax(X, W, b, out_token=ot, out_logit=ob), reps=5)
+        g_v4 = graph_time(lambda: ol.bench_variant(X, W, b, 4), reps=5)
+        print(f"{name}: GRAPH argmax-only path (Alg. 5: fused kernel without exp + row argmax) "
+              f"{g_am:.1f} us | its fused kernel alone {g_v4:.1f} us")
 
 
 if __name__ == "__main__":
