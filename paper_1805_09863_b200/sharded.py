@@ -53,20 +53,27 @@ class ShardedOutputLayer:
         # kernels of ours per step (the NCCL all-gather kernel is not counted)
         self.launches_per_step = 2 if world == 1 else 3
 
-    def __call__(self, X, W, b, prev_cost, beam_offsets, k, k_per_sentence=None, events=None):
+    def __call__(self, X, W, b, prev_cost, beam_offsets, k, k_per_sentence=None, events=None,
+                 out_idx=None, out_cost=None):
         """W, b: this rank's shard. events: optional (start, stop) CUDA events
-        recorded around the fused GEMM kernel (stage 1) on the current stream."""
+        recorded around the fused GEMM kernel (stage 1) on the current stream.
+        out_idx / out_cost: optional preallocated [S, k] outputs."""
+        if self.world == 1 and not events:   # one C-ABI call (amun_output_layer)
+            return self.ol(X, W, b, prev_cost, beam_offsets, k, k_per_sentence,
+                           out_idx=out_idx, out_cost=out_cost)
         if self.world == 1:
             if events:
                 events[0].record()
             self.ol.scores(X, W, b)
             if events:
                 events[1].record()
-            return self.ol.select(X.shape[0], prev_cost, beam_offsets, k, k_per_sentence)
+            return self.ol.select(X.shape[0], prev_cost, beam_offsets, k, k_per_sentence,
+                                  out_idx=out_idx, out_cost=out_cost)
         if events:
             events[0].record()
         part = self.ol.partial(X, W, b)
         if events:
             events[1].record()
         allp = exchange(part, self.world, self.group)
-        return self.ol.merge(allp, prev_cost, beam_offsets, k, k_per_sentence)
+        return self.ol.merge(allp, prev_cost, beam_offsets, k, k_per_sentence,
+                             out_idx=out_idx, out_cost=out_cost)
