@@ -37,7 +37,7 @@ import numpy as np
 
 __all__ = [
     "as_f64", "gemm", "add_bias", "softmax_3pass_stats", "log_softmax",
-    "find_best", "kbest_sentences", "output_layer", "shard_partial",
+    "find_best", "kbest_sentences", "output_layer", "shard_partial", "beam_advance",
     "combine_partials", "online_stats", "argmax_1best", "argmax_1best_parallel",
     "compact", "decode_work",
 ]
@@ -256,6 +256,45 @@ def compact(columns, alive, beam_offsets):
     S_alive = sum(1 for s in range(len(o) - 1) if new_off[s + 1] > new_off[s])
     return (new_cols, np.array(new_off, np.int32), np.array(src_row, np.int32),
             len(src_row), S_alive)
+
+
+def beam_advance(out_idx, out_cost, V_total: int, eos: int, columns):
+    """One beam-search step after the selection (SPEC S:324-331 expand_beam +
+    Alg. 2 "if h = EOS: remove h from b"): sentence s's winners, in
+    their rank order, are out_idx[s, i] = r * V_total + v (-1 = padding) with
+    cost out_cost[s, i]. A winner whose token v is EOS moves to the finished
+    set and frees its slot; every other winner becomes a hypothesis of the
+    next batch, in rank order, carrying its parent row r's state, its token v
+    and its cost:
+        j = 0; for s: new_offsets[s] = j
+                      for i: if idx >= 0 and v != eos:
+                                 src_row[j] = r; token[j] = v; cost[j] = c; j += 1
+    `columns`: list of 2-D uint8 arrays [N, row_bytes] (gathered by src_row).
+    Returns (new_columns, new_offsets[S+1], src_row, token, cost, N', S_alive,
+    finished = [(s, i, r, v, cost)] for the EOS winners)."""
+    idx = np.asarray(out_idx, np.int64)
+    cst = np.asarray(out_cost, np.float32)
+    S, k = idx.shape
+    src_row, token, cost, new_off, finished = [], [], [], [], []
+    for s in range(S):
+        new_off.append(len(src_row))
+        for i in range(k):
+            e = int(idx[s, i])
+            if e < 0:
+                continue
+            r, v = divmod(e, V_total)
+            if v == eos:
+                finished.append((s, i, r, v, float(cst[s, i])))
+            else:
+                src_row.append(r)
+                token.append(v)
+                cost.append(cst[s, i])
+    new_off.append(len(src_row))
+    new_cols = [np.asarray(c)[src_row] if src_row else np.asarray(c)[:0] for c in columns]
+    S_alive = sum(1 for s in range(S) if new_off[s + 1] > new_off[s])
+    return (new_cols, np.array(new_off, np.int32), np.array(src_row, np.int32),
+            np.array(token, np.int32), np.array(cost, np.float32), len(src_row), S_alive,
+            finished)
 
 
 def decode_work(finish_steps, beam: int, mode: str) -> int:

@@ -112,6 +112,56 @@ def test_spec_expand_beam():
     assert idx[0].tolist() == [0, 2]                     # (r0, v0), (r1, v0)
 
 
+def test_beam_advance_spec_and_hand_example():
+    """SPEC S:331 (beam 2 keeps {-1.0, -1.5}) and S:332 (an EOS winner
+    finishes its hypothesis and frees its slot), then a hand-worked batch:
+    EOS in the middle, padding, and one parent chosen twice."""
+    V, eos = 10, 2
+    cols = [np.arange(4 * 8, dtype=np.uint8).reshape(4, 8)]
+    # S:331: winners (slot0, v0) -1.0 and (slot1, v0) -1.5 -> both continue
+    out = O.beam_advance([[0 * V + 0, 1 * V + 0]], [[-1.0, -1.5]], V, eos, cols)
+    ncols, off, src, tok, cost, n, s_alive, fin = out
+    assert src.tolist() == [0, 1] and tok.tolist() == [0, 0] and cost.tolist() == [-1.0, -1.5]
+    assert off.tolist() == [0, 2] and n == 2 and s_alive == 1 and fin == []
+    # S:332: the best candidate is EOS at beam 1 -> the sentence finishes
+    out = O.beam_advance([[0 * V + eos]], [[-0.5]], V, eos, cols)
+    assert out[5] == 0 and out[6] == 0 and out[1].tolist() == [0, 0]
+    assert out[7] == [(0, 0, 0, eos, -0.5)]
+    # hand example: 3 sentences, k = 3
+    idx = [[1 * V + 7, 0 * V + eos, 1 * V + 3],     # s0 rows 0-1: (1,7), EOS, (1,3): parent 1 twice
+           [-1, -1, -1],                             # s1: no candidates
+           [3 * V + 5, 2 * V + eos, -1]]             # s2 rows 2-3: (3,5), EOS, pad
+    cst = [[-1.0, -2.0, -3.0], [-np.inf] * 3, [-0.5, -0.7, -np.inf]]
+    ncols, off, src, tok, cost, n, s_alive, fin = O.beam_advance(idx, cst, V, eos, cols)
+    assert src.tolist() == [1, 1, 3] and tok.tolist() == [7, 3, 5]
+    assert cost.tolist() == [-1.0, -3.0, -0.5]
+    assert off.tolist() == [0, 2, 2, 3] and n == 3 and s_alive == 2
+    assert [f[:4] for f in fin] == [(0, 1, 0, eos), (2, 1, 2, eos)]
+    assert np.array_equal(ncols[0], cols[0][[1, 1, 3]])
+
+
+def test_beam_advance_reduces_to_compact():
+    """Invariant tying the two Alg. 2 oracles together: when sentence s's i-th
+    winner continues its own slot (parent = o_s + i), advancing the beam is
+    exactly the stable compaction by the non-EOS mask (compact is pinned by
+    SPEC S:339-341 independently)."""
+    rng = np.random.default_rng(3)
+    V, eos, S, k = 50, 7, 40, 4
+    N = S * k
+    tok = rng.integers(0, V, N)
+    tok[rng.random(N) < 0.3] = eos
+    idx = (np.arange(N) * V + tok).reshape(S, k)
+    cst = rng.normal(size=(S, k)).astype(np.float32)
+    cols = [rng.integers(0, 256, (N, 24), dtype=np.uint8)]
+    ncols, off, src, t2, c2, n, s_alive, fin = O.beam_advance(idx, cst, V, eos, cols)
+    alive = (tok != eos).astype(np.uint8)
+    ccols, coff, csrc, cn, cs_alive = O.compact(cols, alive, np.arange(S + 1) * k)
+    assert np.array_equal(ncols[0], ccols[0]) and np.array_equal(src, csrc)
+    assert np.array_equal(off, coff) and n == cn and s_alive == cs_alive
+    assert np.array_equal(t2, tok[alive == 1]) and np.array_equal(c2, cst.reshape(-1)[alive == 1])
+    assert len(fin) == N - n
+
+
 def test_spec_compact_examples():
     for e in _load("spec_examples.json")["compact_states"]:
         rows = np.array([[ord(c)] * 16 for c in e["rows"]], np.uint8)
