@@ -206,6 +206,38 @@ amun_status amun_compact(const amun_column* cols, int n_cols, const uint8_t* ali
                          const int32_t* beam_offsets, int S, int32_t* new_beam_offsets,
                          int32_t* src_row, int32_t* counts, int32_t* counts_host, void* stream);
 
+/* Beam advance (SPEC S:324-332 expand_beam + Alg. 2 "if h =
+ * EOS: remove h from b"): one step of beam-search bookkeeping after
+ * the selection, replacing "reorder by parent, then compact" with one
+ * gather. Sentence s's winners, in rank order, are out_idx[s, i] =
+ * r * V_total + v (-1 = padding) with cost out_cost[s, i] (the outputs of
+ * amun_output_layer). A winner whose token v == eos_token finishes (it stays
+ * readable in out_idx / out_cost; the caller keeps it as a finished
+ * hypothesis) and frees its slot; every other winner becomes row j of the
+ * next batch, in sentence order then rank order:
+ *   src_row[j] = r (its parent row in the current batch of N rows),
+ *   new_token[j] = v, new_cost[j] = out_cost[s, i],
+ *   dst rows j of every column = src rows r (duplicated when two winners
+ *   share a parent),
+ *   new_beam_offsets[s] = number of next-batch rows of sentences < s,
+ *   counts = {N', S_alive} on the device (counts_host: optional host copy,
+ *   implies a stream synchronisation; otherwise nothing syncs).
+ *   out_idx [S, k] int64, out_cost [S, k] fp32, device; 0 <= S, 1 <= k,
+ *   S * k <= 2^30; V_total >= 1.
+ *   cols    as amun_compact, src [N, row_bytes], dst [>= S*k, row_bytes],
+ *           non-overlapping.
+ *   src_row, new_token [>= S*k] int32; new_cost [>= S*k] fp32; device.
+ *   workspace  amun_beam_advance_workspace_bytes(S, k) bytes, 256-byte
+ *           aligned, device scratch (winner flags, parents, tokens).
+ * Enqueues 2 kernels (classify, then the compaction gather). EINVAL on
+ * argument errors (nothing enqueued). */
+size_t amun_beam_advance_workspace_bytes(int S, int k);
+amun_status amun_beam_advance(const int64_t* out_idx, const float* out_cost, int S, int k,
+                              int64_t V_total, int eos_token, int N, const amun_column* cols,
+                              int n_cols, int32_t* new_beam_offsets, int32_t* src_row,
+                              int32_t* new_token, float* new_cost, int32_t* counts,
+                              int32_t* counts_host, void* workspace, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

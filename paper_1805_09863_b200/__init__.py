@@ -222,3 +222,53 @@ def compact(columns, alive, beam_offsets, new_offsets=None, src_row=None, counts
     if sync:
         return int(host[0]), int(host[1]), new_offsets, src_row, counts
     return None, None, new_offsets, src_row, counts
+
+
+def beam_advance(out_idx, out_cost, V_total: int, eos: int, N: int, columns=(), sync: bool = True,
+                 out=None):
+    """Beam advance (SPEC S:324-332 expand_beam + Alg. 2): from the selected
+    winners out_idx / out_cost [S, k] (amun_output_layer's outputs), the next
+    batch = every non-EOS winner, in sentence then rank order, with its parent
+    row's state gathered from each (src [N, ...], dst [>= S*k, ...]) column.
+    Returns (N', S_alive, new_offsets [S+1], src_row, new_token, new_cost,
+    counts); with sync=False the first two are None (no host sync)."""
+    dev = out_idx.device
+    S, k = out_idx.shape
+    _need(out_idx, "out_idx", torch.int64, dev, (S, k))
+    _need(out_cost, "out_cost", torch.float32, dev, (S, k))
+    n = max(S * k, 1)
+    if out is None:
+        out = {}
+    def buf(name, size, dtype):
+        t = out.get(name)
+        return torch.empty(size, dtype=dtype, device=dev) if t is None else t
+    new_offsets = buf("new_offsets", S + 1, torch.int32)
+    src_row = buf("src_row", n, torch.int32)
+    new_token = buf("new_token", n, torch.int32)
+    new_cost = buf("new_cost", n, torch.float32)
+    counts = buf("counts", 2, torch.int32)
+    ws = out.get("workspace")
+    if ws is None:
+        ws = torch.empty(max(_L.amun_beam_advance_workspace_bytes(S, k), 256), dtype=torch.uint8,
+                         device=dev)
+    if len(columns) > AMUN_MAX_COLUMNS:
+        raise ValueError(f"at most {AMUN_MAX_COLUMNS} columns per call")
+    arr = (_lib.amun_column * max(1, len(columns)))()
+    for i, (src, dst) in enumerate(columns):
+        if src.shape[0] != N or not src.is_contiguous() or not dst.is_contiguous():
+            raise ValueError(f"column {i}: src must have N rows; src/dst contiguous")
+        rb = src.element_size()
+        for d in src.shape[1:]:
+            rb *= int(d)
+        if dst.numel() * dst.element_size() < rb * S * k:
+            raise ValueError(f"column {i}: dst must hold S*k rows")
+        arr[i] = _lib.amun_column(src.data_ptr(), dst.data_ptr(), rb)
+    host = (ctypes.c_int32 * 2)() if sync else None
+    check(_L.amun_beam_advance(_ptr(out_idx), _ptr(out_cost), S, k, V_total, eos, N, arr,
+                               len(columns), _ptr(new_offsets), _ptr(src_row), _ptr(new_token),
+                               _ptr(new_cost), _ptr(counts),
+                               ctypes.cast(host, ctypes.c_void_p) if sync else None, _ptr(ws),
+                               _stream(dev)))
+    if sync:
+        return int(host[0]), int(host[1]), new_offsets, src_row, new_token, new_cost, counts
+    return None, None, new_offsets, src_row, new_token, new_cost, counts

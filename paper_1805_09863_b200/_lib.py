@@ -22,6 +22,7 @@ EXPORTS = [
     "amun_ol_destroy", "amun_ol_workspace_bytes", "amun_ol_partial_stride",
     "amun_output_layer", "amun_ol_scores", "amun_ol_select", "amun_output_layer_partial",
     "amun_merge_partials", "amun_argmax", "amun_debug_logits", "amun_bench_variant", "amun_compact",
+    "amun_beam_advance_workspace_bytes", "amun_beam_advance",
 ]
 
 
@@ -66,6 +67,10 @@ def load() -> ctypes.CDLL:
         "amun_debug_logits": (st, [vp, vp, vp, vp, i32, vp, vp, vp]),
         "amun_bench_variant": (st, [vp, vp, vp, vp, i32, i32, vp, vp]),
         "amun_compact": (st, [ctypes.POINTER(amun_column), i32, vp, i32, vp, i32, vp, vp, vp, vp, vp]),
+        "amun_beam_advance_workspace_bytes": (sz, [i32, i32]),
+        "amun_beam_advance": (st, [vp, vp, i32, i32, ctypes.c_int64, i32, i32,
+                                   ctypes.POINTER(amun_column), i32, vp, vp, vp, vp, vp, vp, vp,
+                                   vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

@@ -571,42 +571,43 @@ amun_status amun_bench_variant(amun_ol* plan, const void* X, const void* W, cons
                     variant);
 }
 
-amun_status amun_compact(const amun_column* cols, int n_cols, const uint8_t* alive, int N,
-                         const int32_t* beam_offsets, int S, int32_t* new_beam_offsets,
-                         int32_t* src_row, int32_t* counts, int32_t* counts_host, void* stream) {
+}  // extern "C"
+
+namespace {
+// Validate and copy the state columns: src holds n_src rows, dst receives up
+// to n_dst rows; src and dst ranges must not overlap.
+amun_status fill_columns(CompactParams& cp, const amun_column* cols, int n_cols, long long n_src,
+                         long long n_dst) {
   if (n_cols < 0 || n_cols > AMUN_MAX_COLUMNS)
     return fail(AMUN_EINVAL, "n_cols=%d out of [0, %d]", n_cols, AMUN_MAX_COLUMNS);
   if (n_cols > 0 && !cols) return fail(AMUN_EINVAL, "NULL cols");
-  if (N < 0 || S < 0) return fail(AMUN_EINVAL, "negative N or S");
-  if (!beam_offsets || !new_beam_offsets || !counts) return fail(AMUN_EINVAL, "NULL offsets/counts");
-  if (N > 0 && (!alive || !src_row)) return fail(AMUN_EINVAL, "NULL alive/src_row");
-  CompactParams cp;
-  memset(&cp, 0, sizeof(cp));
   for (int c = 0; c < n_cols; ++c) {
     const amun_column& col = cols[c];
     if (col.row_bytes <= 0 || (col.row_bytes & 3))
       return fail(AMUN_EINVAL, "column %d: row_bytes=%lld must be a positive multiple of 4", c,
                   (long long)col.row_bytes);
-    if (N > 0 && (!col.src || !col.dst)) return fail(AMUN_EINVAL, "column %d: NULL src/dst", c);
+    if ((n_src > 0 || n_dst > 0) && (!col.src || !col.dst))
+      return fail(AMUN_EINVAL, "column %d: NULL src/dst", c);
     if (((reinterpret_cast<uintptr_t>(col.src) | reinterpret_cast<uintptr_t>(col.dst)) & 3) != 0)
       return fail(AMUN_EINVAL, "column %d: src/dst must be 4-byte aligned", c);
     const uintptr_t s0 = reinterpret_cast<uintptr_t>(col.src), d0 = reinterpret_cast<uintptr_t>(col.dst);
-    const uintptr_t len = (uintptr_t)col.row_bytes * (uintptr_t)N;
-    if (N > 0 && s0 < d0 + len && d0 < s0 + len)
+    const uintptr_t ls = (uintptr_t)col.row_bytes * (uintptr_t)n_src;
+    const uintptr_t ld = (uintptr_t)col.row_bytes * (uintptr_t)n_dst;
+    if (ls > 0 && ld > 0 && s0 < d0 + ld && d0 < s0 + ls)
       return fail(AMUN_EINVAL, "column %d: src and dst overlap", c);
     cp.col[c].src = static_cast<const uint8_t*>(col.src);
     cp.col[c].dst = static_cast<uint8_t*>(col.dst);
     cp.col[c].row_bytes = col.row_bytes;
   }
   cp.n_cols = n_cols;
+  return AMUN_OK;
+}
+
+amun_status launch_compact(CompactParams& cp, int N, int S, int32_t* counts, int32_t* counts_host,
+                           cudaStream_t st) {
   cp.N = N;
   cp.S = S;
-  cp.alive = alive;
-  cp.offsets = beam_offsets;
-  cp.new_offsets = new_beam_offsets;
-  cp.src_row = src_row;
   cp.counts = counts;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
   cp.per = (int)cdiv(cdiv(N > 0 ? N : 1, CP_THREADS), 16) * 16;
   const int grid = (int)std::max<long long>(
       1, std::max<long long>(cdiv(N, CP_ROWS), cdiv((long long)S + 1, CP_THREADS)));
@@ -617,6 +618,74 @@ amun_status amun_compact(const amun_column* cols, int n_cols, const uint8_t* ali
     CUDA_TRY(cudaStreamSynchronize(st));
   }
   return AMUN_OK;
+}
+
+long long a256(long long n) { return (n + 255) / 256 * 256; }
+}  // namespace
+
+extern "C" {
+
+amun_status amun_compact(const amun_column* cols, int n_cols, const uint8_t* alive, int N,
+                         const int32_t* beam_offsets, int S, int32_t* new_beam_offsets,
+                         int32_t* src_row, int32_t* counts, int32_t* counts_host, void* stream) {
+  if (N < 0 || S < 0) return fail(AMUN_EINVAL, "negative N or S");
+  if (!beam_offsets || !new_beam_offsets || !counts) return fail(AMUN_EINVAL, "NULL offsets/counts");
+  if (N > 0 && (!alive || !src_row)) return fail(AMUN_EINVAL, "NULL alive/src_row");
+  CompactParams cp;
+  memset(&cp, 0, sizeof(cp));
+  amun_status s = fill_columns(cp, cols, n_cols, N, N);
+  if (s != AMUN_OK) return s;
+  cp.alive = alive;
+  cp.offsets = beam_offsets;
+  cp.new_offsets = new_beam_offsets;
+  cp.src_row = src_row;
+  return launch_compact(cp, N, S, counts, counts_host, static_cast<cudaStream_t>(stream));
+}
+
+size_t amun_beam_advance_workspace_bytes(int S, int k) {
+  if (S < 0 || k < 1) return 0;
+  const long long n = (long long)S * k;
+  return (size_t)(a256(n) + 2 * a256(4 * n));
+}
+
+amun_status amun_beam_advance(const int64_t* out_idx, const float* out_cost, int S, int k,
+                              int64_t V_total, int eos_token, int N, const amun_column* cols,
+                              int n_cols, int32_t* new_beam_offsets, int32_t* src_row,
+                              int32_t* new_token, float* new_cost, int32_t* counts,
+                              int32_t* counts_host, void* workspace, void* stream) {
+  if (S < 0 || k < 1 || N < 0) return fail(AMUN_EINVAL, "S=%d, k=%d, N=%d: need S >= 0, k >= 1, N >= 0", S, k, N);
+  if (V_total < 1) return fail(AMUN_EINVAL, "V_total=%lld must be >= 1", (long long)V_total);
+  if (!new_beam_offsets || !counts) return fail(AMUN_EINVAL, "NULL new_beam_offsets/counts");
+  const long long n = (long long)S * k;
+  if (n > (1LL << 30)) return fail(AMUN_EINVAL, "S*k=%lld too large", n);
+  if (n > 0 && (!out_idx || !out_cost || !src_row || !new_token || !new_cost || !workspace))
+    return fail(AMUN_EINVAL, "NULL out_idx/out_cost/src_row/new_token/new_cost/workspace");
+  if ((reinterpret_cast<uintptr_t>(workspace) & 255) != 0)
+    return fail(AMUN_EINVAL, "workspace must be 256-byte aligned");
+  CompactParams cp;
+  memset(&cp, 0, sizeof(cp));
+  amun_status s = fill_columns(cp, cols, n_cols, N, n);
+  if (s != AMUN_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint8_t* live = static_cast<uint8_t*>(workspace);
+  int* parent = reinterpret_cast<int*>(live + a256(n));
+  int* tok = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(parent) + a256(4 * n));
+  if (n > 0) {
+    beam_classify_kernel<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(
+        reinterpret_cast<const long long*>(out_idx), (int)n, (long long)V_total, eos_token, live,
+        parent, tok);
+    CUDA_TRY(cudaGetLastError());
+  }
+  cp.alive = live;
+  cp.off_stride = k;
+  cp.new_offsets = new_beam_offsets;
+  cp.src_row = src_row;
+  cp.parent = parent;
+  cp.vtok = tok;
+  cp.vcost = out_cost;
+  cp.tok_out = new_token;
+  cp.cost_out = new_cost;
+  return launch_compact(cp, (int)n, S, counts, counts_host, st);
 }
 
 #if AMUN_EXP == 4

@@ -13,6 +13,9 @@
 //   * computes new_beam_offsets[s] for s = b*256 + t, ... (a prefix query is
 //     the thread-run prefix + a vectorised count inside one run);
 //   * (CTA 0 only) counts the sentences with a live row -> counts[1].
+// The same kernel advances a beam (amun_beam_advance): the flags are the
+// sentences' selected winner slots (offsets s * k), and each surviving slot
+// gathers its PARENT row's state (SPEC S:324-331 expand_beam + Alg. 2).
 #pragma once
 #include <cstdint>
 
@@ -41,11 +44,38 @@ struct CompactParams {
   CompactCol col[CP_MAXCOLS];
   int n_cols, N, S, per;         // per = flags per thread run (multiple of 16)
   const uint8_t* __restrict__ alive;
-  const int* __restrict__ offsets;
+  const int* __restrict__ offsets;   // [S+1]; unused when off_stride > 0
+  int off_stride;                    // > 0: offsets[s] = s * off_stride (beam advance)
   int* __restrict__ new_offsets;
   int* __restrict__ src_row;
   int* __restrict__ counts;      // {N', S_alive}, written by CTA 0
+  // beam advance (amun_beam_advance): flag i is winner slot i of a sentence;
+  // the state columns are gathered from parent[i], and the winner's token
+  // and cost are written too. All NULL for plain compaction.
+  const int* __restrict__ parent;
+  const int* __restrict__ vtok;
+  const float* __restrict__ vcost;
+  int* __restrict__ tok_out;
+  float* __restrict__ cost_out;
 };
+
+// Beam advance, step 1: classify every selected winner i (one thread each):
+// live = valid and not EOS, parent row r and token v of idx = r * V_total + v.
+__global__ void beam_classify_kernel(const long long* __restrict__ idx, int n, long long V_total,
+                                     int eos, uint8_t* __restrict__ live, int* __restrict__ parent,
+                                     int* __restrict__ tok) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const long long e = idx[i];
+  int r = 0, v = -1;
+  if (e >= 0) {
+    r = (int)(e / V_total);
+    v = (int)(e - (long long)r * V_total);
+  }
+  live[i] = (e >= 0 && v != eos) ? 1 : 0;
+  parent[i] = r;
+  tok[i] = v;
+}
 
 // number of nonzero bytes in [a, b) of the flag array (a % 16 == 0); the
 // partial last word is read whole when it lies inside [0, n) and masked
@@ -108,6 +138,7 @@ __device__ __forceinline__ int block_excl_scan(int v, int* warp_sums, int& total
 __global__ void __launch_bounds__(CP_THREADS, 6) compact_kernel(const CompactParams p) {
   __shared__ int warp_sums[CP_THREADS / 32];
   __shared__ int map[CP_ROWS];
+  __shared__ int gsrc[CP_ROWS];      // gather source row of output row d0 + t
   __shared__ int thr_excl[CP_THREADS];
   const int tid = threadIdx.x;
   const int per = p.per;
@@ -155,13 +186,14 @@ __global__ void __launch_bounds__(CP_THREADS, 6) compact_kernel(const CompactPar
 
   // new beam offsets, spread over all CTAs; CTA 0 alone also counts the
   // sentences still alive (no cross-CTA atomics, so no counts reset needed)
+  auto off_at = [&](int s) { return p.off_stride > 0 ? s * p.off_stride : p.offsets[s]; };
   auto prefix = [&](int row) {
     if (row >= p.N) return total;
     const int t0 = row / per;
     return thr_excl[t0] + count_alive(p.alive, t0 * per, row, p.N);
   };
   for (int s = blockIdx.x * CP_THREADS + tid; s <= p.S; s += gridDim.x * CP_THREADS)
-    p.new_offsets[s] = prefix(p.offsets[s]);
+    p.new_offsets[s] = prefix(off_at(s));
   if (blockIdx.x == 0) {
     // thread t owns sentences [t q, t q + q); boundaries are evaluated eight
     // at a time so their loads are independent (the count is one CTA's job)
@@ -171,7 +203,7 @@ __global__ void __launch_bounds__(CP_THREADS, 6) compact_kernel(const CompactPar
     for (int base = tid * q; base < s_end; base += 8) {
       int v[9];
 #pragma unroll
-      for (int i = 0; i < 9; ++i) v[i] = (base + i <= s_end) ? prefix(p.offsets[base + i]) : 0;
+      for (int i = 0; i < 9; ++i) v[i] = (base + i <= s_end) ? prefix(off_at(base + i)) : 0;
 #pragma unroll
       for (int i = 0; i < 8; ++i) local_alive += (base + i < s_end) && (v[i + 1] > v[i]);
     }
@@ -186,7 +218,15 @@ __global__ void __launch_bounds__(CP_THREADS, 6) compact_kernel(const CompactPar
 
   const int nrows = d1 - d0;
   if (nrows <= 0) return;
-  if (tid < nrows) p.src_row[d0 + tid] = map[tid];
+  if (tid < nrows) {
+    const int v = map[tid];
+    const int src = p.parent ? p.parent[v] : v;
+    gsrc[tid] = src;
+    p.src_row[d0 + tid] = src;
+    if (p.tok_out) p.tok_out[d0 + tid] = p.vtok[v];
+    if (p.cost_out) p.cost_out[d0 + tid] = p.vcost[v];
+  }
+  __syncthreads();
 
   // Gather: the CTA's nrows x n4 16-byte units of each column (unit u -> row
   // d0 + u / n4, word u % n4), CP_UNROLL independent loads in flight per
@@ -209,7 +249,7 @@ __global__ void __launch_bounds__(CP_THREADS, 6) compact_kernel(const CompactPar
           const int uu = u + q * CP_THREADS;
           if (uu < hi) {
             const int j = uu / n4;
-            t[q] = __ldg(src + (long long)map[j] * n4 + (uu - j * n4));
+            t[q] = __ldg(src + (long long)gsrc[j] * n4 + (uu - j * n4));
           }
         }
 #pragma unroll
@@ -224,7 +264,7 @@ __global__ void __launch_bounds__(CP_THREADS, 6) compact_kernel(const CompactPar
       int* dst = reinterpret_cast<int*>(col.dst) + base;
       for (int u = lo + tid; u < hi; u += CP_THREADS) {
         const int j = u / n1;
-        dst[u] = __ldg(src + (long long)map[j] * n1 + (u - j * n1));
+        dst[u] = __ldg(src + (long long)gsrc[j] * n1 + (u - j * n1));
       }
     }
   }

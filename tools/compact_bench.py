@@ -59,3 +59,47 @@ for name, alive in masks.items():
     res.append({"mask": name, "N_alive": n2, "us": round(us, 2), "GBps": round(byts / (us * 1e-6) / 1e9, 1),
                 "frac": round(byts / (us * 1e-6) / 1e9 / peak, 3)})
     print(json.dumps(res[-1]))
+
+# ---- beam advance (amun_beam_advance, NEXT f1): the cfg4 batch's winners
+# S x k = 1280 x 5 (parents inside each sentence's 5 rows, repeats allowed),
+# EOS fraction p; the same 4 state columns gathered by parent row.
+# Algorithmic bytes = S k (8 + 4) (winners) + 2 N' row_bytes + N' (4 + 4 + 4) + 4 (S + 1).
+gen = torch.Generator().manual_seed(7)
+dst_adv = [torch.empty_like(c) for c in cols]
+ws = torch.empty(max(amun._L.amun_beam_advance_workspace_bytes(S, B), 256), dtype=torch.uint8, device=dev)
+outs = {"new_offsets": torch.empty(S + 1, dtype=torch.int32, device=dev),
+        "src_row": torch.empty(N, dtype=torch.int32, device=dev),
+        "new_token": torch.empty(N, dtype=torch.int32, device=dev),
+        "new_cost": torch.empty(N, dtype=torch.float32, device=dev),
+        "counts": torch.empty(2, dtype=torch.int32, device=dev), "workspace": ws}
+V, EOS = 90000, 2
+for p in (0.0, 0.1, 0.5, 0.9):
+    parent = (torch.arange(S)[:, None] * B + torch.randint(0, B, (S, B), generator=gen))
+    tok = torch.randint(0, V, (S, B), generator=gen)
+    tok[torch.rand((S, B), generator=gen) < p] = EOS
+    idx = (parent * V + tok).to(dev)
+    cost = (-torch.rand((S, B), generator=gen) * 20).to(dev)
+
+    def call():
+        amun.beam_advance(idx, cost, V, EOS, N, list(zip(cols, dst_adv)), sync=False, out=outs)
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        call()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            for _ in range(50):
+                call()
+    g.replay()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    g.replay()
+    e.record()
+    torch.cuda.synchronize()
+    us = s.elapsed_time(e) / 50 * 1e3
+    n2 = int((tok != EOS).sum())
+    byts = S * B * 12 + 2 * n2 * row_bytes + n2 * 12 + 4 * (S + 1)
+    print(json.dumps({"beam_advance_eos_p": p, "N_next": n2, "us": round(us, 2),
+                      "GBps": round(byts / (us * 1e-6) / 1e9, 1),
+                      "frac": round(byts / (us * 1e-6) / 1e9 / peak, 3)}))
