@@ -123,6 +123,24 @@ amun_status amun_output_layer(amun_ol* plan, const void* X, const void* W, const
                               const int32_t* k_per_sentence, int k, int64_t* out_idx,
                               float* out_cost, void* workspace, void* stream);
 
+/* amun_output_layer with the row count in DEVICE memory:
+ * N = *N_dev, read by the kernels themselves (e.g. counts[0] written by
+ * amun_beam_advance or amun_compact), so a decode loop needs no host sync
+ * per step and can be captured in one CUDA graph.
+ *   X         [max_rows, H] bf16 (rows >= N are ignored), prev_cost [max_rows];
+ *   N_dev     device int32, clamped to [0, max_rows];
+ *   beam_offsets [S+1] device (o_S = N), other arguments as amun_output_layer.
+ * The fused kernel is launched with one CTA per SM and derives its schedule
+ * from N on the device (CTAs without work only take part in setup). The
+ * kernel is chosen from max_rows: CTA pairs (cta_group::2) when max_rows
+ * spans >= 9 M-tiles of 128 rows, else single CTAs. bf16 plans only
+ * (EUNSUPPORTED otherwise). Enqueues 2 kernels. */
+amun_status amun_output_layer_dev(amun_ol* plan, const void* X, const void* W, const float* b,
+                                  const float* prev_cost, const int32_t* beam_offsets,
+                                  const int32_t* N_dev, int S, const int32_t* k_per_sentence,
+                                  int k, int64_t* out_idx, float* out_cost, void* workspace,
+                                  void* stream);
+
 /* The two stages of amun_output_layer, exposed so a caller can time or
  * overlap them: stage 1 writes per-(row, vocab split) partial records into
  * `workspace`; stage 2 reads them (same N) and selects per sentence. */

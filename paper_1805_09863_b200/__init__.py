@@ -116,6 +116,23 @@ class OutputLayer:
                                    _stream(self.device)))
         return out_idx, out_cost
 
+    def call_dev(self, X, W, b, prev_cost, beam_offsets, N_dev, k: int, k_per_sentence=None,
+                 out_idx=None, out_cost=None):
+        """Steps 1-4 with the row count on the device (N = N_dev[0], no host
+        sync): X [max_rows, H], prev_cost [max_rows]; rows >= N are ignored."""
+        M = self.max_rows
+        _need(X, "X", self.tdtype, self.device, (M, self.H))
+        _need(W, "W", self.tdtype, self.device, (self.V_local, self.H))
+        _need(b, "b", torch.float32, self.device, (self.V_local,))
+        _need(N_dev, "N_dev", torch.int32, self.device)
+        S = self._check_select(prev_cost, beam_offsets, M, k_per_sentence)
+        out_idx, out_cost = self._outputs(S, k, out_idx, out_cost)
+        check(_L.amun_output_layer_dev(self._h, _ptr(X), _ptr(W), _ptr(b), _ptr(prev_cost),
+                                       _ptr(beam_offsets), _ptr(N_dev), S, _ptr(k_per_sentence), k,
+                                       _ptr(out_idx), _ptr(out_cost), _ptr(self.workspace),
+                                       _stream(self.device)))
+        return out_idx, out_cost
+
     def scores(self, X, W, b):
         """Stage 1 only (fused GEMM + bias + online softmax stats + row k-best)."""
         N = self._check_scores(X, W, b)

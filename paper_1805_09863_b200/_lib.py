@@ -20,7 +20,7 @@ AMUN_MAX_COLUMNS = 16
 EXPORTS = [
     "amun_abi_version", "amun_last_error", "amun_status_string", "amun_ol_create",
     "amun_ol_destroy", "amun_ol_workspace_bytes", "amun_ol_partial_stride",
-    "amun_output_layer", "amun_ol_scores", "amun_ol_select", "amun_output_layer_partial",
+    "amun_output_layer", "amun_output_layer_dev", "amun_ol_scores", "amun_ol_select", "amun_output_layer_partial",
     "amun_merge_partials", "amun_argmax", "amun_debug_logits", "amun_bench_variant", "amun_compact",
     "amun_beam_advance_workspace_bytes", "amun_beam_advance",
 ]
@@ -59,6 +59,7 @@ def load() -> ctypes.CDLL:
         "amun_ol_workspace_bytes": (sz, [vp]),
         "amun_ol_partial_stride": (i32, [vp]),
         "amun_output_layer": (st, [vp, vp, vp, vp, vp, vp, i32, i32, vp, i32, vp, vp, vp, vp]),
+        "amun_output_layer_dev": (st, [vp, vp, vp, vp, vp, vp, vp, i32, vp, i32, vp, vp, vp, vp]),
         "amun_ol_scores": (st, [vp, vp, vp, vp, i32, vp, vp]),
         "amun_ol_select": (st, [vp, vp, vp, vp, i32, i32, vp, i32, vp, vp, vp]),
         "amun_output_layer_partial": (st, [vp, vp, vp, vp, i32, vp, vp, vp]),

@@ -163,20 +163,10 @@ bool use_pairs(const amun_ol* pl, int N) {
 // Schedule over "units" of M rows: 128-row M-tiles for single CTAs, 256-row
 // pair tiles for CTA pairs (then *grid counts CTAs = 2 x pairs).
 Schedule make_schedule(const amun_ol* pl, int N, int* grid) {
-  Schedule s;
   const bool pairs = use_pairs(pl, N);
   const long long G = pairs ? pl->num_sms / 2 : pl->num_sms;
   const long long n_mt = cdiv(N > 0 ? N : 1, pairs ? 256 : 128);
-  s.Vp = cdiv(pl->V_local, 16) * 16;
-  const long long splits = G / n_mt;   // aligned mode: vocab splits per M-tile
-  if (splits >= 1 && n_mt * splits * 10 >= G * 9) {
-    s.C = cdiv(cdiv(s.Vp, splits), 16) * 16;
-    s.band = cdiv(s.Vp, s.C) * s.C;
-  } else {
-    s.C = cdiv(cdiv(n_mt * s.Vp, G), 16) * 16;
-    s.band = s.Vp;
-  }
-  s.total = n_mt * s.band;
+  Schedule s = schedule_for(n_mt, cdiv(pl->V_local, 16) * 16, G);
   const int units = (int)cdiv((n_mt - 1) * s.band + s.Vp, s.C);
   *grid = pairs ? 2 * units : units;
   return s;
@@ -241,14 +231,29 @@ amun_status launch_simt(const SimtParams& sp, int grid, cudaStream_t st, int mod
 
 // Stage 1: fused GEMM + epilogue into the workspace slots (mode 0) or the
 // debug logits (mode 1).
+// amun_output_layer_dev: CTA pairs or single CTAs must be chosen at launch,
+// without N; pairs when max_rows spans >= 9 M-tiles (the host rule for
+// large N), unless AMUN_PAIRS=off / force.
+bool dev_pairs(const amun_ol* pl) {
+  if (pl->dtype != AMUN_BF16 || pl->pairs_mode == 1) return false;
+  return pl->pairs_mode == 2 || cdiv(pl->max_rows, 128) >= 9;
+}
+
 amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b, int N,
-                       void* workspace, float* logits, cudaStream_t st, int mode) {
+                       void* workspace, float* logits, cudaStream_t st, int mode,
+                       const int* N_dev = nullptr) {
   if (N == 0) return AMUN_OK;
   CUDA_TRY(cudaSetDevice(pl->device));
   int grid;
   Schedule sch = make_schedule(pl, N, &grid);
+  if (N_dev) {   // N = max_rows here; every SM gets a CTA, the device picks the schedule
+    const bool dp = dev_pairs(pl);
+    sch = schedule_for(cdiv(N, dp ? 256 : 128), cdiv(pl->V_local, 16) * 16,
+                       dp ? pl->num_sms / 2 : pl->num_sms);
+    grid = dp ? pl->num_sms / 2 * 2 : pl->num_sms;
+  }
   if (pl->dtype == AMUN_BF16) {
-    const bool pairs = use_pairs(pl, N);
+    const bool pairs = N_dev ? dev_pairs(pl) : use_pairs(pl, N);
     const CUtensorMap *mx, *mw;
     amun_status s = get_map(pl, pl->xmaps, 4, pl->xnext, X, N, TC_BM, &mx);
     if (s != AMUN_OK) return s;
@@ -272,6 +277,8 @@ amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b
     // ~2 (cfg greedy) they arrive too late and their atomics contend (148
     // publishers per row word)
     tp.use_hint = sch.C >= 4 * TC_BN ? 1 : 0;
+    tp.N_dev = N_dev;
+    tp.num_sms = pl->num_sms;
     if ((mode == 0 || mode == 4) && pl->hint_ws != workspace) {
       // hint words carry the launch generation (advanced on the device by the
       // kernel itself); zero words + counters once per workspace
@@ -484,6 +491,42 @@ amun_status amun_output_layer(amun_ol* plan, const void* X, const void* W, const
   if (s != AMUN_OK) return s;
   return amun_ol_select(plan, workspace, prev_cost, beam_offsets, N, S, k_per_sentence, k,
                         out_idx, out_cost, stream);
+}
+
+amun_status amun_output_layer_dev(amun_ol* plan, const void* X, const void* W, const float* b,
+                                  const float* prev_cost, const int32_t* beam_offsets,
+                                  const int32_t* N_dev, int S, const int32_t* k_per_sentence,
+                                  int k, int64_t* out_idx, float* out_cost, void* workspace,
+                                  void* stream) {
+  if (!plan) return fail(AMUN_EINVAL, "NULL plan");
+  if (!N_dev) return fail(AMUN_EINVAL, "NULL N_dev");
+  if (plan->dtype != AMUN_BF16) return fail(AMUN_EUNSUPPORTED, "device-side N: bf16 plans only");
+  const int Nmax = plan->max_rows;
+  amun_status s = check_score_args(plan, X, W, b, Nmax, workspace);
+  if (s != AMUN_OK) return s;
+  s = check_select_args(plan, prev_cost, beam_offsets, Nmax, S, k, out_idx, out_cost);
+  if (s != AMUN_OK) return s;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  s = run_scores(plan, X, W, b, Nmax, workspace, nullptr, st, 0, N_dev);
+  if (s != AMUN_OK) return s;
+  if (S == 0) return AMUN_OK;
+  MergeParams mp = base_merge(plan);
+  mp.part = static_cast<const float*>(workspace);
+  const bool dp = dev_pairs(plan);
+  mp.layout = dp ? 2 : 0;
+  mp.sch = schedule_for(cdiv(Nmax, dp ? 256 : 128), cdiv(plan->V_local, 16) * 16,
+                        dp ? plan->num_sms / 2 : plan->num_sms);
+  mp.N = Nmax;
+  mp.N_dev = N_dev;
+  mp.num_sms = plan->num_sms;
+  mp.S = S;
+  mp.prev_cost = prev_cost;
+  mp.offsets = beam_offsets;
+  mp.k_s = k_per_sentence;
+  mp.k = k;
+  mp.out_idx = reinterpret_cast<long long*>(out_idx);
+  mp.out_cost = out_cost;
+  return run_merge(plan, mp, false, S, st);
 }
 
 amun_status amun_output_layer_partial(amun_ol* plan, const void* X, const void* W,

@@ -388,6 +388,26 @@ struct Schedule {
   __device__ __forceinline__ long long last_cta(int mt) const { return (mt * band + Vp - 1) / C; }
 };
 
+// The persistent schedule over n_mt row units x Vp vocab columns for G CTAs
+// (or CTA pairs): aligned vocab splits (every unit cut at the same
+// boundaries, so concurrent CTAs share W tiles in L2) when they fill >= 90%
+// of G, else an equal flattened split. Shared by the host (plan) and the
+// device (amun_output_layer_dev, where N is only known on the device).
+__host__ __device__ inline Schedule schedule_for(long long n_mt, long long Vp, long long G) {
+  Schedule s;
+  s.Vp = Vp;
+  const long long splits = G / n_mt;
+  if (splits >= 1 && n_mt * splits * 10 >= G * 9) {
+    s.C = ((Vp + splits - 1) / splits + 15) / 16 * 16;
+    s.band = (Vp + s.C - 1) / s.C * s.C;
+  } else {
+    s.C = ((n_mt * Vp + G - 1) / G + 15) / 16 * 16;
+    s.band = Vp;
+  }
+  s.total = n_mt * s.band;
+  return s;
+}
+
 struct TileIter {
   long long pos, end;
   Schedule sch;

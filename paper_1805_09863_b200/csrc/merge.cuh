@@ -34,7 +34,22 @@ struct MergeParams {
   long long* __restrict__ out_idx;
   float* __restrict__ out_cost;
   float* __restrict__ out_part;  // ROW mode: [N][stride]
+  const int* __restrict__ N_dev; // amun_output_layer_dev: N on the device (layout 0), else NULL
+  int num_sms;
 };
+
+// amun_output_layer_dev: the row count and the fused kernel's schedule are
+// resolved on the device (the same schedule_for as the fused kernel).
+__device__ __forceinline__ MergeParams merge_dyn(const MergeParams& p) {
+  MergeParams q = p;
+  if (p.N_dev) {
+    q.N = max(0, min(*p.N_dev, p.N));
+    const int unit = p.layout == 2 ? 256 : 128;   // layout 2: CTA-pair units
+    q.sch = schedule_for((max(q.N, 1) + unit - 1) / unit, p.sch.Vp,
+                         p.layout == 2 ? p.num_sms / 2 : p.num_sms);
+  }
+  return q;
+}
 
 __device__ __forceinline__ void row_splits(const MergeParams& p, int r, const float*& base,
                                            long long& jstride, int& n) {
@@ -269,7 +284,8 @@ __global__ void __launch_bounds__(32) argmax_rows_kernel(const MergeParams p,
 // rows' candidates are ranked by counting better ones (ranks are unique), and
 // the best k stay at the front for the next batch.
 template <int KB>
-__global__ void __launch_bounds__(MS_WARPS * 32) merge_sentences_kernel(const MergeParams p) {
+__global__ void __launch_bounds__(MS_WARPS * 32) merge_sentences_kernel(const MergeParams p0) {
+  const MergeParams p = merge_dyn(p0);
   __shared__ Cand pool[KB + MS_CAP];
   __shared__ Cand best[KB];
   __shared__ int s_valid;

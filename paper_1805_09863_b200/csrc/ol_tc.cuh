@@ -90,8 +90,9 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
   const uint32_t tmem_base = *tmem_holder;
   const uint32_t gen = *gen_smem;   // this launch's hint tag
 
-  const long long start = (long long)blockIdx.x * p.sch.C;
-  const long long stop = min(start + p.sch.C, p.sch.total);
+  const TcDyn dyn = tc_dyn<false>(p);      // N (and the schedule) from the device in _dev mode
+  const long long start = (long long)blockIdx.x * dyn.sch.C;
+  const long long stop = min(start + dyn.sch.C, dyn.sch.total);
 
   if (role >= 0) {
     reg_dealloc<Cfg::kCtrlRegs>();
@@ -99,7 +100,7 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
       // ------------------------------------------------ TMA producer
       // The whole warp walks the schedule (keeps it converged); lane 0 issues.
       const uint64_t pol_x = policy_evict_last();     // X is re-read by every CTA
-      TileIter it{start, stop, p.sch};
+      TileIter it{start, stop, dyn.sch};
       int mt, v0, width;
       bool last;
       int stage = 0, tile = 0;
@@ -125,7 +126,7 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
       // ------------------------------------------------ MMA issuer
       // The whole warp waits; lane 0 issues tcgen05.mma and the commits (a
       // commit tracks the MMAs issued by the same thread).
-      TileIter it{start, stop, p.sch};
+      TileIter it{start, stop, dyn.sch};
       int mt, v0, width;
       bool last;
       int stage = 0;
@@ -163,7 +164,7 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
   } else {
     reg_alloc<Cfg::kEpiRegs>();
     tc_epilogue<KB, MODE, NG, false>(p, tmem_base, start, stop, tfull, tempty, bfull, sbias, xch,
-                                     thr_x, gen, warp, lane, 0u, (long long)blockIdx.x);
+                                     thr_x, gen, warp, lane, 0u, (long long)blockIdx.x, dyn);
   }
 
   tc_fence_before();

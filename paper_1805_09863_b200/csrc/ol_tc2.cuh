@@ -88,15 +88,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<NG>::kThreads,
   const uint32_t tmem_base = *tmem_holder;
   const uint32_t gen = *gen_smem;
 
-  const long long start = (long long)pair * p.sch.C;
-  const long long stop = min(start + p.sch.C, p.sch.total);
+  const TcDyn dyn = tc_dyn<true>(p);       // N (and the schedule) from the device in _dev mode
+  const long long start = (long long)pair * dyn.sch.C;
+  const long long stop = min(start + dyn.sch.C, dyn.sch.total);
 
   if (role >= 0) {
     reg_dealloc<Cfg::kCtrlRegs>();
     if (role == 0) {
       // ------------------------------------------------ TMA producer (both CTAs)
       const uint64_t pol_x = policy_evict_last();
-      TileIter it{start, stop, p.sch};
+      TileIter it{start, stop, dyn.sch};
       int mp, v0, width;
       bool last;
       int stage = 0, tile = 0;
@@ -123,7 +124,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<NG>::kThreads,
       }
     } else if (role == 1 && rank == 0) {
       // ------------------------------------------------ MMA issuer (leader only)
-      TileIter it{start, stop, p.sch};
+      TileIter it{start, stop, dyn.sch};
       int mp, v0, width;
       bool last;
       int stage = 0;
@@ -161,7 +162,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<NG>::kThreads,
   } else {
     reg_alloc<Cfg::kEpiRegs>();
     tc_epilogue<KB, MODE, NG, true>(p, tmem_base, start, stop, tfull, tempty, bfull, sbias, xch,
-                                    thr_x, gen, warp, lane, rank, (long long)pair);
+                                    thr_x, gen, warp, lane, rank, (long long)pair, dyn);
   }
 
   tc_fence_before();

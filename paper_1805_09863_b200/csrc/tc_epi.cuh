@@ -26,7 +26,28 @@ struct TcParams {
   int use_hint;                            // 0: CTA ranges too short to profit from them
   unsigned int* __restrict__ gen_ctr;      // {generation, CTAs done}: device-side, so every
                                            // launch (graph replays too) gets a fresh tag
+  const int* __restrict__ N_dev;           // amun_output_layer_dev: N on the device (else NULL)
+  int num_sms;                             // the device schedule's CTA count
 };
+
+// Per-launch values that amun_output_layer_dev only knows on the device:
+// the row count, the schedule derived from it and the hint switch.
+struct TcDyn {
+  int N, use_hint;
+  Schedule sch;
+};
+template <bool PAIR>
+__device__ __forceinline__ TcDyn tc_dyn(const TcParams& p) {
+  TcDyn d{p.N, p.use_hint, p.sch};
+  if (p.N_dev) {
+    d.N = max(0, min(*p.N_dev, p.N));      // p.N = max_rows
+    const int unit = PAIR ? 2 * 128 : 128;  // rows per schedule unit (a CTA pair: 256)
+    d.sch = schedule_for((max(d.N, 1) + unit - 1) / unit, p.sch.Vp, PAIR ? p.num_sms / 2 : p.num_sms);
+    if (d.N == 0) d.sch.total = 0;          // nothing to do: every CTA range is empty
+    d.use_hint = d.sch.C >= 4 * 256 ? 1 : 0;
+  }
+  return d;
+}
 
 constexpr int TC_BM = 128;
 #ifndef TC_BN_OVERRIDE
@@ -97,7 +118,8 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
                                             long long stop, uint64_t* tfull, uint64_t* tempty,
                                             uint64_t* bfull, const float* sbias, float* xch,
                                             unsigned long long* thr_x, uint32_t gen, int warp,
-                                            int lane, uint32_t rank, long long slot_base) {
+                                            int lane, uint32_t rank, long long slot_base,
+                                            const TcDyn dyn) {
   const int grp = warp >> 2;                       // epilogue warps are 0 .. 4NG-1
   const int q = warp & 3;                          // TMEM lane quadrant of this warp
   const int row_local = q * 32 + lane;
@@ -109,7 +131,7 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
   }
   RowState<KB> st;
   st.reset();
-  TileIter it{start, stop, p.sch};
+  TileIter it{start, stop, dyn.sch};
   int unit, v0, width;
   bool last;
   int acc = 0, tile = 0;
@@ -124,7 +146,7 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
     const int mt = PAIR ? 2 * unit + (int)rank : unit;
     const uint32_t tag = (uint32_t)mt + 1u;
     const int row = mt * TC_BM + row_local;
-    const bool live = mt * TC_BM < p.N;            // warp-uniform (padding M-tile of a pair)
+    const bool live = mt * TC_BM < dyn.N;            // warp-uniform (padding M-tile of a pair)
     const int limit = min(width, p.V_local - v0);
     const int nch = (width + 31) >> 5;
     const float* bsl = sbias + (tile % TC_NBIAS) * TC_BN;
@@ -133,7 +155,7 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
     // (per-chunk exchange halves the insertions but its loads and atomics cost
     // as much as it saves: DESIGN.md §6.1)
     unsigned long long hraw = 0ull;
-    if ((MODE == 0 || MODE == 4) && p.use_hint && row < p.N && !last) hraw = __ldcg(p.hint + row);
+    if ((MODE == 0 || MODE == 4) && dyn.use_hint && row < dyn.N && !last) hraw = __ldcg(p.hint + row);
     mbar_wait(&bfull[tile % TC_NBIAS], (uint32_t)(tile / TC_NBIAS) & 1u);
     mbar_wait(&tfull[acc], acc_phase);
     tc_fence_after();
@@ -165,7 +187,7 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
           }
         }
         if constexpr (MODE == 1) {
-          if (row < p.N) {
+          if (row < dyn.N) {
             float* out = p.logits + (long long)row * p.V_local + v0 + c0;
             for (int j = 0; j < 32 && j < nv; ++j) out[j] = x[j];
           }
@@ -198,7 +220,7 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
     }
-    if ((MODE == 0 || MODE == 4) && p.use_hint && row < p.N && !last) {
+    if ((MODE == 0 || MODE == 4) && dyn.use_hint && row < dyn.N && !last) {
       // publish our k-th best only if it beats what is already known (with
       // many CTAs per row, e.g. one M-tile over 148 CTAs, unconditional
       // atomics would serialise on the row's word); never after the segment's
@@ -238,7 +260,7 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
           }
           named_bar_sync(5 + q, NG * 32);
         }
-        if (grp == 0 && row < p.N) {
+        if (grp == 0 && row < dyn.N) {
           const long long slot = PAIR ? (slot_base + unit) * 2 + rank : slot_base + unit;
           st.emit(p.part + (slot * TC_BM + row_local) * p.stride, p.k_max);
         }
