@@ -39,7 +39,8 @@ __all__ = [
     "as_f64", "gemm", "add_bias", "softmax_3pass_stats", "log_softmax",
     "find_best", "kbest_sentences", "output_layer", "shard_partial", "beam_advance",
     "combine_partials", "online_stats", "argmax_1best", "argmax_1best_parallel",
-    "compact", "decode_work",
+    "compact", "decode_work", "beam_advance", "e4m3_decode", "quantize_rows_e4m3",
+    "dequant_rows_e4m3",
 ]
 
 
@@ -295,6 +296,42 @@ def beam_advance(out_idx, out_cost, V_total: int, eos: int, columns):
     return (new_cols, np.array(new_off, np.int32), np.array(src_row, np.int32),
             np.array(token, np.int32), np.array(cost, np.float32), len(src_row), S_alive,
             finished)
+
+
+# ---------------------------------------------------------------- FP8 (f4)
+def e4m3_decode(codes):
+    """OCP FP8 E4M3 ("fn": no infinities) code -> exact value, from the
+    format definition: sign = bit 7, exponent e = bits 3-6 (bias 7),
+    mantissa m = bits 0-2; e = 0: (-1)^s m/8 2^-6 (subnormal); e = 15, m = 7:
+    NaN; otherwise (-1)^s (1 + m/8) 2^(e-7). The modern analogue of the
+    paper's 16-bit storage (section 2.3)."""
+    c = np.asarray(codes, np.uint8).astype(np.int64)
+    sgn = np.where(c & 0x80, -1.0, 1.0)
+    e = (c >> 3) & 0xF
+    m = (c & 0x7).astype(np.float64)
+    val = np.where(e == 0, m / 8.0 * 2.0 ** -6, (1.0 + m / 8.0) * np.exp2(e.astype(np.float64) - 7))
+    val = np.where((e == 15) & (c & 0x7 == 7), np.nan, val)
+    return sgn * val
+
+
+def quantize_rows_e4m3(x):
+    """Per-row symmetric FP8 quantisation: scale_r = fl32(max_h |x_rh| / 448)
+    (1 if the row is all zero), code = RNE-to-E4M3(fl32(x_rh / scale_r)),
+    saturating at +-448. The E4M3 rounding step is a library primitive
+    (torch float8_e4m3fn conversion), pinned by brute force in
+    tests/test_oracle.py. Returns (codes uint8 [R, H], scale fp32 [R])."""
+    import torch
+    x32 = np.asarray(x, np.float32)
+    amax = np.abs(x32).max(axis=1) if x32.shape[1] else np.zeros(x32.shape[0], np.float32)
+    scale = np.where(amax > 0, amax / np.float32(448.0), np.float32(1.0)).astype(np.float32)
+    y = (x32 / scale[:, None]).astype(np.float32)
+    codes = torch.from_numpy(y).to(torch.float8_e4m3fn).view(torch.uint8).numpy()
+    return codes, scale
+
+
+def dequant_rows_e4m3(codes, scale):
+    """Exact fp64 value of code * scale (<= 4 + 24 significant bits)."""
+    return e4m3_decode(codes) * np.asarray(scale, np.float64)[:, None]
 
 
 def decode_work(finish_steps, beam: int, mode: str) -> int:

@@ -377,3 +377,49 @@ def test_compact_random(p):
     cols2, no2, src2, n2, _ = O.compact(cols, np.ones(n, np.uint8), no)
     assert np.array_equal(cols2[0], cols[0]) and src2.tolist() == list(range(n))
     assert no2.tolist() == no.tolist()
+
+
+# ------------------------------------------------------------------ FP8 (f4)
+def test_e4m3_decode_definition_points():
+    """Values fixed by the OCP E4M3 definition: 1.0 = 0x38, max 448 = 0x7E,
+    min normal 2^-6 = 0x08, min subnormal 2^-9 = 0x01, -0 = 0x80, NaN = 0x7F."""
+    d = O.e4m3_decode(np.array([0x38, 0x7E, 0x08, 0x01, 0x80, 0x00, 0xFE, 0x3C, 0x07], np.uint8))
+    assert d[:4].tolist() == [1.0, 448.0, 2.0 ** -6, 2.0 ** -9]
+    assert d[4] == 0.0 and np.signbit(d[4]) and d[5] == 0.0
+    assert d[6] == -448.0 and d[7] == 1.5 and d[8] == 7 / 8 * 2.0 ** -6
+    assert np.isnan(O.e4m3_decode(np.array([0x7F, 0xFF], np.uint8))).all()
+
+
+def test_e4m3_decode_matches_library_all_codes():
+    import torch
+    codes = np.array([c for c in range(256) if c not in (0x7F, 0xFF)], np.uint8)
+    lib = torch.from_numpy(codes).view(torch.float8_e4m3fn).to(torch.float64).numpy()
+    assert np.array_equal(O.e4m3_decode(codes), lib)
+
+
+def test_quantize_rows_e4m3_is_nearest_by_brute_force():
+    """Every code is the nearest of all 254 finite E4M3 values to x / scale
+    (ties: even mantissa), the row scale maps the row max to 448 exactly,
+    and representable inputs round-trip exactly."""
+    rng = np.random.default_rng(8)
+    x = (rng.normal(size=(6, 200)) * np.exp(rng.normal(size=(6, 1)) * 3)).astype(np.float32)
+    x[5] = 0.0
+    codes, scale = O.quantize_rows_e4m3(x)
+    finite = np.array([c for c in range(256) if c not in (0x7F, 0xFF)], np.uint8)
+    vals = O.e4m3_decode(finite)
+    y = (x / scale[:, None]).astype(np.float32).astype(np.float64)
+    got = O.e4m3_decode(codes)
+    for r in range(x.shape[0]):
+        for h in range(x.shape[1]):
+            dist = np.abs(vals - y[r, h])
+            best = dist.min()
+            assert abs(got[r, h] - y[r, h]) == best
+            cands = finite[dist == best]
+            if len(set(O.e4m3_decode(cands).tolist())) > 1:      # a true tie: even mantissa
+                assert codes[r, h] & 1 == 0
+    assert scale[5] == 1.0 and (codes[5] == 0).all()
+    assert np.allclose(np.abs(O.dequant_rows_e4m3(codes, scale)[:5]).max(axis=1),
+                       np.abs(x[:5]).max(axis=1), rtol=1e-6)
+    rep = O.e4m3_decode(np.array([[0x38, 0x30, 0x7E, 0x01]], np.uint8)).astype(np.float32)
+    c2, s2 = O.quantize_rows_e4m3(rep)
+    assert np.array_equal(O.dequant_rows_e4m3(c2, s2), rep.astype(np.float64))
