@@ -60,7 +60,7 @@ typedef enum amun_status {
   AMUN_ECUDA = 3          /* a CUDA runtime/driver call failed */
 } amun_status;
 
-typedef enum amun_dtype { AMUN_F32 = 0, AMUN_BF16 = 1 } amun_dtype;
+typedef enum amun_dtype { AMUN_F32 = 0, AMUN_BF16 = 1, AMUN_E4M3 = 2 } amun_dtype;
 
 /* Opaque plan: shapes, kernel choice, persistent-grid schedule and cached TMA
  * tensor maps. Not thread-safe: use one plan per host thread. */
@@ -182,6 +182,36 @@ amun_status amun_merge_partials(amun_ol* plan, const float* partials, int G,
  * Errors: EINVAL for N < 0, N > max_rows or NULL outputs with N > 0. */
 amun_status amun_argmax(amun_ol* plan, const void* X, const void* W, const float* b, int N,
                         int64_t* out_token, float* out_logit, void* workspace, void* stream);
+
+/* FP8 path (the modern analogue of the paper's 16-bit
+ * storage, section 2.3): X and W as OCP E4M3 codes with one fp32
+ * scale per row, the logits computed as
+ *   L[r][v] = (sum_h x8[r][h] w8[v][h]) * x_scale[r] * w_scale[v] + b[v]
+ * on tcgen05.mma kind::f8f6f4 (fp32 accumulation), then the same softmax /
+ * k-best / merge as amun_output_layer. Plan: amun_ol_create(..., AMUN_E4M3,
+ * ...), H % 16 == 0; single-CTA kernel.
+ *   X8 [N, H] uint8, x_scale [N] fp32, W8 [V_local, H] uint8, w_scale
+ *   [V_local] fp32 (16-byte aligned), other arguments as amun_output_layer.
+ * Enqueues 2 kernels. Parity: the oracle computes on the exactly dequantised
+ * values (oracle.dequant_rows_e4m3). */
+amun_status amun_output_layer_e4m3(amun_ol* plan, const uint8_t* X8, const float* x_scale,
+                                   const uint8_t* W8, const float* w_scale, const float* b,
+                                   const float* prev_cost, const int32_t* beam_offsets, int N,
+                                   int S, const int32_t* k_per_sentence, int k, int64_t* out_idx,
+                                   float* out_cost, void* workspace, void* stream);
+/* Stage 1 alone of amun_output_layer_e4m3 (then amun_ol_select), or with
+ * variant 2 / 3 the bare-GEMM / no-k-best benchmark builds (as
+ * amun_bench_variant). variant 0 = the real stage 1. */
+amun_status amun_ol_scores_e4m3(amun_ol* plan, const uint8_t* X8, const float* x_scale,
+                                const uint8_t* W8, const float* w_scale, const float* b, int N,
+                                int variant, void* workspace, void* stream);
+/* Per-row E4M3 quantisation: scale[r] = max_h |src[r][h]| / 448 (1 for an
+ * all-zero row), dst[r][h] = RNE-to-E4M3(src[r][h] / scale[r]), saturating;
+ * IEEE fp32 arithmetic, so the codes equal oracle.quantize_rows_e4m3 bit for
+ * bit. src [R, H] fp32 (src_dtype AMUN_F32) or bf16 (AMUN_BF16), H even,
+ * device; dst [R, H] uint8, scale [R] fp32, device. One launch. */
+amun_status amun_quantize_e4m3(const void* src, amun_dtype src_dtype, int R, int H, uint8_t* dst,
+                               float* scale, void* stream);
 
 /* Test hook: steps 1-2 only. Writes the biased logits of the same tcgen05
  * (bf16) or SIMT (f32) GEMM to logits [N, V_local] fp32 (these never reach

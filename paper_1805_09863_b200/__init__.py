@@ -20,7 +20,8 @@ from ._lib import AMUN_MAX_COLUMNS, AMUN_MAX_K, AmunError, check
 
 _L = _lib.load()
 
-__all__ = ["OutputLayer", "compact", "AmunError", "AMUN_MAX_K", "AMUN_MAX_COLUMNS", "lib_path"]
+__all__ = ["OutputLayer", "compact", "beam_advance", "quantize_e4m3", "AmunError", "AMUN_MAX_K",
+           "AMUN_MAX_COLUMNS", "lib_path"]
 
 lib_path = _lib.LIB_PATH
 
@@ -61,11 +62,12 @@ class OutputLayer:
         self.H, self.V_local, self.v_offset = H, V_local, v_offset
         self.V_total = V_local if V_total is None else V_total
         self.dtype = dtype
-        self.tdtype = torch.bfloat16 if dtype == "bf16" else torch.float32
+        self.tdtype = {"bf16": torch.bfloat16, "f32": torch.float32, "e4m3": torch.uint8}[dtype]
         self.k_max, self.max_rows, self.max_sentences = k_max, max_rows, max_sentences
         h = ctypes.c_void_p()
         check(_L.amun_ol_create(ctypes.byref(h), H, V_local, v_offset, self.V_total,
-                                _lib.AMUN_BF16 if dtype == "bf16" else _lib.AMUN_F32,
+                                {"bf16": _lib.AMUN_BF16, "f32": _lib.AMUN_F32,
+                                 "e4m3": _lib.AMUN_E4M3}[dtype],
                                 k_max, max_rows, max_sentences, dev.index or 0))
         self._h = h
         self.stride = _L.amun_ol_partial_stride(h)
@@ -132,6 +134,31 @@ class OutputLayer:
                                        _ptr(out_idx), _ptr(out_cost), _ptr(self.workspace),
                                        _stream(self.device)))
         return out_idx, out_cost
+
+    def _check_e4m3(self, X8, xs, W8, ws, b):
+        N = self._check_scores(X8, W8, b)
+        _need(xs, "x_scale", torch.float32, self.device, (N,))
+        _need(ws, "w_scale", torch.float32, self.device, (self.V_local,))
+        return N
+
+    def call_e4m3(self, X8, x_scale, W8, w_scale, b, prev_cost, beam_offsets, k: int,
+                  k_per_sentence=None, out_idx=None, out_cost=None):
+        """FP8 steps 1-4 (plan dtype "e4m3"): X8 / W8 uint8 E4M3 codes with
+        per-row fp32 scales (see quantize_e4m3). Returns (idx, cost)."""
+        N = self._check_e4m3(X8, x_scale, W8, w_scale, b)
+        S = self._check_select(prev_cost, beam_offsets, N, k_per_sentence)
+        out_idx, out_cost = self._outputs(S, k, out_idx, out_cost)
+        check(_L.amun_output_layer_e4m3(self._h, _ptr(X8), _ptr(x_scale), _ptr(W8), _ptr(w_scale),
+                                        _ptr(b), _ptr(prev_cost), _ptr(beam_offsets), N, S,
+                                        _ptr(k_per_sentence), k, _ptr(out_idx), _ptr(out_cost),
+                                        _ptr(self.workspace), _stream(self.device)))
+        return out_idx, out_cost
+
+    def scores_e4m3(self, X8, x_scale, W8, w_scale, b, variant: int = 0):
+        """FP8 stage 1 (variant 0), or the bare-GEMM (2) / no-k-best (3) builds."""
+        N = self._check_e4m3(X8, x_scale, W8, w_scale, b)
+        check(_L.amun_ol_scores_e4m3(self._h, _ptr(X8), _ptr(x_scale), _ptr(W8), _ptr(w_scale),
+                                     _ptr(b), N, variant, _ptr(self.workspace), _stream(self.device)))
 
     def scores(self, X, W, b):
         """Stage 1 only (fused GEMM + bias + online softmax stats + row k-best)."""
@@ -289,3 +316,22 @@ def beam_advance(out_idx, out_cost, V_total: int, eos: int, N: int, columns=(), 
     if sync:
         return int(host[0]), int(host[1]), new_offsets, src_row, new_token, new_cost, counts
     return None, None, new_offsets, src_row, new_token, new_cost, counts
+
+
+def quantize_e4m3(src, out=None, scale=None):
+    """Per-row E4M3 quantisation on the GPU (amun_quantize_e4m3): src [R, H]
+    fp32 or bf16 -> (codes [R, H] uint8, scale [R] fp32) with
+    src ~= codes * scale[:, None]."""
+    if src.dim() != 2 or not src.is_contiguous() or src.dtype not in (torch.float32, torch.bfloat16):
+        raise ValueError("src must be a contiguous 2-D fp32 or bf16 tensor")
+    R, H = src.shape
+    dev = src.device
+    if out is None:
+        out = torch.empty((R, H), dtype=torch.uint8, device=dev)
+    if scale is None:
+        scale = torch.empty(R, dtype=torch.float32, device=dev)
+    _need(out, "out", torch.uint8, dev, (R, H))
+    _need(scale, "scale", torch.float32, dev, (R,))
+    check(_L.amun_quantize_e4m3(_ptr(src), _lib.AMUN_BF16 if src.dtype == torch.bfloat16 else _lib.AMUN_F32,
+                                R, H, _ptr(out), _ptr(scale), _stream(dev)))
+    return out, scale

@@ -13,7 +13,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("AMUN_LIB", os.path.join(_HERE, "libamun.so"))
 
 AMUN_OK, AMUN_EINVAL, AMUN_EUNSUPPORTED, AMUN_ECUDA = 0, 1, 2, 3
-AMUN_F32, AMUN_BF16 = 0, 1
+AMUN_F32, AMUN_BF16, AMUN_E4M3 = 0, 1, 2
 AMUN_MAX_K = 16
 AMUN_MAX_COLUMNS = 16
 
@@ -22,7 +22,8 @@ EXPORTS = [
     "amun_ol_destroy", "amun_ol_workspace_bytes", "amun_ol_partial_stride",
     "amun_output_layer", "amun_output_layer_dev", "amun_ol_scores", "amun_ol_select", "amun_output_layer_partial",
     "amun_merge_partials", "amun_argmax", "amun_debug_logits", "amun_bench_variant", "amun_compact",
-    "amun_beam_advance_workspace_bytes", "amun_beam_advance",
+    "amun_beam_advance_workspace_bytes", "amun_beam_advance", "amun_output_layer_e4m3",
+    "amun_ol_scores_e4m3", "amun_quantize_e4m3",
 ]
 
 
@@ -69,6 +70,10 @@ def load() -> ctypes.CDLL:
         "amun_bench_variant": (st, [vp, vp, vp, vp, i32, i32, vp, vp]),
         "amun_compact": (st, [ctypes.POINTER(amun_column), i32, vp, i32, vp, i32, vp, vp, vp, vp, vp]),
         "amun_beam_advance_workspace_bytes": (sz, [i32, i32]),
+        "amun_output_layer_e4m3": (st, [vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, vp, i32, vp, vp,
+                                        vp, vp]),
+        "amun_ol_scores_e4m3": (st, [vp, vp, vp, vp, vp, vp, i32, i32, vp, vp]),
+        "amun_quantize_e4m3": (st, [vp, i32, i32, i32, vp, vp, vp]),
         "amun_beam_advance": (st, [vp, vp, i32, i32, ctypes.c_int64, i32, i32,
                                    ctypes.POINTER(amun_column), i32, vp, vp, vp, vp, vp, vp, vp,
                                    vp]),

@@ -20,6 +20,7 @@
 #include "ol_simt.cuh"
 #include "ol_tc.cuh"
 #include "ol_tc2.cuh"
+#include "quant.cuh"
 
 using namespace amun;
 
@@ -115,11 +116,13 @@ amun_status encode_map(amun_ol* pl, const void* ptr, long long rows, int box_row
                        CUtensorMap* out) {
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return fail(AMUN_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
+  const bool f8 = pl->dtype == AMUN_E4M3;   // 1-byte elements, 128 per 128-byte box row
   cuuint64_t dims[2] = {(cuuint64_t)pl->H, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)pl->H * 2};
-  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+  cuuint64_t strides[1] = {(cuuint64_t)pl->H * (f8 ? 1 : 2)};
+  cuuint32_t box[2] = {f8 ? 128u : 64u, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(out, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides,
+  CUresult r = enc(out, f8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                   const_cast<void*>(ptr), dims, strides,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(AMUN_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -174,6 +177,23 @@ Schedule make_schedule(const amun_ol* pl, int N, int* grid) {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
+// Launch one fused-kernel instantiation; the warpgroup register hand-off
+// needs the full launch pool (see TcCfg), checked here.
+template <int NG>
+amun_status launch_kernel(void (*kern)(const CUtensorMap, const CUtensorMap, const TcParams),
+                          const CUtensorMap* mx, const CUtensorMap* mw, const TcParams& tp,
+                          int grid, cudaStream_t st, int smem_bytes) {
+  cudaFuncAttributes fa;
+  CUDA_TRY(cudaFuncGetAttributes(&fa, kern));
+  if (fa.numRegs < TcCfg<NG>::kLaunchRegs)
+    return fail(AMUN_ECUDA, "fused kernel compiled with %d registers/thread, needs %d for its "
+                "setmaxnreg budget", fa.numRegs, TcCfg<NG>::kLaunchRegs);
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
+  kern<<<grid, TcCfg<NG>::kThreads, smem_bytes, st>>>(*mx, *mw, tp);
+  CUDA_TRY(cudaGetLastError());
+  return AMUN_OK;
+}
+
 template <int KB, int NG>
 amun_status launch_tc_ng(const CUtensorMap* mx, const CUtensorMap* mw, const TcParams& tp,
                          int grid, cudaStream_t st, int mode, bool pairs) {
@@ -190,25 +210,33 @@ amun_status launch_tc_ng(const CUtensorMap* mx, const CUtensorMap* mw, const TcP
          : mode == 3 ? ol_tc_kernel<KB, 3, NG>
          : mode == 4 ? ol_tc_kernel<1, 4, NG>
                      : ol_tc_kernel<1, 1, NG>;
-  const int smem_bytes = pairs ? TC2_SMEM : TC_SMEM;
-  // the warpgroup register hand-off needs the full launch pool (see TcCfg)
-  cudaFuncAttributes fa;
-  CUDA_TRY(cudaFuncGetAttributes(&fa, kern));
-  if (fa.numRegs < TcCfg<NG>::kLaunchRegs)
-    return fail(AMUN_ECUDA, "fused kernel compiled with %d registers/thread, needs %d for its "
-                "setmaxnreg budget", fa.numRegs, TcCfg<NG>::kLaunchRegs);
-  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
-  kern<<<grid, TcCfg<NG>::kThreads, smem_bytes, st>>>(*mx, *mw, tp);
-  CUDA_TRY(cudaGetLastError());
-  return AMUN_OK;
+  return launch_kernel<NG>(kern, mx, mw, tp, grid, st, pairs ? TC2_SMEM : TC_SMEM);
 }
 
-// Two epilogue warpgroups: measured faster than four at every config tried
-// (four warps per sub-partition cost issue slots and registers).
-// Building with -DAMUN_WITH_NG4 adds the 4-group kernels (env AMUN_NG=4).
+// e4m3 plans: single CTAs; the full path and the two benchmark builds.
+template <int KB, int NG>
+amun_status launch_tc_f8(const CUtensorMap* mx, const CUtensorMap* mw, const TcParams& tp,
+                         int grid, cudaStream_t st, int mode) {
+  void (*kern)(const CUtensorMap, const CUtensorMap, const TcParams) =
+      mode == 0 ? ol_tc_kernel<KB, 0, NG, 1> : mode == 2 ? ol_tc_kernel<KB, 2, NG, 1>
+                                             : ol_tc_kernel<KB, 3, NG, 1>;
+  return launch_kernel<NG>(kern, mx, mw, tp, grid, st, TC_SMEM);
+}
+
+// Two epilogue warpgroups. bf16: measured faster than three or four (their
+// extra warps cost issue slots and registers while the tensor pipe bounds;
+// DESIGN.md §6.1). e4m3: four measured within run-to-run noise of two
+// (cfg beam fused 80-85 vs 80-83 us). Building with -DAMUN_WITH_NG3 /
+// -DAMUN_WITH_NG4 adds the other counts (env AMUN_NG).
 template <int KB>
 amun_status launch_tc(amun_ol* pl, const CUtensorMap* mx, const CUtensorMap* mw,
                       const TcParams& tp, int grid, cudaStream_t st, int mode, bool pairs) {
+  if (pl->dtype == AMUN_E4M3) {
+#ifdef AMUN_WITH_NG4
+    if (pl->ng_override == 4) return launch_tc_f8<KB, 4>(mx, mw, tp, grid, st, mode);
+#endif
+    return launch_tc_f8<KB, 2>(mx, mw, tp, grid, st, mode);
+  }
 #ifdef AMUN_WITH_NG4
   if (pl->ng_override == 4) return launch_tc_ng<KB, 4>(mx, mw, tp, grid, st, mode, pairs);
 #endif
@@ -241,7 +269,8 @@ bool dev_pairs(const amun_ol* pl) {
 
 amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b, int N,
                        void* workspace, float* logits, cudaStream_t st, int mode,
-                       const int* N_dev = nullptr) {
+                       const int* N_dev = nullptr, const float* x_scale = nullptr,
+                       const float* w_scale = nullptr) {
   if (N == 0) return AMUN_OK;
   CUDA_TRY(cudaSetDevice(pl->device));
   int grid;
@@ -252,7 +281,7 @@ amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b
                        dp ? pl->num_sms / 2 : pl->num_sms);
     grid = dp ? pl->num_sms / 2 * 2 : pl->num_sms;
   }
-  if (pl->dtype == AMUN_BF16) {
+  if (pl->dtype != AMUN_F32) {   // tcgen05: bf16 (kind::f16) or e4m3 (kind::f8f6f4)
     const bool pairs = N_dev ? dev_pairs(pl) : use_pairs(pl, N);
     const CUtensorMap *mx, *mw;
     amun_status s = get_map(pl, pl->xmaps, 4, pl->xnext, X, N, TC_BM, &mx);
@@ -263,7 +292,9 @@ amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b
     tp.N = N;
     tp.V_local = pl->V_local;
     tp.v_offset = pl->v_offset;
-    tp.n_kblk = (int)cdiv(pl->H, TC_BK);
+    tp.n_kblk = (int)cdiv(pl->H, pl->dtype == AMUN_E4M3 ? 2 * TC_BK : TC_BK);
+    tp.x_scale = x_scale;
+    tp.w_scale = w_scale;
     tp.sch = sch;
     tp.bias = b;
     tp.part = static_cast<float*>(workspace);
@@ -388,10 +419,12 @@ amun_status amun_ol_create(amun_ol** plan, int H, int V_local, int v_offset, int
                            int device) {
   if (!plan) return fail(AMUN_EINVAL, "NULL plan pointer");
   *plan = nullptr;
-  if (dtype != AMUN_F32 && dtype != AMUN_BF16) return fail(AMUN_EINVAL, "unknown dtype %d", (int)dtype);
+  if (dtype != AMUN_F32 && dtype != AMUN_BF16 && dtype != AMUN_E4M3)
+    return fail(AMUN_EINVAL, "unknown dtype %d", (int)dtype);
   if (H < 1) return fail(AMUN_EINVAL, "H=%d must be >= 1", H);
   if (dtype == AMUN_BF16 && H % 8 != 0) return fail(AMUN_EINVAL, "bf16 needs H %% 8 == 0 (H=%d)", H);
   if (dtype == AMUN_F32 && H % 4 != 0) return fail(AMUN_EINVAL, "f32 needs H %% 4 == 0 (H=%d)", H);
+  if (dtype == AMUN_E4M3 && H % 16 != 0) return fail(AMUN_EINVAL, "e4m3 needs H %% 16 == 0 (H=%d)", H);
   if (V_local < 1) return fail(AMUN_EINVAL, "V_local=%d must be >= 1", V_local);
   if (v_offset < 0 || V_total < 1 || (long long)v_offset + V_local > V_total)
     return fail(AMUN_EINVAL, "need 0 <= v_offset and v_offset + V_local <= V_total");
@@ -448,6 +481,8 @@ int amun_ol_partial_stride(const amun_ol* plan) { return plan ? plan->stride : 0
 
 amun_status amun_ol_scores(amun_ol* plan, const void* X, const void* W, const float* b, int N,
                            void* workspace, void* stream) {
+  if (plan && plan->dtype == AMUN_E4M3)
+    return fail(AMUN_EINVAL, "e4m3 plans take the *_e4m3 entry points (they carry the scales)");
   amun_status s = check_score_args(plan, X, W, b, N, workspace);
   if (s != AMUN_OK) return s;
   return run_scores(plan, X, W, b, N, workspace, nullptr, static_cast<cudaStream_t>(stream), 0);
@@ -532,6 +567,8 @@ amun_status amun_output_layer_dev(amun_ol* plan, const void* X, const void* W, c
 amun_status amun_output_layer_partial(amun_ol* plan, const void* X, const void* W,
                                       const float* b, int N, float* partial, void* workspace,
                                       void* stream) {
+  if (plan && plan->dtype == AMUN_E4M3)
+    return fail(AMUN_EINVAL, "e4m3 plans take the *_e4m3 entry points (they carry the scales)");
   amun_status s = check_score_args(plan, X, W, b, N, workspace);
   if (s != AMUN_OK) return s;
   if (N == 0) return AMUN_OK;
@@ -576,6 +613,8 @@ amun_status amun_merge_partials(amun_ol* plan, const float* partials, int G,
 
 amun_status amun_debug_logits(amun_ol* plan, const void* X, const void* W, const float* b, int N,
                               float* logits, void* workspace, void* stream) {
+  if (plan && plan->dtype == AMUN_E4M3)
+    return fail(AMUN_EINVAL, "e4m3 plans take the *_e4m3 entry points (they carry the scales)");
   amun_status s = check_score_args(plan, X, W, b, N, workspace);
   if (s != AMUN_OK) return s;
   if (N > 0 && !logits) return fail(AMUN_EINVAL, "NULL logits");
@@ -584,6 +623,8 @@ amun_status amun_debug_logits(amun_ol* plan, const void* X, const void* W, const
 
 amun_status amun_argmax(amun_ol* plan, const void* X, const void* W, const float* b, int N,
                         int64_t* out_token, float* out_logit, void* workspace, void* stream) {
+  if (plan && plan->dtype == AMUN_E4M3)
+    return fail(AMUN_EINVAL, "e4m3 plans take the *_e4m3 entry points (they carry the scales)");
   amun_status s = check_score_args(plan, X, W, b, N, workspace);
   if (s != AMUN_OK) return s;
   if (N > 0 && (!out_token || !out_logit)) return fail(AMUN_EINVAL, "NULL out_token / out_logit");
@@ -600,6 +641,52 @@ amun_status amun_argmax(amun_ol* plan, const void* X, const void* W, const float
   // one warp per row (more CTAs spread the latency-bound reduction)
   argmax_rows_kernel<<<(unsigned)N, 32, 0, st>>>(mp, reinterpret_cast<long long*>(out_token),
                                                  out_logit);
+  CUDA_TRY(cudaGetLastError());
+  return AMUN_OK;
+}
+
+amun_status amun_ol_scores_e4m3(amun_ol* plan, const uint8_t* X8, const float* x_scale,
+                                const uint8_t* W8, const float* w_scale, const float* b, int N,
+                                int variant, void* workspace, void* stream) {
+  amun_status s = check_score_args(plan, X8, W8, b, N, workspace);
+  if (s != AMUN_OK) return s;
+  if (plan->dtype != AMUN_E4M3) return fail(AMUN_EINVAL, "plan dtype is not AMUN_E4M3");
+  if (variant != 0 && variant != 2 && variant != 3)
+    return fail(AMUN_EINVAL, "variant %d not in {0, 2, 3}", variant);
+  if (N > 0 && (!x_scale || !w_scale)) return fail(AMUN_EINVAL, "NULL x_scale / w_scale");
+  if (N > 0 && !aligned16(w_scale)) return fail(AMUN_EINVAL, "w_scale must be 16-byte aligned");
+  return run_scores(plan, X8, W8, b, N, workspace, nullptr, static_cast<cudaStream_t>(stream),
+                    variant, nullptr, x_scale, w_scale);
+}
+
+amun_status amun_output_layer_e4m3(amun_ol* plan, const uint8_t* X8, const float* x_scale,
+                                   const uint8_t* W8, const float* w_scale, const float* b,
+                                   const float* prev_cost, const int32_t* beam_offsets, int N,
+                                   int S, const int32_t* k_per_sentence, int k, int64_t* out_idx,
+                                   float* out_cost, void* workspace, void* stream) {
+  if (!plan) return fail(AMUN_EINVAL, "NULL plan");
+  amun_status s = check_select_args(plan, prev_cost, beam_offsets, N, S, k, out_idx, out_cost);
+  if (s != AMUN_OK) return s;
+  s = amun_ol_scores_e4m3(plan, X8, x_scale, W8, w_scale, b, N, 0, workspace, stream);
+  if (s != AMUN_OK) return s;
+  return amun_ol_select(plan, workspace, prev_cost, beam_offsets, N, S, k_per_sentence, k,
+                        out_idx, out_cost, stream);
+}
+
+amun_status amun_quantize_e4m3(const void* src, amun_dtype src_dtype, int R, int H, uint8_t* dst,
+                               float* scale, void* stream) {
+  if (R < 0 || H < 0 || (H & 1)) return fail(AMUN_EINVAL, "R=%d, H=%d: need R, H >= 0 and H even", R, H);
+  if (src_dtype != AMUN_F32 && src_dtype != AMUN_BF16)
+    return fail(AMUN_EINVAL, "src_dtype must be AMUN_F32 or AMUN_BF16");
+  if (R == 0 || H == 0) return AMUN_OK;
+  if (!src || !dst || !scale) return fail(AMUN_EINVAL, "NULL src/dst/scale");
+  if ((reinterpret_cast<uintptr_t>(dst) & 1) != 0) return fail(AMUN_EINVAL, "dst must be 2-byte aligned");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int grid = (int)std::min<long long>(R, 148LL * 16);
+  if (src_dtype == AMUN_BF16)
+    quantize_e4m3_kernel<true><<<grid, QZ_THREADS, 0, st>>>(src, R, H, dst, scale);
+  else
+    quantize_e4m3_kernel<false><<<grid, QZ_THREADS, 0, st>>>(src, R, H, dst, scale);
   CUDA_TRY(cudaGetLastError());
   return AMUN_OK;
 }

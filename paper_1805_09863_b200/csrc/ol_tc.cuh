@@ -34,7 +34,10 @@ constexpr int TC_SMEM = TC_STAGES * (TC_A_BYTES + TC_B_BYTES) + TC_BIAS_BYTES + 
                         TC_THRX_BYTES + 1024 /*align*/ + 512 /*barriers*/;
 static_assert(TC_NBIAS >= 2 + TC_STAGES, "bias ring too small for the producer's lead");
 
-template <int KB, int MODE, int NG>
+// ELT = 0: bf16 X, W (kind::f16, 64 elements per 128-byte K block);
+// ELT = 1: e4m3 X, W with per-row scales (kind::f8f6f4, 128 elements per
+// block; NEXT f4, the modern analogue of the paper's 16-bit storage P:264-268).
+template <int KB, int MODE, int NG, int ELT = 0>
 __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
     ol_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                  const TcParams p) {
@@ -111,8 +114,10 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
           mbar_wait_spin(&empty[stage], phase ^ 1);
           if (lane == 0) {
             mbar_arrive_expect_tx(&full[stage], TC_A_BYTES + TC_B_BYTES);
-            tma_load_2d(&tmX, &full[stage], sA + stage * TC_A_BYTES, kb * TC_BK, mt * TC_BM, pol_x);
-            tma_load_2d(&tmW, &full[stage], sB + stage * TC_B_BYTES, kb * TC_BK, v0, 0ull);
+            constexpr int kBlockElems = ELT ? 2 * TC_BK : TC_BK;   // 128 bytes of K either way
+            tma_load_2d(&tmX, &full[stage], sA + stage * TC_A_BYTES, kb * kBlockElems, mt * TC_BM,
+                        pol_x);
+            tma_load_2d(&tmW, &full[stage], sB + stage * TC_B_BYTES, kb * kBlockElems, v0, 0ull);
           }
           __syncwarp();
           if (++stage == TC_STAGES) {
@@ -137,7 +142,7 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
         mbar_wait_spin(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + acc * TC_BN;
-        const uint32_t idesc = idesc_bf16_f32(TC_BM, width);
+        const uint32_t idesc = ELT ? idesc_e4m3_f32(TC_BM, width) : idesc_bf16_f32(TC_BM, width);
         for (int kb = 0; kb < p.n_kblk; ++kb) {
           mbar_wait_spin(&full[stage], phase);
           tc_fence_after();
@@ -145,8 +150,12 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
             const uint64_t ad = sdesc_k_sw128(smem_u32(sA + stage * TC_A_BYTES));
             const uint64_t bd = sdesc_k_sw128(smem_u32(sB + stage * TC_B_BYTES));
 #pragma unroll
-            for (int k = 0; k < TC_BK / 16; ++k)   // +32 bytes of K per MMA (>>4 = 2)
-              mma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+            for (int k = 0; k < TC_BK / 16; ++k) {   // +32 bytes of K per MMA (>>4 = 2)
+              if constexpr (ELT == 0)
+                mma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+              else
+                mma_e4m3(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+            }
             mma_commit(&empty[stage]);              // smem slot free once these MMAs finish
           }
           __syncwarp();
@@ -163,7 +172,7 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
     }
   } else {
     reg_alloc<Cfg::kEpiRegs>();
-    tc_epilogue<KB, MODE, NG, false>(p, tmem_base, start, stop, tfull, tempty, bfull, sbias, xch,
+    tc_epilogue<KB, MODE, NG, false, ELT>(p, tmem_base, start, stop, tfull, tempty, bfull, sbias, xch,
                                      thr_x, gen, warp, lane, 0u, (long long)blockIdx.x, dyn);
   }
 

@@ -27,6 +27,8 @@ struct TcParams {
   unsigned int* __restrict__ gen_ctr;      // {generation, CTAs done}: device-side, so every
                                            // launch (graph replays too) gets a fresh tag
   const int* __restrict__ N_dev;           // amun_output_layer_dev: N on the device (else NULL)
+  const float* __restrict__ x_scale;       // e4m3 plans: [N] per-row scales of X (else NULL)
+  const float* __restrict__ w_scale;       // e4m3 plans: [V_local] per-row scales of W
   int num_sms;                             // the device schedule's CTA count
 };
 
@@ -113,7 +115,7 @@ __device__ __forceinline__ void bias_ring_load(const TcParams& p, float* sbias, 
 
 // The epilogue. PAIR: the CTA is rank `rank` of a CTA pair (its M-tile is
 // 2 mp + rank of the pair schedule; TMEM-empty arrivals go to the leader).
-template <int KB, int MODE, int NG, bool PAIR>
+template <int KB, int MODE, int NG, bool PAIR, int ELT = 0>
 __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_base, long long start,
                                             long long stop, uint64_t* tfull, uint64_t* tempty,
                                             uint64_t* bfull, const float* sbias, float* xch,
@@ -150,6 +152,7 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
     const int limit = min(width, p.V_local - v0);
     const int nch = (width + 31) >> 5;
     const float* bsl = sbias + (tile % TC_NBIAS) * TC_BN;
+    const float xs = (ELT != 0 && row < dyn.N) ? __ldg(p.x_scale + row) : 1.f;   // e4m3 row scale
     // request the newest cross-CTA hint now (L2, not L1: other SMs update it);
     // it is folded in after this tile's chunks, for the next tile of the segment
     // (per-chunk exchange halves the insertions but its loads and atomics cost
@@ -170,20 +173,43 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
         tmem_ld_wait(r);
         if (nv >= 32) {   // full chunk: bias from the ring (same address in all lanes)
           const uint32_t b4 = smem_u32(bsl + c0);
+          if constexpr (ELT == 0) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const float4 bq = lds128(b4 + 16 * j);
-            fadd2(x[4 * j + 0], x[4 * j + 1], __uint_as_float(r[4 * j + 0]), __uint_as_float(r[4 * j + 1]),
-                  bq.x, bq.y);
-            fadd2(x[4 * j + 2], x[4 * j + 3], __uint_as_float(r[4 * j + 2]), __uint_as_float(r[4 * j + 3]),
-                  bq.z, bq.w);
+            for (int j = 0; j < 8; ++j) {
+              const float4 bq = lds128(b4 + 16 * j);
+              fadd2(x[4 * j + 0], x[4 * j + 1], __uint_as_float(r[4 * j + 0]),
+                    __uint_as_float(r[4 * j + 1]), bq.x, bq.y);
+              fadd2(x[4 * j + 2], x[4 * j + 3], __uint_as_float(r[4 * j + 2]),
+                    __uint_as_float(r[4 * j + 3]), bq.z, bq.w);
+            }
+          } else {
+            // e4m3: logit = acc * (x_scale[row] * w_scale[v]) + b[v]; the 32
+            // column scales are the same for every lane (L1 broadcast)
+            const float4* ws4 = reinterpret_cast<const float4*>(p.w_scale + v0 + c0);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float4 bq = lds128(b4 + 16 * j);
+              const float4 wq = __ldg(ws4 + j);
+              float s0, s1, s2, s3;
+              fmul2(s0, s1, wq.x, wq.y, xs, xs);
+              fmul2(s2, s3, wq.z, wq.w, xs, xs);
+              ffma2(x[4 * j + 0], x[4 * j + 1], __uint_as_float(r[4 * j + 0]),
+                    __uint_as_float(r[4 * j + 1]), s0, s1, bq.x, bq.y);
+              ffma2(x[4 * j + 2], x[4 * j + 3], __uint_as_float(r[4 * j + 2]),
+                    __uint_as_float(r[4 * j + 3]), s2, s3, bq.z, bq.w);
+            }
           }
         } else {          // vocabulary tail: mask, and the unstaged <= 3-float bias tail
           const int nv4 = (limit & ~3) - c0;
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const float bj = (j < nv4) ? bsl[c0 + j] : ((j < nv) ? __ldg(p.bias + v0 + c0 + j) : 0.f);
-            x[j] = (j < nv) ? __uint_as_float(r[j]) + bj : kNegInf;
+            if constexpr (ELT == 0) {
+              x[j] = (j < nv) ? __uint_as_float(r[j]) + bj : kNegInf;
+            } else {
+              const float sj = (j < nv) ? xs * __ldg(p.w_scale + v0 + c0 + j) : 0.f;
+              x[j] = (j < nv) ? fmaf(__uint_as_float(r[j]), sj, bj) : kNegInf;
+            }
           }
         }
         if constexpr (MODE == 1) {

@@ -22,7 +22,7 @@ def lib():
 def header_functions():
     src = open(os.path.join(ROOT, "include", "amun.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(amun_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(amun_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_exports_every_declared_symbol(lib):

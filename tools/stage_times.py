@@ -88,6 +88,16 @@ def main():
         g_v4 = graph_time(lambda: ol.bench_variant(X, W, b, 4), reps=5)
         print(f"{name}: GRAPH argmax-only path (Alg. 5: fused kernel without exp + row argmax) "
               f"{g_am:.1f} us | its fused kernel alone {g_v4:.1f} us")
+        # FP8 (E4M3, NEXT f4): same shapes, X / W quantised per row on the GPU
+        X8, xs = amun.quantize_e4m3(X)
+        W8, ws = amun.quantize_e4m3(W)
+        o8 = amun.OutputLayer(w.H, w.V, dtype="e4m3", k_max=w.k, max_rows=w.N, max_sentences=w.S)
+        f8 = {v: graph_time(lambda v=v: o8.scores_e4m3(X8, xs, W8, ws, b, v), reps=5) for v in (2, 3, 0)}
+        f8_all = graph_time(lambda: o8.call_e4m3(X8, xs, W8, ws, b, pc, off, w.k, out_idx=oi,
+                                                 out_cost=oc), reps=5)
+        g_q = graph_time(lambda: amun.quantize_e4m3(X, out=X8, scale=xs), reps=5)
+        print(f"{name}: GRAPH e4m3 bare GEMM {f8[2]:.1f} us | + stats {f8[3]:.1f} us | full fused "
+              f"{f8[0]:.1f} us | path (fused + select) {f8_all:.1f} us | X quantise {g_q:.1f} us")
 
 
 if __name__ == "__main__":
