@@ -220,7 +220,7 @@ amun_status launch_tc_f8(const CUtensorMap* mx, const CUtensorMap* mw, const TcP
   void (*kern)(const CUtensorMap, const CUtensorMap, const TcParams) =
       mode == 0 ? ol_tc_kernel<KB, 0, NG, 1> : mode == 2 ? ol_tc_kernel<KB, 2, NG, 1>
                                              : ol_tc_kernel<KB, 3, NG, 1>;
-  return launch_kernel<NG>(kern, mx, mw, tp, grid, st, TC_SMEM);
+  return launch_kernel<NG>(kern, mx, mw, tp, grid, st, TC_SMEM_F8);
 }
 
 // Two epilogue warpgroups. bf16: measured faster than three or four (their

@@ -32,6 +32,8 @@ constexpr int TC_A_BYTES = TC_BM * TC_BK * 2;   // 16 KB
 constexpr int TC_B_BYTES = TC_BN * TC_BK * 2;   // 32 KB
 constexpr int TC_SMEM = TC_STAGES * (TC_A_BYTES + TC_B_BYTES) + TC_BIAS_BYTES + TC_XCH_BYTES +
                         TC_THRX_BYTES + 1024 /*align*/ + 512 /*barriers*/;
+constexpr int TC_SMEM_F8 = TC_SMEM + TC_SCALE_BYTES;   // + the e4m3 column-scale ring
+static_assert(TC_SMEM_F8 <= 227 * 1024, "shared memory budget");
 static_assert(TC_NBIAS >= 2 + TC_STAGES, "bias ring too small for the producer's lead");
 
 // ELT = 0: bf16 X, W (kind::f16, 64 elements per 128-byte K block);
@@ -57,6 +59,10 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
   uint64_t* bfull = tempty + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bfull + TC_NBIAS);
   uint32_t* gen_smem = tmem_holder + 1;
+  // e4m3 column-scale ring, after the 512-byte barrier area (TC_SMEM_F8)
+  float* sscale = (ELT != 0 && scale_ring_ok(p, TC_STAGES))
+                      ? reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 512)
+                      : nullptr;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -109,7 +115,7 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
       int stage = 0, tile = 0;
       uint32_t phase = 0;
       while (it.next(mt, v0, width, last)) {
-        if (lane == 0) bias_ring_load(p, sbias, bfull, tile, v0, width);
+        if (lane == 0) bias_ring_load(p, sbias, bfull, tile, v0, width, sscale);
         for (int kb = 0; kb < p.n_kblk; ++kb) {
           mbar_wait_spin(&empty[stage], phase ^ 1);
           if (lane == 0) {
@@ -173,7 +179,8 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
   } else {
     reg_alloc<Cfg::kEpiRegs>();
     tc_epilogue<KB, MODE, NG, false, ELT>(p, tmem_base, start, stop, tfull, tempty, bfull, sbias, xch,
-                                     thr_x, gen, warp, lane, 0u, (long long)blockIdx.x, dyn);
+                                     thr_x, gen, warp, lane, 0u, (long long)blockIdx.x, dyn,
+                                     sscale);
   }
 
   tc_fence_before();

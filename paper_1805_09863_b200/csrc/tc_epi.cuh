@@ -63,6 +63,13 @@ constexpr int TC_BIAS_BYTES = TC_NBIAS * TC_BN * 4;
 constexpr int TC_XCH_FLOATS = 2 + 2 * 16;            // one row's state in the exchange area
 constexpr int TC_XCH_BYTES = 128 * TC_XCH_FLOATS * 4;
 constexpr int TC_THRX_BYTES = 4 * 128 * 8;           // per-(group, row) k-th-best words (NG <= 4)
+// e4m3 column-scale ring. 4 slots suffice when a tile has more K blocks than
+// pipeline stages: the producer can only start tile t after the MMA started
+// tile t-1, which needed the epilogue of tile t-3 to have released its
+// accumulator, so tile t-4's slot is no longer read. Otherwise (small H) the
+// epilogue reads the scales from global memory.
+constexpr int TC_NSCALE = 4;
+constexpr int TC_SCALE_BYTES = TC_NSCALE * TC_BN * 4;
 
 // Launch configuration of NG epilogue warpgroups (warps 0 .. 4NG-1) + the
 // control warpgroup (TMA producer warp, MMA warp, 2 idle warps), and the setmaxnreg budget,
@@ -105,23 +112,33 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 // ahead of the slowest epilogue warp (the MMA cannot start tile t+2 before
 // every epilogue warp released tile t), so TC_NBIAS >= 2 + STAGES suffices.
 __device__ __forceinline__ void bias_ring_load(const TcParams& p, float* sbias, uint64_t* bfull,
-                                               int tile, int v0, int width) {
+                                               int tile, int v0, int width,
+                                               float* sscale = nullptr) {
   const int slot = tile % TC_NBIAS;
   const int limit = min(width, p.V_local - v0);
   const uint32_t bytes = (uint32_t)(limit & ~3) * 4u;
-  mbar_arrive_expect_tx(&bfull[slot], bytes);
-  if (bytes) bulk_load(sbias + slot * TC_BN, p.bias + v0, bytes, &bfull[slot]);
+  mbar_arrive_expect_tx(&bfull[slot], sscale ? 2 * bytes : bytes);
+  if (bytes) {
+    bulk_load(sbias + slot * TC_BN, p.bias + v0, bytes, &bfull[slot]);
+    // e4m3: the column scales ride along, into the 4-slot scale ring
+    // (safe when n_kblk > STAGES, see scale_ring_ok), completing on bfull too
+    if (sscale) bulk_load(sscale + (tile % TC_NSCALE) * TC_BN, p.w_scale + v0, bytes, &bfull[slot]);
+  }
 }
 
 // The epilogue. PAIR: the CTA is rank `rank` of a CTA pair (its M-tile is
 // 2 mp + rank of the pair schedule; TMEM-empty arrivals go to the leader).
+__device__ __forceinline__ bool scale_ring_ok(const TcParams& p, int stages) {
+  return p.n_kblk > stages;
+}
+
 template <int KB, int MODE, int NG, bool PAIR, int ELT = 0>
 __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_base, long long start,
                                             long long stop, uint64_t* tfull, uint64_t* tempty,
                                             uint64_t* bfull, const float* sbias, float* xch,
                                             unsigned long long* thr_x, uint32_t gen, int warp,
                                             int lane, uint32_t rank, long long slot_base,
-                                            const TcDyn dyn) {
+                                            const TcDyn dyn, const float* sscale = nullptr) {
   const int grp = warp >> 2;                       // epilogue warps are 0 .. 4NG-1
   const int q = warp & 3;                          // TMEM lane quadrant of this warp
   const int row_local = q * 32 + lane;
@@ -184,12 +201,14 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
             }
           } else {
             // e4m3: logit = acc * (x_scale[row] * w_scale[v]) + b[v]; the 32
-            // column scales are the same for every lane (L1 broadcast)
+            // column scales (the same for every lane) from the scale ring,
+            // else an L1-broadcast global load (small H, see scale_ring_ok)
             const float4* ws4 = reinterpret_cast<const float4*>(p.w_scale + v0 + c0);
+            const uint32_t s4 = sscale ? smem_u32(sscale + (tile % TC_NSCALE) * TC_BN + c0) : 0u;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
               const float4 bq = lds128(b4 + 16 * j);
-              const float4 wq = __ldg(ws4 + j);
+              const float4 wq = sscale ? lds128(s4 + 16 * j) : __ldg(ws4 + j);
               float s0, s1, s2, s3;
               fmul2(s0, s1, wq.x, wq.y, xs, xs);
               fmul2(s2, s3, wq.z, wq.w, xs, xs);

@@ -1,5 +1,5 @@
 """Run the fused output layer a few times eagerly (for ncu captures).
-  python tools/one_call.py [config] [calls]   (env AMUN_SENTENCES, AMUN_PAIRS)"""
+  python tools/one_call.py [config] [calls] [bf16|e4m3]   (env AMUN_SENTENCES, AMUN_PAIRS)"""
 import dataclasses
 import os
 import sys
@@ -18,8 +18,16 @@ if os.environ.get("AMUN_SENTENCES"):
 dev = torch.device("cuda", 0)
 X, W, b = synth.gen_X(w).to(dev), synth.gen_W(w, device=dev), synth.gen_b(w).to(dev)
 pc, off = synth.gen_prev_cost(w).to(dev), synth.gen_offsets(w).to(dev)
-ol = amun.OutputLayer(w.H, w.V, k_max=w.k, max_rows=w.N, max_sentences=w.S)
-for _ in range(calls):
-    ol(X, W, b, pc, off, w.k)
+prec = sys.argv[3] if len(sys.argv) > 3 else "bf16"
+if prec == "e4m3":
+    X8, xs = amun.quantize_e4m3(X)
+    W8, ws = amun.quantize_e4m3(W)
+    ol = amun.OutputLayer(w.H, w.V, dtype="e4m3", k_max=w.k, max_rows=w.N, max_sentences=w.S)
+    for _ in range(calls):
+        ol.call_e4m3(X8, xs, W8, ws, b, pc, off, w.k)
+else:
+    ol = amun.OutputLayer(w.H, w.V, k_max=w.k, max_rows=w.N, max_sentences=w.S)
+    for _ in range(calls):
+        ol(X, W, b, pc, off, w.k)
 torch.cuda.synchronize()
 print("ok", name, w.N)
