@@ -111,40 +111,62 @@ struct RowState {
   // statistics and gate; a candidate group's four values (x[g], x[g+8],
   // x[g+16], x[g+24]) are selected from registers by a 3-level select tree
   // and offered with the full tie key (ids arrive out of order).
-  template <bool TOPK = true, bool STATS = true>
-  __device__ __forceinline__ void chunk32r(const float (&x)[32], int vbase, float hint) {
+  // group maxima g[j] = max(x[j], x[j+8], x[j+16], x[j+24]) and the chunk max
+  __device__ __forceinline__ static float groups32(const float (&x)[32], float (&g)[8]) {
     float t[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) t[j] = fmaxf(x[j], x[j + 16]);
-    float g[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) g[j] = fmaxf(t[j], t[j + 8]);
-    const float cm = fmaxf(fmaxf(fmaxf(g[0], g[4]), fmaxf(g[1], g[5])),
-                           fmaxf(fmaxf(g[2], g[6]), fmaxf(g[3], g[7])));
-    if (STATS && cm != kNegInf) {   // (STATS = false: Alg. 5 argmax only, no exp)
-      if (cm > m) {
-        s *= ex2((m - cm) * kLog2e);
-        m = cm;
-      }
-      const float ms = m * kLog2e;
-      // exp2 arguments and the 8 running sums on packed fp32 pairs (same
-      // association as the scalar form: a[u] = e[u] + e[u+8] + e[u+16] + e[u+24])
-      float e[32];
+    return fmaxf(fmaxf(fmaxf(g[0], g[4]), fmaxf(g[1], g[5])),
+                 fmaxf(fmaxf(g[2], g[6]), fmaxf(g[3], g[7])));
+  }
+  // Alg. 4's online update for a block whose maximum is cm: one rescale by
+  // e^{m_old - m_new}, then sum exp(x - m) over the block.
+  __device__ __forceinline__ void rescale(float cm) {
+    if (cm > m) {
+      s *= ex2((m - cm) * kLog2e);
+      m = cm;
+    }
+  }
+  // exp2 arguments and 8 running sums on packed fp32 pairs:
+  // a[u] += e[u] + e[u+8] + e[u+16] + e[u+24] (in that order)
+  __device__ __forceinline__ void expsum32(const float (&x)[32], float ms, float (&a)[8], bool first) {
+    float e[32];
 #pragma unroll
-      for (int u = 0; u < 32; u += 2)
-        ffma2(e[u], e[u + 1], x[u], x[u + 1], kLog2e, kLog2e, -ms, -ms);
+    for (int u = 0; u < 32; u += 2)
+      ffma2(e[u], e[u + 1], x[u], x[u + 1], kLog2e, kLog2e, -ms, -ms);
 #pragma unroll
-      for (int u = 0; u < 32; ++u) e[u] = ex2(e[u]);
-      float a[8];
+    for (int u = 0; u < 32; ++u) e[u] = ex2(e[u]);
+    if (first) {
 #pragma unroll
       for (int u = 0; u < 8; ++u) a[u] = e[u];
+    } else {
 #pragma unroll
-      for (int j = 8; j < 32; j += 8)
+      for (int u = 0; u < 8; u += 2) fadd2(a[u], a[u + 1], a[u], a[u + 1], e[u], e[u + 1]);
+    }
 #pragma unroll
-        for (int u = 0; u < 8; u += 2) fadd2(a[u], a[u + 1], a[u], a[u + 1], e[j + u], e[j + u + 1]);
+    for (int j = 8; j < 32; j += 8)
+#pragma unroll
+      for (int u = 0; u < 8; u += 2) fadd2(a[u], a[u + 1], a[u], a[u + 1], e[j + u], e[j + u + 1]);
+  }
+
+  template <bool TOPK = true, bool STATS = true>
+  __device__ __forceinline__ void chunk32r(const float (&x)[32], int vbase, float hint) {
+    float g[8];
+    const float cm = groups32(x, g);
+    if (STATS && cm != kNegInf) {   // (STATS = false: Alg. 5 argmax only, no exp)
+      rescale(cm);
+      float a[8];
+      expsum32(x, m * kLog2e, a, true);
       s += ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
     }
-    if constexpr (!TOPK) return;
+    if constexpr (TOPK) kbest32(x, g, cm, vbase, hint);
+  }
+
+  // The k-best step for one 32-column chunk with group maxima g and max cm.
+  __device__ __forceinline__ void kbest32(const float (&x)[32], const float (&g)[8], float cm,
+                                          int vbase, float hint) {
     if constexpr (KB == 1) {
       // Alg. 4 / Alg. 5 "if p' > max: best <- i", per chunk: only the chunk
       // maximum can replace the best; its token is the lowest index holding

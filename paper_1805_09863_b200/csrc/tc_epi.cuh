@@ -180,6 +180,54 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
     mbar_wait(&tfull[acc], acc_phase);
     tc_fence_after();
     const uint32_t tbase = tmem_base + t_lane + acc * TC_BN;
+    // biased (and, e4m3, scaled) logits of 32-column chunk c from its TMEM words
+    auto build_x = [&](const uint32_t (&r)[32], int c, float (&x)[32]) {
+      const int c0 = c * 32;
+      const int nv = limit - c0;
+      if (nv >= 32) {   // full chunk: bias from the ring (same address in all lanes)
+        const uint32_t b4 = smem_u32(bsl + c0);
+        if constexpr (ELT == 0) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float4 bq = lds128(b4 + 16 * j);
+            fadd2(x[4 * j + 0], x[4 * j + 1], __uint_as_float(r[4 * j + 0]),
+                  __uint_as_float(r[4 * j + 1]), bq.x, bq.y);
+            fadd2(x[4 * j + 2], x[4 * j + 3], __uint_as_float(r[4 * j + 2]),
+                  __uint_as_float(r[4 * j + 3]), bq.z, bq.w);
+          }
+        } else {
+          // e4m3: logit = acc * (x_scale[row] * w_scale[v]) + b[v]; the 32
+          // column scales (the same for every lane) from the scale ring,
+          // else an L1-broadcast global load (small H, see scale_ring_ok)
+          const float4* ws4 = reinterpret_cast<const float4*>(p.w_scale + v0 + c0);
+          const uint32_t s4 = sscale ? smem_u32(sscale + (tile % TC_NSCALE) * TC_BN + c0) : 0u;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float4 bq = lds128(b4 + 16 * j);
+            const float4 wq = sscale ? lds128(s4 + 16 * j) : __ldg(ws4 + j);
+            float s0, s1, s2, s3;
+            fmul2(s0, s1, wq.x, wq.y, xs, xs);
+            fmul2(s2, s3, wq.z, wq.w, xs, xs);
+            ffma2(x[4 * j + 0], x[4 * j + 1], __uint_as_float(r[4 * j + 0]),
+                  __uint_as_float(r[4 * j + 1]), s0, s1, bq.x, bq.y);
+            ffma2(x[4 * j + 2], x[4 * j + 3], __uint_as_float(r[4 * j + 2]),
+                  __uint_as_float(r[4 * j + 3]), s2, s3, bq.z, bq.w);
+          }
+        }
+      } else {          // vocabulary tail: mask, and the unstaged <= 3-float bias tail
+        const int nv4 = (limit & ~3) - c0;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float bj = (j < nv4) ? bsl[c0 + j] : ((j < nv) ? __ldg(p.bias + v0 + c0 + j) : 0.f);
+          if constexpr (ELT == 0) {
+            x[j] = (j < nv) ? __uint_as_float(r[j]) + bj : kNegInf;
+          } else {
+            const float sj = (j < nv) ? xs * __ldg(p.w_scale + v0 + c0 + j) : 0.f;
+            x[j] = (j < nv) ? fmaf(__uint_as_float(r[j]), sj, bj) : kNegInf;
+          }
+        }
+      }
+    };
     if (live) {
       for (int c = grp; c < nch; c += NG) {
         uint32_t r[32];
@@ -188,49 +236,7 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
         const int nv = limit - c0;
         float x[32];
         tmem_ld_wait(r);
-        if (nv >= 32) {   // full chunk: bias from the ring (same address in all lanes)
-          const uint32_t b4 = smem_u32(bsl + c0);
-          if constexpr (ELT == 0) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const float4 bq = lds128(b4 + 16 * j);
-              fadd2(x[4 * j + 0], x[4 * j + 1], __uint_as_float(r[4 * j + 0]),
-                    __uint_as_float(r[4 * j + 1]), bq.x, bq.y);
-              fadd2(x[4 * j + 2], x[4 * j + 3], __uint_as_float(r[4 * j + 2]),
-                    __uint_as_float(r[4 * j + 3]), bq.z, bq.w);
-            }
-          } else {
-            // e4m3: logit = acc * (x_scale[row] * w_scale[v]) + b[v]; the 32
-            // column scales (the same for every lane) from the scale ring,
-            // else an L1-broadcast global load (small H, see scale_ring_ok)
-            const float4* ws4 = reinterpret_cast<const float4*>(p.w_scale + v0 + c0);
-            const uint32_t s4 = sscale ? smem_u32(sscale + (tile % TC_NSCALE) * TC_BN + c0) : 0u;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const float4 bq = lds128(b4 + 16 * j);
-              const float4 wq = sscale ? lds128(s4 + 16 * j) : __ldg(ws4 + j);
-              float s0, s1, s2, s3;
-              fmul2(s0, s1, wq.x, wq.y, xs, xs);
-              fmul2(s2, s3, wq.z, wq.w, xs, xs);
-              ffma2(x[4 * j + 0], x[4 * j + 1], __uint_as_float(r[4 * j + 0]),
-                    __uint_as_float(r[4 * j + 1]), s0, s1, bq.x, bq.y);
-              ffma2(x[4 * j + 2], x[4 * j + 3], __uint_as_float(r[4 * j + 2]),
-                    __uint_as_float(r[4 * j + 3]), s2, s3, bq.z, bq.w);
-            }
-          }
-        } else {          // vocabulary tail: mask, and the unstaged <= 3-float bias tail
-          const int nv4 = (limit & ~3) - c0;
-#pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float bj = (j < nv4) ? bsl[c0 + j] : ((j < nv) ? __ldg(p.bias + v0 + c0 + j) : 0.f);
-            if constexpr (ELT == 0) {
-              x[j] = (j < nv) ? __uint_as_float(r[j]) + bj : kNegInf;
-            } else {
-              const float sj = (j < nv) ? xs * __ldg(p.w_scale + v0 + c0 + j) : 0.f;
-              x[j] = (j < nv) ? fmaf(__uint_as_float(r[j]), sj, bj) : kNegInf;
-            }
-          }
-        }
+        build_x(r, c, x);
         if constexpr (MODE == 1) {
           if (row < dyn.N) {
             float* out = p.logits + (long long)row * p.V_local + v0 + c0;
