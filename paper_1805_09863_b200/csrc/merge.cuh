@@ -131,15 +131,14 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long x)
   return x;
 }
 
-// Row r, one full warp: lse_r = M + log Z over the row's partial records and
-// the row's top-k_max (l, v). Lane i < k_max receives entry i (v = -1 if none).
+// One full warp over n partial records at base + j * js, j = lane, lane +
+// step, ... (step = 32: all of a row's records; a multiple of 32: one warp's
+// share when a row's records are split over several warps): M + log Z and the
+// top-k_max (l, v) of their union. Lane i < k_max receives entry i (v = -1 if none).
 template <int KB>
-__device__ __forceinline__ void row_topk(const MergeParams& p, int r, int lane, float& lse,
-                                         float& M_out, float& Z_out, float& ol, int& ov) {
-  const float* base;
-  long long js;
-  int n;
-  row_splits(p, r, base, js, n);
+__device__ __forceinline__ void records_topk(const MergeParams& p, const float* base, long long js,
+                                             int n, int step, int lane, float& lse, float& M_out,
+                                             float& Z_out, float& ol, int& ov) {
   RowState<KB> lst;      // lane-local sorted list (l desc, v asc)
   lst.reset();
   float m0 = kNegInf, s0 = 0.f;
@@ -161,7 +160,7 @@ __device__ __forceinline__ void row_topk(const MergeParams& p, int r, int lane, 
   // insertions (no data-dependent early exit between loads)
   float M = m0;
 #pragma unroll 2
-  for (int j = lane + 32; j < n; j += 32) {
+  for (int j = lane + step; j < n; j += step) {
     const float* rec = base + j * js;
     M = fmaxf(M, rec[0]);
     float rl[KB];
@@ -181,7 +180,7 @@ __device__ __forceinline__ void row_topk(const MergeParams& p, int r, int lane, 
   for (int o = 16; o >= 1; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
   float Z = (m0 != kNegInf) ? s0 * expf(m0 - M) : 0.f;
 #pragma unroll 4
-  for (int j = lane + 32; j < n; j += 32) {
+  for (int j = lane + step; j < n; j += step) {
     const float* rec = base + j * js;
     const float mj = rec[0];
     const float sj = rec[1];
@@ -212,6 +211,18 @@ __device__ __forceinline__ void row_topk(const MergeParams& p, int r, int lane, 
       ol = o2f((uint32_t)(best >> 32));
     }
   }
+}
+
+// Row r, one full warp: lse_r = M + log Z over the row's partial records and
+// the row's top-k_max (l, v).
+template <int KB>
+__device__ __forceinline__ void row_topk(const MergeParams& p, int r, int lane, float& lse,
+                                         float& M_out, float& Z_out, float& ol, int& ov) {
+  const float* base;
+  long long js;
+  int n;
+  row_splits(p, r, base, js, n);
+  records_topk<KB>(p, base, js, n, 32, lane, lse, M_out, Z_out, ol, ov);
 }
 
 constexpr int MS_WARPS = 8;
