@@ -161,8 +161,9 @@ amun_status amun_output_layer_partial(amun_ol* plan, const void* X, const void* 
 /* Vocab-sharded path, piece 2 (Alg. 6 reduce step): exact merge of
  * G shards' partial records, combined in shard order g = 0..G-1, then the
  * per-sentence selection of amun_output_layer.
- *   partials [G, N, amun_ol_partial_stride(plan)] fp32 (e.g. the result of an
- *            all-gather of every rank's amun_output_layer_partial output).
+ *   partials [G, N, amun_ol_partial_stride(plan)] fp32, 8-byte aligned (e.g.
+ *            the result of an all-gather of every rank's
+ *            amun_output_layer_partial output).
  * Other arguments as amun_output_layer. Token ids are already global. */
 amun_status amun_merge_partials(amun_ol* plan, const float* partials, int G,
                                 const float* prev_cost, const int32_t* beam_offsets, int N, int S,

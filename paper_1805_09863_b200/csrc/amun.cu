@@ -284,7 +284,12 @@ amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b
   if (pl->dtype != AMUN_F32) {   // tcgen05: bf16 (kind::f16) or e4m3 (kind::f8f6f4)
     const bool pairs = N_dev ? dev_pairs(pl) : use_pairs(pl, N);
     const CUtensorMap *mx, *mw;
-    amun_status s = get_map(pl, pl->xmaps, 4, pl->xnext, X, N, TC_BM, &mx);
+    // N < 128: the X box covers only the rows that exist (rounded up to 8).
+    // A 128-row box that is mostly out of bounds made TMA measurably slower
+    // (cfg beam at S = 1: 59 vs 53 us per call); the MMA still reads the full
+    // 128-row A tile, whose extra rows only feed accumulator rows >= N.
+    const int a_rows = (!pairs && !N_dev && N < TC_BM) ? (int)cdiv(N, 8) * 8 : TC_BM;
+    amun_status s = get_map(pl, pl->xmaps, 4, pl->xnext, X, N, a_rows, &mx);
     if (s != AMUN_OK) return s;
     s = get_map(pl, pl->wmaps, 8, pl->wnext, W, pl->V_local, pairs ? TC_BN / 2 : TC_BN, &mw);
     if (s != AMUN_OK) return s;
@@ -295,6 +300,7 @@ amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b
     tp.n_kblk = (int)cdiv(pl->H, pl->dtype == AMUN_E4M3 ? 2 * TC_BK : TC_BK);
     tp.x_scale = x_scale;
     tp.w_scale = w_scale;
+    tp.a_box_bytes = a_rows * 128;   // 128 bytes of K per row (bf16 and e4m3 alike)
     tp.sch = sch;
     tp.bias = b;
     tp.part = static_cast<float*>(workspace);
@@ -594,6 +600,8 @@ amun_status amun_merge_partials(amun_ol* plan, const float* partials, int G,
   amun_status s = check_select_args(plan, prev_cost, beam_offsets, N, S, k, out_idx, out_cost);
   if (s != AMUN_OK) return s;
   if (N > 0 && !partials) return fail(AMUN_EINVAL, "NULL partials");
+  if ((reinterpret_cast<uintptr_t>(partials) & 7) != 0)
+    return fail(AMUN_EINVAL, "partials must be 8-byte aligned");
   if (S == 0) return AMUN_OK;
   CUDA_TRY(cudaSetDevice(plan->device));
   MergeParams mp = base_merge(plan);

@@ -131,6 +131,72 @@ __device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long x)
   return x;
 }
 
+// One partial record {m, s, l[k_max], v[k_max]} into registers. With
+// k_max == KB the layout is static and the record (2 + 2 KB floats, 8-byte
+// aligned) is read as float2 pairs: half the load instructions, which matters
+// when one SM reads a row's ~148 scattered records (small batches).
+template <int KB>
+__device__ __forceinline__ void load_record(const MergeParams& p, const float* rec, bool ok,
+                                            float& m, float& s, float (&l)[KB], int (&v)[KB]) {
+  m = kNegInf;
+  s = 0.f;
+#pragma unroll
+  for (int i = 0; i < KB; ++i) {
+    l[i] = kNegInf;
+    v[i] = -1;
+  }
+  if (!ok) return;
+  if (p.k_max == KB) {
+    float f[2 + 2 * KB];
+    if constexpr ((2 + 2 * KB) % 4 == 0) {   // odd KB: whole 16-byte units when aligned
+      if ((reinterpret_cast<uintptr_t>(rec) & 15) == 0) {
+        const float4* r4 = reinterpret_cast<const float4*>(rec);
+#pragma unroll
+        for (int t = 0; t < (2 + 2 * KB) / 4; ++t) {
+          const float4 q = r4[t];
+          f[4 * t] = q.x;
+          f[4 * t + 1] = q.y;
+          f[4 * t + 2] = q.z;
+          f[4 * t + 3] = q.w;
+        }
+      } else {
+        const float2* r2 = reinterpret_cast<const float2*>(rec);
+#pragma unroll
+        for (int t = 0; t < 1 + KB; ++t) {
+          const float2 q = r2[t];
+          f[2 * t] = q.x;
+          f[2 * t + 1] = q.y;
+        }
+      }
+    } else {
+      const float2* r2 = reinterpret_cast<const float2*>(rec);
+#pragma unroll
+      for (int t = 0; t < 1 + KB; ++t) {
+        const float2 q = r2[t];
+        f[2 * t] = q.x;
+        f[2 * t + 1] = q.y;
+      }
+    }
+    m = f[0];
+    s = f[1];
+#pragma unroll
+    for (int i = 0; i < KB; ++i) {
+      l[i] = f[2 + i];
+      v[i] = __float_as_int(f[2 + KB + i]);
+    }
+  } else {
+    m = rec[0];
+    s = rec[1];
+#pragma unroll
+    for (int i = 0; i < KB; ++i) {
+      if (i < p.k_max) {
+        l[i] = rec[2 + i];
+        v[i] = __float_as_int(rec[2 + p.k_max + i]);
+      }
+    }
+  }
+}
+
 // One full warp over n partial records at base + j * js, j = lane, lane +
 // step, ... (step = 32: all of a row's records; a multiple of 32: one warp's
 // share when a row's records are split over several warps): M + log Z and the
@@ -141,50 +207,80 @@ __device__ __forceinline__ void records_topk(const MergeParams& p, const float* 
                                              float& Z_out, float& ol, int& ov) {
   RowState<KB> lst;      // lane-local sorted list (l desc, v asc)
   lst.reset();
-  float m0 = kNegInf, s0 = 0.f;
-  if (lane < n) {        // record `lane` is already sorted: it is the lane's list
-    const float* rec = base + lane * js;
-    m0 = rec[0];
-    s0 = rec[1];
+  float m0, s0;           // record `lane` is already sorted: it is the lane's list
+  load_record<KB>(p, base + (lane < n ? lane : 0) * js, lane < n, m0, s0, lst.l, lst.v);
+  // Lower bound on the row's k-th best: some lane holds k_max entries >= its
+  // own k-th (one record's sorted top-k), so entries of further records below
+  // the warp maximum of those can be skipped (ties are kept: the full key
+  // decides them). Most of a row's ~148 records (one M-tile over all CTAs)
+  // then contribute no insertion at all.
+  auto kth_bound = [&]() {
+    float T = (p.k_max == KB) ? lst.l[KB - 1] : kNegInf;
 #pragma unroll
-    for (int i = 0; i < KB; ++i) {
-      if (i < p.k_max) {
-        lst.l[i] = rec[2 + i];
-        lst.v[i] = __float_as_int(rec[2 + p.k_max + i]);
+    for (int o = 16; o >= 1; o >>= 1) T = fmaxf(T, __shfl_xor_sync(0xffffffffu, T, o));
+    return T;
+  };
+  float M = m0, Z;
+  constexpr int RMAX = (KB <= 6) ? 4 : 1;   // further records per lane held in registers
+  if (KB <= 6 && n <= (RMAX + 1) * step) {
+    // every further record of this lane loaded in ONE round of independent
+    // loads (the merge is latency-bound: each dependent round costs ~1 us)
+    float xm[RMAX], xs[RMAX], xl[RMAX][KB];
+    int xv[RMAX][KB];
+#pragma unroll
+    for (int t = 0; t < RMAX; ++t) {
+      const int j = lane + (t + 1) * step;
+      load_record<KB>(p, base + (j < n ? j : 0) * js, j < n, xm[t], xs[t], xl[t], xv[t]);
+    }
+    const float T = (n > step) ? kth_bound() : kNegInf;
+#pragma unroll
+    for (int t = 0; t < RMAX; ++t) {
+      M = fmaxf(M, xm[t]);
+#pragma unroll
+      for (int i = 0; i < KB; ++i) {   // a record is sorted: stop at its first loser
+        if (xv[t][i] < 0 || xl[t][i] < T ||
+            !better_lv(xl[t][i], xv[t][i], lst.l[KB - 1], lst.v[KB - 1]))
+          break;
+        lst.insert(xl[t][i], xv[t][i]);
       }
     }
-  }
-  // records beyond the first 32 (many vocab splits per row, e.g. one M-tile
-  // over 148 CTAs): all of a record's fields are loaded before its entries
-  // are offered, so the loads of successive records do not wait on the
-  // insertions (no data-dependent early exit between loads)
-  float M = m0;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    Z = (m0 != kNegInf) ? s0 * expf(m0 - M) : 0.f;
+#pragma unroll
+    for (int t = 0; t < RMAX; ++t)
+      if (xm[t] != kNegInf) Z += xs[t] * expf(xm[t] - M);
+  } else {
+    // more records per lane: loop, all of a record's fields loaded before its
+    // entries are offered (no data-dependent exit between the loads)
+    const float T = (n > step) ? kth_bound() : kNegInf;
 #pragma unroll 2
-  for (int j = lane + step; j < n; j += step) {
-    const float* rec = base + j * js;
-    M = fmaxf(M, rec[0]);
-    float rl[KB];
-    int rv[KB];
+    for (int j = lane + step; j < n; j += step) {
+      const float* rec = base + j * js;
+      M = fmaxf(M, rec[0]);
+      float rl[KB];
+      int rv[KB];
 #pragma unroll
-    for (int i = 0; i < KB; ++i) {
-      rl[i] = i < p.k_max ? rec[2 + i] : kNegInf;
-      rv[i] = i < p.k_max ? __float_as_int(rec[2 + p.k_max + i]) : -1;
+      for (int i = 0; i < KB; ++i) {
+        rl[i] = i < p.k_max ? rec[2 + i] : kNegInf;
+        rv[i] = i < p.k_max ? __float_as_int(rec[2 + p.k_max + i]) : -1;
+      }
+#pragma unroll
+      for (int i = 0; i < KB; ++i) {
+        if (rv[i] < 0 || rl[i] < T || !better_lv(rl[i], rv[i], lst.l[KB - 1], lst.v[KB - 1])) break;
+        lst.insert(rl[i], rv[i]);
+      }
     }
 #pragma unroll
-    for (int i = 0; i < KB; ++i) {   // a record is sorted: stop at its first loser
-      if (rv[i] < 0 || !better_lv(rl[i], rv[i], lst.l[KB - 1], lst.v[KB - 1])) break;
-      lst.insert(rl[i], rv[i]);
-    }
-  }
-#pragma unroll
-  for (int o = 16; o >= 1; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-  float Z = (m0 != kNegInf) ? s0 * expf(m0 - M) : 0.f;
+    for (int o = 16; o >= 1; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    Z = (m0 != kNegInf) ? s0 * expf(m0 - M) : 0.f;
 #pragma unroll 4
-  for (int j = lane + step; j < n; j += step) {
-    const float* rec = base + j * js;
-    const float mj = rec[0];
-    const float sj = rec[1];
-    if (mj != kNegInf) Z += sj * expf(mj - M);
+    for (int j = lane + step; j < n; j += step) {
+      const float* rec = base + j * js;
+      const float mj = rec[0];
+      const float sj = rec[1];
+      if (mj != kNegInf) Z += sj * expf(mj - M);
+    }
   }
 #pragma unroll
   for (int o = 16; o >= 1; o >>= 1) Z += __shfl_xor_sync(0xffffffffu, Z, o);

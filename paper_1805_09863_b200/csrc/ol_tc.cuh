@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
         for (int kb = 0; kb < p.n_kblk; ++kb) {
           mbar_wait_spin(&empty[stage], phase ^ 1);
           if (lane == 0) {
-            mbar_arrive_expect_tx(&full[stage], TC_A_BYTES + TC_B_BYTES);
+            mbar_arrive_expect_tx(&full[stage], p.a_box_bytes + TC_B_BYTES);
             constexpr int kBlockElems = ELT ? 2 * TC_BK : TC_BK;   // 128 bytes of K either way
             tma_load_2d(&tmX, &full[stage], sA + stage * TC_A_BYTES, kb * kBlockElems, mt * TC_BM,
                         pol_x);

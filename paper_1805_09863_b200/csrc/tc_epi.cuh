@@ -29,6 +29,7 @@ struct TcParams {
   const int* __restrict__ N_dev;           // amun_output_layer_dev: N on the device (else NULL)
   const float* __restrict__ x_scale;       // e4m3 plans: [N] per-row scales of X (else NULL)
   const float* __restrict__ w_scale;       // e4m3 plans: [V_local] per-row scales of W
+  int a_box_bytes;                         // bytes of one X box (rows x 128; single-CTA kernel)
   int num_sms;                             // the device schedule's CTA count
 };
 
@@ -165,7 +166,9 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
     const int mt = PAIR ? 2 * unit + (int)rank : unit;
     const uint32_t tag = (uint32_t)mt + 1u;
     const int row = mt * TC_BM + row_local;
-    const bool live = mt * TC_BM < dyn.N;            // warp-uniform (padding M-tile of a pair)
+    // warp-uniform: this warp's 32 rows hold at least one real row (N <= 96
+    // leaves whole lane quadrants, and a pair's padding M-tile all four, idle)
+    const bool live = mt * TC_BM + q * 32 < dyn.N;
     const int limit = min(width, p.V_local - v0);
     const int nch = (width + 31) >> 5;
     const float* bsl = sbias + (tile % TC_NBIAS) * TC_BN;
