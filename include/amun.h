@@ -15,20 +15,23 @@
  *                                             beam x vocab of
  *                                             cost = prev_cost[r] + log p[r][v]
  *   + mini-batching (Alg. 2): remove finished hypotheses
- *     ("Remove h from b") by stable compaction.
+ *     ("Remove h from b") by stable compaction, or fused with the
+ *     beam reorder (amun_beam_advance); greedy argmax without the softmax
+ *     (Alg. 5, amun_argmax); 8-bit storage (amun_*_e4m3).
  *
  * Conventions (all entry points):
  *   - Every pointer argument that names device memory is a CUDA device
  *     pointer (cudaMalloc / torch CUDA storage) on the plan's device.
  *     The CALLER owns all memory: inputs, outputs and workspace. The library
  *     never allocates device memory and never synchronises the stream, except
- *     amun_compact() when counts_host != NULL.
+ *     amun_compact() / amun_beam_advance() when counts_host != NULL.
  *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default
  *     stream). Calls are stream-ordered and CUDA-graph capturable (except
- *     amun_compact with counts_host).
+ *     those two with counts_host).
  *   - Layouts are row-major, C order. dtype AMUN_BF16 means IEEE bfloat16
  *     storage (fp32 accumulation); AMUN_F32 means fp32 storage and true fp32
- *     products (SIMT kernel).
+ *     products (SIMT kernel); AMUN_E4M3 means OCP FP8 E4M3 codes with fp32
+ *     per-row scales (fp32 accumulation; the *_e4m3 entry points).
  *   - Errors: every call returns amun_status; no exception crosses the ABI.
  *     The message of the last failure on the calling thread is returned by
  *     amun_last_error(). Host-side validation happens before anything is
@@ -71,8 +74,9 @@ const char* amun_last_error(void);
 const char* amun_status_string(amun_status s);
 
 /* Create a plan for one vocabulary shard.
- *   H         hidden size (K of the GEMM). bf16: H % 8 == 0; f32: H % 4 == 0
- *             (TMA / vector alignment: a row is a multiple of 16 bytes).
+ *   H         hidden size (K of the GEMM). bf16: H % 8 == 0; f32: H % 4 == 0;
+ *             e4m3: H % 16 == 0 (TMA / vector alignment: a row is a
+ *             multiple of 16 bytes).
  *   V_local   rows of W (and entries of b) this plan owns, 1 <= V_local.
  *   v_offset  global token id of local row 0 (vocab sharding; 0 on one GPU).
  *   V_total   global vocabulary size; out_idx encodes r * V_total + token.
