@@ -144,3 +144,71 @@ class DecodeTrace:
         st.steps = t
         st.total_ms = t_all0.elapsed_time(t_all1)
         return st
+
+    def run_graph(self, X0, W, b, prev0, finish) -> TraceStats:
+        """Alg. 2 (dynamic) with every step on the device: N stays in device
+        memory (amun_output_layer_dev reads it; amun_compact writes it), the
+        bookkeeping glue uses fixed shapes over the N0-row buffers, and all
+        T_max steps are captured in ONE CUDA graph, timed as one replay.
+        Rows per step are logged on the device (they must equal the eager
+        dynamic mode's: the finish schedule alone decides them)."""
+        dev, S, B, N0 = self.dev, self.S, self.B, self.N0
+        st = TraceStats("dynamic_graph")
+        fin = finish.to(dev).reshape(-1).contiguous()
+        T = int(fin.max().item())
+        ar = torch.arange(N0, device=dev)
+        ar32 = ar.to(torch.int32)
+
+        def fresh():
+            cols = [X0.to(dev).contiguous(),
+                    torch.zeros(N0, self.state_floats, dtype=torch.float32, device=dev),
+                    prev0.to(dev).clone(), torch.arange(N0, dtype=torch.int64, device=dev)]
+            cols[1].copy_(torch.arange(N0, dtype=torch.float32, device=dev)[:, None])
+            return {"cols": [cols, [torch.empty_like(c) for c in cols]],
+                    "off": [(torch.arange(S + 1, dtype=torch.int32, device=dev) * B),
+                            torch.empty(S + 1, dtype=torch.int32, device=dev)],
+                    "cnt": [torch.tensor([N0, S], dtype=torch.int32, device=dev),
+                            torch.empty(2, dtype=torch.int32, device=dev)]}
+
+        idx = torch.empty((S, B), dtype=torch.int64, device=dev)
+        cost = torch.empty((S, B), dtype=torch.float32, device=dev)
+        k_s = torch.empty(S, dtype=torch.int32, device=dev)
+        alive = torch.empty(N0, dtype=torch.uint8, device=dev)
+        src_row = torch.empty(N0, dtype=torch.int32, device=dev)
+        rows_log = torch.zeros(T, dtype=torch.int32, device=dev)
+
+        def steps(state):
+            for t in range(T):
+                a, c = t % 2, (t + 1) % 2
+                X, prev, ids = state["cols"][a][0], state["cols"][a][2], state["cols"][a][3]
+                off, cnt = state["off"][a], state["cnt"][a]
+                torch.sub(off[1:], off[:-1], out=k_s)                       # live beam per sentence
+                self.ol.call_dev(X, W, b, prev, off, cnt[:1], B, k_s, out_idx=idx, out_cost=cost)
+                # synthetic beam bookkeeping (driver glue), fixed shapes over N0 rows
+                sent = torch.searchsorted(off[1:], ar32, right=True).clamp_(max=S - 1)
+                slot = (ar - off.to(torch.int64)[sent]).clamp_(0, B - 1)
+                prev.copy_(cost[sent, slot])
+                rows_log[t:t + 1].copy_(cnt[:1])
+                torch.logical_and(fin[ids] > t + 1, ar < cnt[0], out=alive.view(torch.bool))
+                compact([(x, y) for x, y in zip(state["cols"][a], state["cols"][c])], alive, off,
+                        state["off"][c], src_row, state["cnt"][c], sync=False)
+
+        s = torch.cuda.Stream(dev)
+        with torch.cuda.stream(s):
+            steps(fresh())                     # warm-up: kernels, plans, tensor maps
+            torch.cuda.synchronize()
+            state = fresh()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                steps(state)
+        e0, e1 = self._ev(), self._ev()
+        torch.cuda.synchronize()
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        st.total_ms = e0.elapsed_time(e1)
+        st.rows = [int(n) for n in rows_log.cpu().tolist()]
+        st.steps = T
+        self._graph_state = state              # (tests read the final state)
+        return st

@@ -118,3 +118,25 @@ def test_trace_full_size_sampled():
     dyn = tr.run(X, W.to(dev), b.to(dev), pc, f, mode="dynamic", check=check)
     assert seen["compact"] == dyn.steps and seen["ol"] == 4
     assert sum(dyn.rows) == int(f.sum())
+
+
+def test_trace_graph_mode_same_rows_as_dynamic():
+    """Alg. 2 with N on the device, all steps in one CUDA graph (run_graph):
+    the schedule alone decides the live rows, so every step must decode
+    exactly the rows the eager dynamic mode decodes."""
+    from paper_1805_09863_b200.trace import DecodeTrace
+    S, B, H, V = 40, 5, 128, 3000
+    w = synth.Workload("trace-graph", H=H, V=V, S=S, B=B, k=B, seed=synth.BASE_SEED + 45)
+    X, W, b, pc = synth.gen_X(w), synth.gen_W(w), synth.gen_b(w), synth.gen_prev_cost(w)
+    f = synth.eos_schedule(w.seed, S, B, p=1 / 4, cap=9)
+    dev = torch.device("cuda", 0)
+    tr = DecodeTrace(H, V, S, B, device=dev)
+    Wd, bd = W.to(dev), b.to(dev)
+    dyn = tr.run(X, Wd, bd, pc, f, mode="dynamic")
+    gr = tr.run_graph(X, Wd, bd, pc, f)
+    assert gr.rows[:len(dyn.rows)] == dyn.rows
+    assert all(n == 0 for n in gr.rows[len(dyn.rows):])
+    assert sum(gr.rows) == int(f.sum())
+    # the surviving ids after the last step: none (everything finished)
+    final = tr._graph_state["cnt"][gr.steps % 2]
+    assert int(final[0].item()) == 0

@@ -29,12 +29,19 @@ def main():
     tr.run(X, W, b, pc, f, mode="dynamic")        # warm-up
     dyn = tr.run(X, W, b, pc, f, mode="dynamic")
     nai = tr.run(X, W, b, pc, f, mode="naive")
+    gr = tr.run_graph(X, W, b, pc, f)
+    assert gr.rows[:len(dyn.rows)] == dyn.rows, "graph mode must decode the same rows per step"
     useful = int(f.sum())
     out = {"workload": f"trace: H={w.H}, V={w.V}, {S} sentences x beam {B}, geometric lengths "
                        f"(p=1/20, cap 60), hypothesis j finishes at L_s + j",
            "useful_rows": useful, "T_max": int(f.max()),
            "dynamic": dyn.summary(useful), "naive": nai.summary(useful),
-           "speedup_dynamic_vs_naive": nai.total_ms / dyn.total_ms}
+           "dynamic_graph": {"total_ms": gr.total_ms, "steps": gr.steps,
+                             "useful_rows_per_s": useful / (gr.total_ms * 1e-3),
+                             "note": "Alg. 2 with N on the device (amun_output_layer_dev + "
+                                     "amun_compact), all steps in one CUDA graph"},
+           "speedup_dynamic_vs_naive": nai.total_ms / dyn.total_ms,
+           "speedup_dynamic_graph_vs_naive": nai.total_ms / gr.total_ms}
     line = json.dumps(out)
     print(json.dumps({k: (v if not isinstance(v, dict) else {kk: vv for kk, vv in v.items()
                                                             if kk not in ("step_ms", "rows_per_step")})
