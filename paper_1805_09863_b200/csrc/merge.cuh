@@ -290,8 +290,16 @@ __device__ __forceinline__ void records_topk(const MergeParams& p, const float* 
   ol = kNegInf;
   ov = -1;
   for (int i = 0; i < p.k_max; ++i) {
-    const unsigned long long head = lv_key(lst.l[0], lst.v[0]);
-    const unsigned long long best = warp_max_u64(head);
+    // the max of the 64-bit key (ordered logit, inverted id) in two 32-bit
+    // warp reductions (one REDUX each): the best logit, then the lowest id
+    // among the lanes holding it; an empty head has key 0
+    const uint32_t hi = lst.v[0] < 0 ? 0u : f2o(lst.l[0]);
+    const uint32_t bhi = __reduce_max_sync(0xffffffffu, hi);
+    const uint32_t lo = (hi == bhi && lst.v[0] >= 0) ? (uint32_t)(0x7fffffff - lst.v[0]) : 0u;
+    const uint32_t blo = __reduce_max_sync(0xffffffffu, lo);
+    const unsigned long long best = ((unsigned long long)bhi << 32) | blo;
+    const unsigned long long head = lst.v[0] < 0 ? 0ull
+                                                 : (((unsigned long long)hi << 32) | (uint32_t)(0x7fffffff - lst.v[0]));
     if (best == 0ull) break;                  // warp-uniform: no more entries
     if (head == best) {                       // unique (token ids are unique in a row)
 #pragma unroll
