@@ -93,13 +93,15 @@ __device__ __forceinline__ uint32_t read_generation(const unsigned int* gen_ctr)
   return 1u + *reinterpret_cast<const volatile unsigned int*>(gen_ctr);
 }
 // Called once per CTA after all its work: the last CTA advances the generation.
+// No fences: every CTA read the generation at its start, long before the last
+// one finishes, and the next launch sees the new value (and the reset count)
+// across the kernel boundary; a fence here only delayed each CTA's exit
+// behind its partial-record stores (ncu: ~6% of greedy's stall samples).
 __device__ __forceinline__ void finish_generation(unsigned int* gen_ctr) {
-  __threadfence();
   const unsigned int prev = atomicAdd(gen_ctr + 1, 1u);
   if (prev == gridDim.x - 1) {   // every CTA has read the generation and finished
     gen_ctr[1] = 0u;
     atomicAdd(gen_ctr, 1u);
-    __threadfence();
   }
 }
 
