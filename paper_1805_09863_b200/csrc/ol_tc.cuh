@@ -73,7 +73,7 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
   constexpr int kCtrl = 4 * NG;                    // first control warp
   const int role = warp - kCtrl;                   // 0 = TMA, 1 = MMA, 2-3 idle, < 0 epilogue
 
-  for (int i = threadIdx.x; i < 4 * 128; i += blockDim.x) thr_x[i] = 0ull;   // no stale tags
+  for (int i = threadIdx.x; i < 4 * 128; i += blockDim.x) sts_u64(smem_u32(thr_x + i), 0ull);   // no stale tags
   if (role == 0 && lane == 0) {
     prefetch_tmap(&tmX);
     prefetch_tmap(&tmW);

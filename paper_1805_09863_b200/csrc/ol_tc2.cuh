@@ -62,7 +62,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<NG>::kThreads,
   const uint32_t rank = cluster_ctarank();          // 0 = leader, 1 = peer
   const int pair = blockIdx.x >> 1;
 
-  for (int i = threadIdx.x; i < 4 * 128; i += blockDim.x) thr_x[i] = 0ull;   // no stale tags
+  for (int i = threadIdx.x; i < 4 * 128; i += blockDim.x) sts_u64(smem_u32(thr_x + i), 0ull);   // no stale tags
   if (role == 0 && lane == 0) {
     prefetch_tmap(&tmX);
     prefetch_tmap(&tmW);

@@ -258,13 +258,14 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
 #pragma unroll
           for (int g2 = 0; g2 < NG; ++g2) {
             if (g2 != grp && AMUN_EXP != 3) {
-              const unsigned long long w = thr_x[g2 * 128 + row_local];
+              const unsigned long long w = lds_u64(smem_u32(thr_x + g2 * 128 + row_local));
               if ((uint32_t)(w >> 32) == tag) shared_kth = fmaxf(shared_kth, o2f((uint32_t)w));
             }
           }
           const float before = st.l[KB - 1];
           st.template chunk32r<true, MODE != 4>(x, p.v_offset + v0 + c0, fmaxf(hintv, shared_kth));
-          if (AMUN_EXP != 3 && st.l[KB - 1] > before) *my_thr = ((unsigned long long)tag << 32) | f2o(st.l[KB - 1]);
+          if (AMUN_EXP != 3 && st.l[KB - 1] > before)
+            sts_u64(smem_u32(my_thr), ((unsigned long long)tag << 32) | f2o(st.l[KB - 1]));
         }
       }
     }
