@@ -194,7 +194,8 @@ amun_status amun_argmax(amun_ol* plan, const void* X, const void* W, const float
  *   L[r][v] = (sum_h x8[r][h] w8[v][h]) * x_scale[r] * w_scale[v] + b[v]
  * on tcgen05.mma kind::f8f6f4 (fp32 accumulation), then the same softmax /
  * k-best / merge as amun_output_layer. Plan: amun_ol_create(..., AMUN_E4M3,
- * ...), H % 16 == 0; single-CTA kernel.
+ * ...), H % 16 == 0; single-CTA kernel; one vocabulary shard (there is no
+ * e4m3 partial / merge entry point yet).
  *   X8 [N, H] uint8, x_scale [N] fp32, W8 [V_local, H] uint8, w_scale
  *   [V_local] fp32 (16-byte aligned), other arguments as amun_output_layer.
  * Enqueues 2 kernels. Parity: the oracle computes on the exactly dequantised
