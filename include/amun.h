@@ -194,8 +194,8 @@ amun_status amun_argmax(amun_ol* plan, const void* X, const void* W, const float
  *   L[r][v] = (sum_h x8[r][h] w8[v][h]) * x_scale[r] * w_scale[v] + b[v]
  * on tcgen05.mma kind::f8f6f4 (fp32 accumulation), then the same softmax /
  * k-best / merge as amun_output_layer. Plan: amun_ol_create(..., AMUN_E4M3,
- * ...), H % 16 == 0; single-CTA kernel; one vocabulary shard (there is no
- * e4m3 partial / merge entry point yet).
+ * ...), H % 16 == 0; single-CTA kernel; vocab shards through
+ * amun_output_layer_partial_e4m3 + amun_merge_partials.
  *   X8 [N, H] uint8, x_scale [N] fp32, W8 [V_local, H] uint8, w_scale
  *   [V_local] fp32 (16-byte aligned), other arguments as amun_output_layer.
  * Enqueues 2 kernels. Parity: the oracle computes on the exactly dequantised
@@ -211,6 +211,12 @@ amun_status amun_output_layer_e4m3(amun_ol* plan, const uint8_t* X8, const float
 amun_status amun_ol_scores_e4m3(amun_ol* plan, const uint8_t* X8, const float* x_scale,
                                 const uint8_t* W8, const float* w_scale, const float* b, int N,
                                 int variant, void* workspace, void* stream);
+/* Vocab-shard piece 1 for e4m3 plans (as amun_output_layer_partial; the
+ * records merge with amun_merge_partials like bf16 ones). Arguments as
+ * amun_ol_scores_e4m3, partial [N, amun_ol_partial_stride(plan)] fp32. */
+amun_status amun_output_layer_partial_e4m3(amun_ol* plan, const uint8_t* X8, const float* x_scale,
+                                           const uint8_t* W8, const float* w_scale, const float* b,
+                                           int N, float* partial, void* workspace, void* stream);
 /* Per-row E4M3 quantisation: scale[r] = max_h |src[r][h]| / 448 (1 for an
  * all-zero row), dst[r][h] = RNE-to-E4M3(src[r][h] / scale[r]), saturating;
  * IEEE fp32 arithmetic, so the codes equal oracle.quantize_rows_e4m3 bit for

@@ -160,6 +160,17 @@ class OutputLayer:
         check(_L.amun_ol_scores_e4m3(self._h, _ptr(X8), _ptr(x_scale), _ptr(W8), _ptr(w_scale),
                                      _ptr(b), N, variant, _ptr(self.workspace), _stream(self.device)))
 
+    def partial_e4m3(self, X8, x_scale, W8, w_scale, b, out=None):
+        """FP8 vocab-shard piece 1: per-row partial record [N, stride] fp32."""
+        N = self._check_e4m3(X8, x_scale, W8, w_scale, b)
+        if out is None:
+            out = torch.empty((N, self.stride), dtype=torch.float32, device=self.device)
+        _need(out, "partial", torch.float32, self.device, (N, self.stride))
+        check(_L.amun_output_layer_partial_e4m3(self._h, _ptr(X8), _ptr(x_scale), _ptr(W8),
+                                                _ptr(w_scale), _ptr(b), N, _ptr(out),
+                                                _ptr(self.workspace), _stream(self.device)))
+        return out
+
     def scores(self, X, W, b):
         """Stage 1 only (fused GEMM + bias + online softmax stats + row k-best)."""
         N = self._check_scores(X, W, b)

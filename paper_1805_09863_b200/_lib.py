@@ -23,7 +23,7 @@ EXPORTS = [
     "amun_output_layer", "amun_output_layer_dev", "amun_ol_scores", "amun_ol_select", "amun_output_layer_partial",
     "amun_merge_partials", "amun_argmax", "amun_debug_logits", "amun_bench_variant", "amun_compact",
     "amun_beam_advance_workspace_bytes", "amun_beam_advance", "amun_output_layer_e4m3",
-    "amun_ol_scores_e4m3", "amun_quantize_e4m3",
+    "amun_ol_scores_e4m3", "amun_quantize_e4m3", "amun_output_layer_partial_e4m3",
 ]
 
 
@@ -74,6 +74,7 @@ def load() -> ctypes.CDLL:
                                         vp, vp]),
         "amun_ol_scores_e4m3": (st, [vp, vp, vp, vp, vp, vp, i32, i32, vp, vp]),
         "amun_quantize_e4m3": (st, [vp, i32, i32, i32, vp, vp, vp]),
+        "amun_output_layer_partial_e4m3": (st, [vp, vp, vp, vp, vp, vp, i32, vp, vp, vp]),
         "amun_beam_advance": (st, [vp, vp, i32, i32, ctypes.c_int64, i32, i32,
                                    ctypes.POINTER(amun_column), i32, vp, vp, vp, vp, vp, vp, vp,
                                    vp]),

@@ -404,6 +404,30 @@ MergeParams base_merge(const amun_ol* pl) {
 
 }  // namespace
 
+namespace {
+// Vocab-shard piece 1 for any tcgen05 / SIMT plan: the fused kernel, then
+// the row-mode merge into one record per row (scales: e4m3 plans only).
+amun_status partial_impl(amun_ol* plan, const void* X, const void* W, const float* b, int N,
+                         float* partial, void* workspace, void* stream, const float* x_scale,
+                         const float* w_scale) {
+  amun_status s = check_score_args(plan, X, W, b, N, workspace);
+  if (s != AMUN_OK) return s;
+  if (N == 0) return AMUN_OK;
+  if (!partial) return fail(AMUN_EINVAL, "NULL partial");
+  s = run_scores(plan, X, W, b, N, workspace, nullptr, static_cast<cudaStream_t>(stream), 0,
+                 nullptr, x_scale, w_scale);
+  if (s != AMUN_OK) return s;
+  MergeParams mp = base_merge(plan);
+  int grid_unused;
+  mp.part = static_cast<const float*>(workspace);
+  mp.layout = use_pairs(plan, N) ? 2 : 0;
+  mp.sch = make_schedule(plan, N, &grid_unused);
+  mp.N = N;
+  mp.out_part = partial;
+  return run_merge(plan, mp, true, (int)cdiv(N, MS_WARPS), static_cast<cudaStream_t>(stream));
+}
+}  // namespace
+
 extern "C" {
 
 int amun_abi_version(void) { return AMUN_ABI_VERSION; }
@@ -575,20 +599,17 @@ amun_status amun_output_layer_partial(amun_ol* plan, const void* X, const void* 
                                       void* stream) {
   if (plan && plan->dtype == AMUN_E4M3)
     return fail(AMUN_EINVAL, "e4m3 plans take the *_e4m3 entry points (they carry the scales)");
-  amun_status s = check_score_args(plan, X, W, b, N, workspace);
-  if (s != AMUN_OK) return s;
-  if (N == 0) return AMUN_OK;
-  if (!partial) return fail(AMUN_EINVAL, "NULL partial");
-  s = run_scores(plan, X, W, b, N, workspace, nullptr, static_cast<cudaStream_t>(stream), 0);
-  if (s != AMUN_OK) return s;
-  MergeParams mp = base_merge(plan);
-  int grid_unused;
-  mp.part = static_cast<const float*>(workspace);
-  mp.layout = use_pairs(plan, N) ? 2 : 0;
-  mp.sch = make_schedule(plan, N, &grid_unused);
-  mp.N = N;
-  mp.out_part = partial;
-  return run_merge(plan, mp, true, (int)cdiv(N, MS_WARPS), static_cast<cudaStream_t>(stream));
+  return partial_impl(plan, X, W, b, N, partial, workspace, stream, nullptr, nullptr);
+}
+
+amun_status amun_output_layer_partial_e4m3(amun_ol* plan, const uint8_t* X8, const float* x_scale,
+                                           const uint8_t* W8, const float* w_scale, const float* b,
+                                           int N, float* partial, void* workspace, void* stream) {
+  if (!plan) return fail(AMUN_EINVAL, "NULL plan");
+  if (plan->dtype != AMUN_E4M3) return fail(AMUN_EINVAL, "plan dtype is not AMUN_E4M3");
+  if (N > 0 && (!x_scale || !w_scale)) return fail(AMUN_EINVAL, "NULL x_scale / w_scale");
+  if (N > 0 && !aligned16(w_scale)) return fail(AMUN_EINVAL, "w_scale must be 16-byte aligned");
+  return partial_impl(plan, X8, W8, b, N, partial, workspace, stream, x_scale, w_scale);
 }
 
 amun_status amun_merge_partials(amun_ol* plan, const float* partials, int G,

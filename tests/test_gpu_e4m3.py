@@ -102,3 +102,36 @@ def test_e4m3_plan_rejects_bf16_entry_points():
     W = torch.zeros(100, 64, dtype=torch.uint8, device=DEV)
     with pytest.raises(amun().AmunError if hasattr(amun(), "AmunError") else Exception):
         ol.scores(X, W, torch.zeros(100, device=DEV))
+
+
+@pytest.mark.parametrize("G", [2, 3])
+def test_e4m3_vocab_shard_emulation(G):
+    """FP8 vocab shards (amun_output_layer_partial_e4m3 per shard, stacked like
+    an all-gather, amun_merge_partials): equal to the oracle on the full
+    dequantised vocabulary. W's per-row scales do not depend on the split."""
+    w = synth.Workload("f8shard", H=256, V=30000, S=16, B=4, k=6, seed=synth.BASE_SEED + 98)
+    X, W, b = synth.gen_X(w).float(), synth.gen_W(w).float(), synth.gen_b(w)
+    pc, off = synth.gen_prev_cost(w), synth.gen_offsets(w)
+    X8, xs = O.quantize_rows_e4m3(X.numpy())
+    W8, ws = O.quantize_rows_e4m3(W.numpy())
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+    per = -(-w.V // G)
+    per = -(-per // 256) * 256
+    bounds = [0]
+    while bounds[-1] < w.V:
+        bounds.append(min(w.V, bounds[-1] + per))
+    parts, plans = [], []
+    for g in range(len(bounds) - 1):
+        v0, v1 = bounds[g], bounds[g + 1]
+        ol = amun().OutputLayer(w.H, v1 - v0, v_offset=v0, V_total=w.V, dtype="e4m3", k_max=w.k,
+                                max_rows=w.N, max_sentences=w.S)
+        plans.append(ol)
+        parts.append(ol.partial_e4m3(t(X8), t(xs), t(W8[v0:v1]), t(ws[v0:v1]), b[v0:v1].to(DEV)))
+    idx, cost = plans[0].merge(torch.stack(parts), pc.to(DEV), off.to(DEV), w.k)
+    torch.cuda.synchronize()
+    L = O.add_bias(O.gemm(O.dequant_rows_e4m3(X8, xs), O.dequant_rows_e4m3(W8, ws)), O.as_f64(b))
+    logp = O.log_softmax(L)
+    pcd = O.as_f64(pc)
+    oi, _, oc64, nxt = O.kbest_sentences(logp, pcd, off.numpy(), w.k)
+    compare_kbest(idx.cpu().numpy(), cost.cpu().numpy(), lambda s, r, v: pcd[r] + logp[r, v],
+                  oc64, np.full(w.S, w.k), "bf16", w.V, o_next=nxt)
