@@ -217,6 +217,11 @@ amun_status amun_ol_scores_e4m3(amun_ol* plan, const uint8_t* X8, const float* x
 amun_status amun_output_layer_partial_e4m3(amun_ol* plan, const uint8_t* X8, const float* x_scale,
                                            const uint8_t* W8, const float* w_scale, const float* b,
                                            int N, float* partial, void* workspace, void* stream);
+/* Greedy argmax (Alg. 5) for e4m3 plans: as amun_argmax, out_logit =
+ * (sum_h x8 w8) * x_scale[r] * w_scale[token] + b[token]. */
+amun_status amun_argmax_e4m3(amun_ol* plan, const uint8_t* X8, const float* x_scale,
+                             const uint8_t* W8, const float* w_scale, const float* b, int N,
+                             int64_t* out_token, float* out_logit, void* workspace, void* stream);
 /* Per-row E4M3 quantisation: scale[r] = max_h |src[r][h]| / 448 (1 for an
  * all-zero row), dst[r][h] = RNE-to-E4M3(src[r][h] / scale[r]), saturating;
  * IEEE fp32 arithmetic, so the codes equal oracle.quantize_rows_e4m3 bit for

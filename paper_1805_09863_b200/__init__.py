@@ -171,6 +171,18 @@ class OutputLayer:
                                                 _ptr(self.workspace), _stream(self.device)))
         return out
 
+    def argmax_e4m3(self, X8, x_scale, W8, w_scale, b, out_token=None, out_logit=None):
+        """FP8 greedy argmax (Alg. 5): (token [N] int64, scaled biased logit [N] fp32)."""
+        N = self._check_e4m3(X8, x_scale, W8, w_scale, b)
+        if out_token is None:
+            out_token = torch.empty(N, dtype=torch.int64, device=self.device)
+        if out_logit is None:
+            out_logit = torch.empty(N, dtype=torch.float32, device=self.device)
+        check(_L.amun_argmax_e4m3(self._h, _ptr(X8), _ptr(x_scale), _ptr(W8), _ptr(w_scale),
+                                  _ptr(b), N, _ptr(out_token), _ptr(out_logit),
+                                  _ptr(self.workspace), _stream(self.device)))
+        return out_token, out_logit
+
     def scores(self, X, W, b):
         """Stage 1 only (fused GEMM + bias + online softmax stats + row k-best)."""
         N = self._check_scores(X, W, b)

@@ -24,6 +24,7 @@ EXPORTS = [
     "amun_merge_partials", "amun_argmax", "amun_debug_logits", "amun_bench_variant", "amun_compact",
     "amun_beam_advance_workspace_bytes", "amun_beam_advance", "amun_output_layer_e4m3",
     "amun_ol_scores_e4m3", "amun_quantize_e4m3", "amun_output_layer_partial_e4m3",
+    "amun_argmax_e4m3",
 ]
 
 
@@ -75,6 +76,7 @@ def load() -> ctypes.CDLL:
         "amun_ol_scores_e4m3": (st, [vp, vp, vp, vp, vp, vp, i32, i32, vp, vp]),
         "amun_quantize_e4m3": (st, [vp, i32, i32, i32, vp, vp, vp]),
         "amun_output_layer_partial_e4m3": (st, [vp, vp, vp, vp, vp, vp, i32, vp, vp, vp]),
+        "amun_argmax_e4m3": (st, [vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, vp]),
         "amun_beam_advance": (st, [vp, vp, i32, i32, ctypes.c_int64, i32, i32,
                                    ctypes.POINTER(amun_column), i32, vp, vp, vp, vp, vp, vp, vp,
                                    vp]),

@@ -218,8 +218,10 @@ template <int KB, int NG>
 amun_status launch_tc_f8(const CUtensorMap* mx, const CUtensorMap* mw, const TcParams& tp,
                          int grid, cudaStream_t st, int mode) {
   void (*kern)(const CUtensorMap, const CUtensorMap, const TcParams) =
-      mode == 0 ? ol_tc_kernel<KB, 0, NG, 1> : mode == 2 ? ol_tc_kernel<KB, 2, NG, 1>
-                                             : ol_tc_kernel<KB, 3, NG, 1>;
+      mode == 0 ? ol_tc_kernel<KB, 0, NG, 1>
+    : mode == 2 ? ol_tc_kernel<KB, 2, NG, 1>
+    : mode == 4 ? ol_tc_kernel<1, 4, NG, 1>
+                : ol_tc_kernel<KB, 3, NG, 1>;
   return launch_kernel<NG>(kern, mx, mw, tp, grid, st, TC_SMEM_F8);
 }
 
@@ -650,16 +652,16 @@ amun_status amun_debug_logits(amun_ol* plan, const void* X, const void* W, const
   return run_scores(plan, X, W, b, N, workspace, logits, static_cast<cudaStream_t>(stream), 1);
 }
 
-amun_status amun_argmax(amun_ol* plan, const void* X, const void* W, const float* b, int N,
-                        int64_t* out_token, float* out_logit, void* workspace, void* stream) {
-  if (plan && plan->dtype == AMUN_E4M3)
-    return fail(AMUN_EINVAL, "e4m3 plans take the *_e4m3 entry points (they carry the scales)");
+namespace {
+amun_status argmax_impl(amun_ol* plan, const void* X, const void* W, const float* b, int N,
+                        int64_t* out_token, float* out_logit, void* workspace, void* stream,
+                        const float* x_scale, const float* w_scale) {
   amun_status s = check_score_args(plan, X, W, b, N, workspace);
   if (s != AMUN_OK) return s;
   if (N > 0 && (!out_token || !out_logit)) return fail(AMUN_EINVAL, "NULL out_token / out_logit");
   if (N == 0) return AMUN_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  s = run_scores(plan, X, W, b, N, workspace, nullptr, st, 4);
+  s = run_scores(plan, X, W, b, N, workspace, nullptr, st, 4, nullptr, x_scale, w_scale);
   if (s != AMUN_OK) return s;
   MergeParams mp = base_merge(plan);
   int grid_unused;
@@ -672,6 +674,24 @@ amun_status amun_argmax(amun_ol* plan, const void* X, const void* W, const float
                                                  out_logit);
   CUDA_TRY(cudaGetLastError());
   return AMUN_OK;
+}
+}  // namespace
+
+amun_status amun_argmax(amun_ol* plan, const void* X, const void* W, const float* b, int N,
+                        int64_t* out_token, float* out_logit, void* workspace, void* stream) {
+  if (plan && plan->dtype == AMUN_E4M3)
+    return fail(AMUN_EINVAL, "e4m3 plans take the *_e4m3 entry points (they carry the scales)");
+  return argmax_impl(plan, X, W, b, N, out_token, out_logit, workspace, stream, nullptr, nullptr);
+}
+
+amun_status amun_argmax_e4m3(amun_ol* plan, const uint8_t* X8, const float* x_scale,
+                             const uint8_t* W8, const float* w_scale, const float* b, int N,
+                             int64_t* out_token, float* out_logit, void* workspace, void* stream) {
+  if (!plan) return fail(AMUN_EINVAL, "NULL plan");
+  if (plan->dtype != AMUN_E4M3) return fail(AMUN_EINVAL, "plan dtype is not AMUN_E4M3");
+  if (N > 0 && (!x_scale || !w_scale)) return fail(AMUN_EINVAL, "NULL x_scale / w_scale");
+  if (N > 0 && !aligned16(w_scale)) return fail(AMUN_EINVAL, "w_scale must be 16-byte aligned");
+  return argmax_impl(plan, X8, W8, b, N, out_token, out_logit, workspace, stream, x_scale, w_scale);
 }
 
 amun_status amun_ol_scores_e4m3(amun_ol* plan, const uint8_t* X8, const float* x_scale,

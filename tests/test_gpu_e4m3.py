@@ -135,3 +135,40 @@ def test_e4m3_vocab_shard_emulation(G):
     oi, _, oc64, nxt = O.kbest_sentences(logp, pcd, off.numpy(), w.k)
     compare_kbest(idx.cpu().numpy(), cost.cpu().numpy(), lambda s, r, v: pcd[r] + logp[r, v],
                   oc64, np.full(w.S, w.k), "bf16", w.V, o_next=nxt)
+
+
+def test_e4m3_argmax():
+    """FP8 greedy argmax (Alg. 5) vs oracle.argmax_1best on the dequantised
+    logits: exact in the integer regime (unit scales, lowest id on ties);
+    otherwise within the fp32 accumulation band (reading G16)."""
+    rng = np.random.default_rng(21)
+    N, H, V = 130, 64, 20000
+    X = rng.integers(-3, 4, (N, H)).astype(np.float32)
+    W = rng.integers(-3, 4, (V, H)).astype(np.float32)
+    X[:, 0] = 448.0
+    W[:, 0] = 448.0
+    b = rng.integers(-2, 3, V).astype(np.float32)
+    t = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+    for Xf, Wf, exact in [(X, W, True),
+                          (synth.gen_X(synth.CONFIGS["greedy"]).float().numpy()[:N, :H],
+                           synth.gen_W(synth.CONFIGS["greedy"]).float().numpy()[:V, :H], False)]:
+        N = Xf.shape[0]
+        X8, xs = O.quantize_rows_e4m3(Xf)
+        W8, ws = O.quantize_rows_e4m3(Wf)
+        ol = amun().OutputLayer(H, V, dtype="e4m3", k_max=1, max_rows=N, max_sentences=1)
+        tok, logit = ol.argmax_e4m3(t(X8), t(xs), t(W8), t(ws), t(b))
+        torch.cuda.synchronize()
+        P = O.gemm(O.dequant_rows_e4m3(X8, xs), O.dequant_rows_e4m3(W8, ws))
+        L = O.add_bias(P, O.as_f64(b))
+        ref = np.array([O.argmax_1best(P[r], O.as_f64(b)) for r in range(N)])
+        tok, logit = tok.cpu().numpy(), logit.cpu().numpy()
+        rows = np.arange(N)
+        if exact:
+            assert np.array_equal(tok, ref)
+            assert np.array_equal(logit.astype(np.float64), L[rows, ref])
+        else:
+            band = H * 2.0 ** -24 * (np.abs(O.dequant_rows_e4m3(X8, xs)) @
+                                     np.abs(O.dequant_rows_e4m3(W8, ws)).T).max(axis=1) \
+                + np.abs(L).max(axis=1) * 2.0 ** -22
+            assert (L[rows, ref] - L[rows, tok] <= 2 * band).all()
+            assert (tok == ref).mean() > 0.99
