@@ -63,7 +63,13 @@ typedef enum amun_status {
   AMUN_ECUDA = 3          /* a CUDA runtime/driver call failed */
 } amun_status;
 
-typedef enum amun_dtype { AMUN_F32 = 0, AMUN_BF16 = 1, AMUN_E4M3 = 2 } amun_dtype;
+typedef enum amun_dtype {
+  AMUN_F32 = 0,     /* fp32 X, W: SIMT kernel, true fp32 products */
+  AMUN_BF16 = 1,    /* bf16 X, W: tcgen05 kind::f16 */
+  AMUN_E4M3 = 2,    /* E4M3 codes + per-row fp32 scales: tcgen05 kind::f8f6f4 (*_e4m3 calls) */
+  AMUN_TF32X3 = 3   /* fp32 as 3xTF32 on tcgen05 kind::tf32: X, W passed pre-split by
+                       amun_split_tf32x3 as [N, 3H] / [V_local, 3H] fp32 rows */
+} amun_dtype;
 
 /* Opaque plan: shapes, kernel choice, persistent-grid schedule and cached TMA
  * tensor maps. Not thread-safe: use one plan per host thread. */
@@ -74,9 +80,9 @@ const char* amun_last_error(void);
 const char* amun_status_string(amun_status s);
 
 /* Create a plan for one vocabulary shard.
- *   H         hidden size (K of the GEMM). bf16: H % 8 == 0; f32: H % 4 == 0;
- *             e4m3: H % 16 == 0 (TMA / vector alignment: a row is a
- *             multiple of 16 bytes).
+ *   H         hidden size (K of the GEMM). bf16: H % 8 == 0; f32, tf32x3:
+ *             H % 4 == 0; e4m3: H % 16 == 0 (TMA / vector alignment: a row
+ *             is a multiple of 16 bytes).
  *   V_local   rows of W (and entries of b) this plan owns, 1 <= V_local.
  *   v_offset  global token id of local row 0 (vocab sharding; 0 on one GPU).
  *   V_total   global vocabulary size; out_idx encodes r * V_total + token.
@@ -137,8 +143,9 @@ amun_status amun_output_layer(amun_ol* plan, const void* X, const void* W, const
  * The fused kernel is launched with one CTA per SM and derives its schedule
  * from N on the device (CTAs without work only take part in setup). The
  * kernel is chosen from max_rows: CTA pairs (cta_group::2) when max_rows
- * spans >= 9 M-tiles of 128 rows, else single CTAs. bf16 plans only
- * (EUNSUPPORTED otherwise). Enqueues 2 kernels. */
+ * spans >= 9 M-tiles of 128 rows, else single CTAs (always for tf32x3).
+ * bf16 and tf32x3 plans (X then [max_rows, 3H] fp32); EUNSUPPORTED otherwise.
+ * Enqueues 2 kernels. */
 amun_status amun_output_layer_dev(amun_ol* plan, const void* X, const void* W, const float* b,
                                   const float* prev_cost, const int32_t* beam_offsets,
                                   const int32_t* N_dev, int S, const int32_t* k_per_sentence,
@@ -222,6 +229,15 @@ amun_status amun_output_layer_partial_e4m3(amun_ol* plan, const uint8_t* X8, con
 amun_status amun_argmax_e4m3(amun_ol* plan, const uint8_t* X8, const float* x_scale,
                              const uint8_t* W8, const float* w_scale, const float* b, int N,
                              int64_t* out_token, float* out_logit, void* workspace, void* stream);
+/* 3xTF32 split for AMUN_TF32X3 plans: every fp32 value x is
+ * split as hi = tf32(x) (round to nearest), lo = tf32(x - hi), and a row of H
+ * values becomes 3H values: role 0 (X) [hi | hi | lo], role 1 (W)
+ * [hi | lo | hi], so the plain tf32 GEMM over K = 3H computes
+ * X_hi W_hi + X_hi W_lo + X_lo W_hi (the 3xTF32 product; the dropped
+ * X_lo W_lo term is ~2^-22 relative).
+ *   src [R, H] fp32, dst [R, 3H] fp32, device; H % 4 == 0. One launch. */
+amun_status amun_split_tf32x3(const float* src, int R, int H, int role, float* dst, void* stream);
+
 /* Per-row E4M3 quantisation: scale[r] = max_h |src[r][h]| / 448 (1 for an
  * all-zero row), dst[r][h] = RNE-to-E4M3(src[r][h] / scale[r]), saturating;
  * IEEE fp32 arithmetic, so the codes equal oracle.quantize_rows_e4m3 bit for

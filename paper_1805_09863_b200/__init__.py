@@ -20,7 +20,7 @@ from ._lib import AMUN_MAX_COLUMNS, AMUN_MAX_K, AmunError, check
 
 _L = _lib.load()
 
-__all__ = ["OutputLayer", "compact", "beam_advance", "quantize_e4m3", "AmunError", "AMUN_MAX_K",
+__all__ = ["OutputLayer", "compact", "beam_advance", "quantize_e4m3", "split_tf32x3", "AmunError", "AMUN_MAX_K",
            "AMUN_MAX_COLUMNS", "lib_path"]
 
 lib_path = _lib.LIB_PATH
@@ -62,12 +62,14 @@ class OutputLayer:
         self.H, self.V_local, self.v_offset = H, V_local, v_offset
         self.V_total = V_local if V_total is None else V_total
         self.dtype = dtype
-        self.tdtype = {"bf16": torch.bfloat16, "f32": torch.float32, "e4m3": torch.uint8}[dtype]
+        self.tdtype = {"bf16": torch.bfloat16, "f32": torch.float32, "e4m3": torch.uint8,
+                       "tf32x3": torch.float32}[dtype]
+        self.K = 3 * H if dtype == "tf32x3" else H   # columns of X / W rows as passed
         self.k_max, self.max_rows, self.max_sentences = k_max, max_rows, max_sentences
         h = ctypes.c_void_p()
         check(_L.amun_ol_create(ctypes.byref(h), H, V_local, v_offset, self.V_total,
                                 {"bf16": _lib.AMUN_BF16, "f32": _lib.AMUN_F32,
-                                 "e4m3": _lib.AMUN_E4M3}[dtype],
+                                 "e4m3": _lib.AMUN_E4M3, "tf32x3": _lib.AMUN_TF32X3}[dtype],
                                 k_max, max_rows, max_sentences, dev.index or 0))
         self._h = h
         self.stride = _L.amun_ol_partial_stride(h)
@@ -83,8 +85,8 @@ class OutputLayer:
     # ------------------------------------------------------------- checks
     def _check_scores(self, X, W, b):
         N = X.shape[0]
-        _need(X, "X", self.tdtype, self.device, (N, self.H))
-        _need(W, "W", self.tdtype, self.device, (self.V_local, self.H))
+        _need(X, "X", self.tdtype, self.device, (N, self.K))
+        _need(W, "W", self.tdtype, self.device, (self.V_local, self.K))
         _need(b, "b", torch.float32, self.device, (self.V_local,))
         return N
 
@@ -123,8 +125,8 @@ class OutputLayer:
         """Steps 1-4 with the row count on the device (N = N_dev[0], no host
         sync): X [max_rows, H], prev_cost [max_rows]; rows >= N are ignored."""
         M = self.max_rows
-        _need(X, "X", self.tdtype, self.device, (M, self.H))
-        _need(W, "W", self.tdtype, self.device, (self.V_local, self.H))
+        _need(X, "X", self.tdtype, self.device, (M, self.K))
+        _need(W, "W", self.tdtype, self.device, (self.V_local, self.K))
         _need(b, "b", torch.float32, self.device, (self.V_local,))
         _need(N_dev, "N_dev", torch.int32, self.device)
         S = self._check_select(prev_cost, beam_offsets, M, k_per_sentence)
@@ -358,3 +360,18 @@ def quantize_e4m3(src, out=None, scale=None):
     check(_L.amun_quantize_e4m3(_ptr(src), _lib.AMUN_BF16 if src.dtype == torch.bfloat16 else _lib.AMUN_F32,
                                 R, H, _ptr(out), _ptr(scale), _stream(dev)))
     return out, scale
+
+
+def split_tf32x3(src, role: str, out=None):
+    """3xTF32 split for dtype="tf32x3" plans (amun_split_tf32x3): src [R, H]
+    fp32 -> [R, 3H] fp32 rows [hi | hi | lo] (role "X") or [hi | lo | hi]
+    (role "W"), hi = tf32(x), lo = tf32(x - hi)."""
+    if src.dim() != 2 or src.dtype != torch.float32 or not src.is_contiguous():
+        raise ValueError("src must be a contiguous 2-D fp32 tensor")
+    R, H = src.shape
+    if out is None:
+        out = torch.empty((R, 3 * H), dtype=torch.float32, device=src.device)
+    _need(out, "out", torch.float32, src.device, (R, 3 * H))
+    check(_L.amun_split_tf32x3(_ptr(src), R, H, {"X": 0, "W": 1}[role], _ptr(out),
+                               _stream(src.device)))
+    return out

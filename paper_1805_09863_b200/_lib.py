@@ -13,7 +13,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("AMUN_LIB", os.path.join(_HERE, "libamun.so"))
 
 AMUN_OK, AMUN_EINVAL, AMUN_EUNSUPPORTED, AMUN_ECUDA = 0, 1, 2, 3
-AMUN_F32, AMUN_BF16, AMUN_E4M3 = 0, 1, 2
+AMUN_F32, AMUN_BF16, AMUN_E4M3, AMUN_TF32X3 = 0, 1, 2, 3
 AMUN_MAX_K = 16
 AMUN_MAX_COLUMNS = 16
 
@@ -24,7 +24,7 @@ EXPORTS = [
     "amun_merge_partials", "amun_argmax", "amun_debug_logits", "amun_bench_variant", "amun_compact",
     "amun_beam_advance_workspace_bytes", "amun_beam_advance", "amun_output_layer_e4m3",
     "amun_ol_scores_e4m3", "amun_quantize_e4m3", "amun_output_layer_partial_e4m3",
-    "amun_argmax_e4m3",
+    "amun_argmax_e4m3", "amun_split_tf32x3",
 ]
 
 
@@ -77,6 +77,7 @@ def load() -> ctypes.CDLL:
         "amun_quantize_e4m3": (st, [vp, i32, i32, i32, vp, vp, vp]),
         "amun_output_layer_partial_e4m3": (st, [vp, vp, vp, vp, vp, vp, i32, vp, vp, vp]),
         "amun_argmax_e4m3": (st, [vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, vp]),
+        "amun_split_tf32x3": (st, [vp, i32, i32, i32, vp, vp]),
         "amun_beam_advance": (st, [vp, vp, i32, i32, ctypes.c_int64, i32, i32,
                                    ctypes.POINTER(amun_column), i32, vp, vp, vp, vp, vp, vp, vp,
                                    vp]),

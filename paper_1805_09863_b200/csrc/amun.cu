@@ -116,13 +116,17 @@ amun_status encode_map(amun_ol* pl, const void* ptr, long long rows, int box_row
                        CUtensorMap* out) {
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return fail(AMUN_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
-  const bool f8 = pl->dtype == AMUN_E4M3;   // 1-byte elements, 128 per 128-byte box row
-  cuuint64_t dims[2] = {(cuuint64_t)pl->H, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)pl->H * (f8 ? 1 : 2)};
-  cuuint32_t box[2] = {f8 ? 128u : 64u, (cuuint32_t)box_rows};
+  // 128-byte box rows: 64 bf16, 128 e4m3 codes, or 32 fp32 of the 3H-wide tf32x3 rows
+  const bool f8 = pl->dtype == AMUN_E4M3, t3 = pl->dtype == AMUN_TF32X3;
+  const cuuint64_t K = t3 ? 3ull * pl->H : (cuuint64_t)pl->H;
+  cuuint64_t dims[2] = {K, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {K * (f8 ? 1 : t3 ? 4 : 2)};
+  cuuint32_t box[2] = {f8 ? 128u : t3 ? 32u : 64u, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(out, f8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
-                   const_cast<void*>(ptr), dims, strides,
+  CUresult r = enc(out,
+                   f8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                      : t3 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                   2, const_cast<void*>(ptr), dims, strides,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(AMUN_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
@@ -225,6 +229,20 @@ amun_status launch_tc_f8(const CUtensorMap* mx, const CUtensorMap* mw, const TcP
   return launch_kernel<NG>(kern, mx, mw, tp, grid, st, TC_SMEM_F8);
 }
 
+// tf32x3 plans: single CTAs; every mode (the fused path, the test/bench
+// builds and the argmax kernel).
+template <int KB, int NG>
+amun_status launch_tc_t3(const CUtensorMap* mx, const CUtensorMap* mw, const TcParams& tp,
+                         int grid, cudaStream_t st, int mode) {
+  void (*kern)(const CUtensorMap, const CUtensorMap, const TcParams) =
+      mode == 0 ? ol_tc_kernel<KB, 0, NG, 2>
+    : mode == 1 ? ol_tc_kernel<1, 1, NG, 2>
+    : mode == 2 ? ol_tc_kernel<KB, 2, NG, 2>
+    : mode == 3 ? ol_tc_kernel<KB, 3, NG, 2>
+                : ol_tc_kernel<1, 4, NG, 2>;
+  return launch_kernel<NG>(kern, mx, mw, tp, grid, st, TC_SMEM);
+}
+
 // Two epilogue warpgroups. bf16: measured faster than three or four (their
 // extra warps cost issue slots and registers while the tensor pipe bounds;
 // DESIGN.md §6.1). e4m3: four measured within run-to-run noise of two
@@ -233,6 +251,7 @@ amun_status launch_tc_f8(const CUtensorMap* mx, const CUtensorMap* mw, const TcP
 template <int KB>
 amun_status launch_tc(amun_ol* pl, const CUtensorMap* mx, const CUtensorMap* mw,
                       const TcParams& tp, int grid, cudaStream_t st, int mode, bool pairs) {
+  if (pl->dtype == AMUN_TF32X3) return launch_tc_t3<KB, 2>(mx, mw, tp, grid, st, mode);
   if (pl->dtype == AMUN_E4M3) {
 #ifdef AMUN_WITH_NG4
     if (pl->ng_override == 4) return launch_tc_f8<KB, 4>(mx, mw, tp, grid, st, mode);
@@ -299,7 +318,9 @@ amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b
     tp.N = N;
     tp.V_local = pl->V_local;
     tp.v_offset = pl->v_offset;
-    tp.n_kblk = (int)cdiv(pl->H, pl->dtype == AMUN_E4M3 ? 2 * TC_BK : TC_BK);
+    tp.n_kblk = (int)(pl->dtype == AMUN_E4M3 ? cdiv(pl->H, 2 * TC_BK)
+                      : pl->dtype == AMUN_TF32X3 ? cdiv(3LL * pl->H, TC_BK / 2)
+                                                 : cdiv(pl->H, TC_BK));
     tp.x_scale = x_scale;
     tp.w_scale = w_scale;
     tp.a_box_bytes = a_rows * 128;   // 128 bytes of K per row (bf16 and e4m3 alike)
@@ -451,11 +472,12 @@ amun_status amun_ol_create(amun_ol** plan, int H, int V_local, int v_offset, int
                            int device) {
   if (!plan) return fail(AMUN_EINVAL, "NULL plan pointer");
   *plan = nullptr;
-  if (dtype != AMUN_F32 && dtype != AMUN_BF16 && dtype != AMUN_E4M3)
+  if (dtype != AMUN_F32 && dtype != AMUN_BF16 && dtype != AMUN_E4M3 && dtype != AMUN_TF32X3)
     return fail(AMUN_EINVAL, "unknown dtype %d", (int)dtype);
   if (H < 1) return fail(AMUN_EINVAL, "H=%d must be >= 1", H);
   if (dtype == AMUN_BF16 && H % 8 != 0) return fail(AMUN_EINVAL, "bf16 needs H %% 8 == 0 (H=%d)", H);
-  if (dtype == AMUN_F32 && H % 4 != 0) return fail(AMUN_EINVAL, "f32 needs H %% 4 == 0 (H=%d)", H);
+  if ((dtype == AMUN_F32 || dtype == AMUN_TF32X3) && H % 4 != 0)
+    return fail(AMUN_EINVAL, "f32 / tf32x3 need H %% 4 == 0 (H=%d)", H);
   if (dtype == AMUN_E4M3 && H % 16 != 0) return fail(AMUN_EINVAL, "e4m3 needs H %% 16 == 0 (H=%d)", H);
   if (V_local < 1) return fail(AMUN_EINVAL, "V_local=%d must be >= 1", V_local);
   if (v_offset < 0 || V_total < 1 || (long long)v_offset + V_local > V_total)
@@ -567,7 +589,8 @@ amun_status amun_output_layer_dev(amun_ol* plan, const void* X, const void* W, c
                                   void* stream) {
   if (!plan) return fail(AMUN_EINVAL, "NULL plan");
   if (!N_dev) return fail(AMUN_EINVAL, "NULL N_dev");
-  if (plan->dtype != AMUN_BF16) return fail(AMUN_EUNSUPPORTED, "device-side N: bf16 plans only");
+  if (plan->dtype != AMUN_BF16 && plan->dtype != AMUN_TF32X3)
+    return fail(AMUN_EUNSUPPORTED, "device-side N: bf16 / tf32x3 plans only");
   const int Nmax = plan->max_rows;
   amun_status s = check_score_args(plan, X, W, b, Nmax, workspace);
   if (s != AMUN_OK) return s;
@@ -877,5 +900,17 @@ amun_status amun_debug_counters(unsigned long long* host8, int reset) {
   return AMUN_OK;
 }
 #endif
+
+amun_status amun_split_tf32x3(const float* src, int R, int H, int role, float* dst, void* stream) {
+  if (R < 0 || H < 0 || (H & 3)) return fail(AMUN_EINVAL, "R=%d, H=%d: need R, H >= 0, H %% 4 == 0", R, H);
+  if (role != 0 && role != 1) return fail(AMUN_EINVAL, "role %d not in {0 (X), 1 (W)}", role);
+  if (R == 0 || H == 0) return AMUN_OK;
+  if (!src || !dst) return fail(AMUN_EINVAL, "NULL src/dst");
+  const long long n = (long long)R * H;
+  const int grid = (int)std::min<long long>(cdiv(n, 256), 148LL * 32);
+  split_tf32x3_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(src, n, H, role, dst);
+  CUDA_TRY(cudaGetLastError());
+  return AMUN_OK;
+}
 
 }  // extern "C"

@@ -38,7 +38,10 @@ static_assert(TC_NBIAS >= 2 + TC_STAGES, "bias ring too small for the producer's
 
 // ELT = 0: bf16 X, W (kind::f16, 64 elements per 128-byte K block);
 // ELT = 1: e4m3 X, W with per-row scales (kind::f8f6f4, 128 elements per
-// block; NEXT f4, the modern analogue of the paper's 16-bit storage P:264-268).
+// block; NEXT f4, the modern analogue of the paper's 16-bit storage P:264-268);
+// ELT = 2: fp32 as 3xTF32 (kind::tf32, 32 elements per block): rows stored
+// as [X_hi | X_hi | X_lo] and [W_hi | W_lo | W_hi], so the K = 3H product is
+// X_hi W_hi + X_hi W_lo + X_lo W_hi (NEXT f2).
 template <int KB, int MODE, int NG, int ELT = 0>
 __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
     ol_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
@@ -60,7 +63,7 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bfull + TC_NBIAS);
   uint32_t* gen_smem = tmem_holder + 1;
   // e4m3 column-scale ring, after the 512-byte barrier area (TC_SMEM_F8)
-  float* sscale = (ELT != 0 && scale_ring_ok(p, TC_STAGES))
+  float* sscale = (ELT == 1 && scale_ring_ok(p, TC_STAGES))
                       ? reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 512)
                       : nullptr;
 
@@ -120,7 +123,8 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
           mbar_wait_spin(&empty[stage], phase ^ 1);
           if (lane == 0) {
             mbar_arrive_expect_tx(&full[stage], p.a_box_bytes + TC_B_BYTES);
-            constexpr int kBlockElems = ELT ? 2 * TC_BK : TC_BK;   // 128 bytes of K either way
+            // 128 bytes of K per block: 64 bf16, 128 e4m3 or 32 fp32 (tf32x3)
+            constexpr int kBlockElems = ELT == 1 ? 2 * TC_BK : ELT == 2 ? TC_BK / 2 : TC_BK;
             tma_load_2d(&tmX, &full[stage], sA + stage * TC_A_BYTES, kb * kBlockElems, mt * TC_BM,
                         pol_x);
             tma_load_2d(&tmW, &full[stage], sB + stage * TC_B_BYTES, kb * kBlockElems, v0, 0ull);
@@ -148,7 +152,9 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
         mbar_wait_spin(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d = tmem_base + acc * TC_BN;
-        const uint32_t idesc = ELT ? idesc_e4m3_f32(TC_BM, width) : idesc_bf16_f32(TC_BM, width);
+        const uint32_t idesc = ELT == 1 ? idesc_e4m3_f32(TC_BM, width)
+                             : ELT == 2 ? idesc_tf32_f32(TC_BM, width)
+                                        : idesc_bf16_f32(TC_BM, width);
         for (int kb = 0; kb < p.n_kblk; ++kb) {
           mbar_wait_spin(&full[stage], phase);
           tc_fence_after();
@@ -159,8 +165,10 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
             for (int k = 0; k < TC_BK / 16; ++k) {   // +32 bytes of K per MMA (>>4 = 2)
               if constexpr (ELT == 0)
                 mma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
-              else
+              else if constexpr (ELT == 1)
                 mma_e4m3(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+              else
+                mma_tf32(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
             }
             mma_commit(&empty[stage]);              // smem slot free once these MMAs finish
           }

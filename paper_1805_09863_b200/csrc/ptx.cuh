@@ -166,6 +166,17 @@ __device__ __forceinline__ void mma_e4m3(uint32_t d_tmem, uint64_t adesc, uint64
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// TF32: D(fp32) += A(tf32) * B(tf32)^T from fp32 storage, K = 8 per
+// instruction (32 bytes of K, the same descriptor advance again).
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 // Arrive on an mbarrier when all previously issued tcgen05.mma of this thread
 // complete (implies tcgen05.fence::before_thread_sync).
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -226,6 +237,16 @@ __device__ __forceinline__ uint32_t idesc_bf16_f32(int M, int N) {
   return d;
 }
 
+// instruction descriptor, kind::tf32: D = F32, A = B = TF32 (format 2)
+__device__ __forceinline__ uint32_t idesc_tf32_f32(int M, int N) {
+  uint32_t d = 0;
+  d |= 1u << 4;                           // c_format = F32
+  d |= 2u << 7;                           // a_format = TF32
+  d |= 2u << 10;                          // b_format = TF32
+  d |= (uint32_t)(N >> 3) << 17;          // n_dim
+  d |= (uint32_t)(M >> 4) << 24;          // m_dim
+  return d;
+}
 // instruction descriptor, kind::f8f6f4: D = F32 (bit 4), A = B = E4M3 (format 0)
 __device__ __forceinline__ uint32_t idesc_e4m3_f32(int M, int N) {
   uint32_t d = 0;

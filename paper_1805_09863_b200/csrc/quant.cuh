@@ -49,4 +49,25 @@ __global__ void __launch_bounds__(QZ_THREADS) quantize_e4m3_kernel(const void* _
   }
 }
 
+// 3xTF32 split (amun_split_tf32x3): hi = tf32(x), lo = tf32(x - hi); row r
+// of dst = role 0: [hi | hi | lo], role 1: [hi | lo | hi].
+__global__ void split_tf32x3_kernel(const float* __restrict__ src, long long n, int H, int role,
+                                    float* __restrict__ dst) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / H;
+    const int h = (int)(i - r * H);
+    const float x = src[i];
+    uint32_t hb, lb;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(x));
+    const float hi = __uint_as_float(hb);
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lb) : "f"(x - hi));
+    const float lo = __uint_as_float(lb);
+    float* row = dst + r * 3LL * H;
+    row[h] = hi;
+    row[H + h] = role == 0 ? hi : lo;
+    row[2 * H + h] = role == 0 ? lo : hi;
+  }
+}
+
 }  // namespace amun

@@ -174,7 +174,7 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
     const int limit = min(width, p.V_local - v0);
     const int nch = (width + 31) >> 5;
     const float* bsl = sbias + (tile % TC_NBIAS) * TC_BN;
-    const float xs = (ELT != 0 && row < dyn.N) ? __ldg(p.x_scale + row) : 1.f;   // e4m3 row scale
+    const float xs = (ELT == 1 && row < dyn.N) ? __ldg(p.x_scale + row) : 1.f;   // e4m3 row scale
     // request the newest cross-CTA hint now (L2, not L1: other SMs update it);
     // it is folded in after this tile's chunks, for the next tile of the segment
     // (per-chunk exchange halves the insertions but its loads and atomics cost
@@ -191,7 +191,7 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
       const int nv = limit - c0;
       if (nv >= 32) {   // full chunk: bias from the ring (same address in all lanes)
         const uint32_t b4 = smem_u32(bsl + c0);
-        if constexpr (ELT == 0) {
+        if constexpr (ELT != 1) {   // bf16 / tf32x3: + bias
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const float4 bq = lds128(b4 + 16 * j);
@@ -224,7 +224,7 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const float bj = (j < nv4) ? bsl[c0 + j] : ((j < nv) ? __ldg(p.bias + v0 + c0 + j) : 0.f);
-          if constexpr (ELT == 0) {
+          if constexpr (ELT != 1) {
             x[j] = (j < nv) ? __uint_as_float(r[j]) + bj : kNegInf;
           } else {
             const float sj = (j < nv) ? xs * __ldg(p.w_scale + v0 + c0 + j) : 0.f;
