@@ -319,6 +319,72 @@ amun_status amun_beam_advance(const int64_t* out_idx, const float* out_cost, int
                               int32_t* new_token, float* new_cost, int32_t* counts,
                               int32_t* counts_host, void* workspace, void* stream);
 
+/* ------------------------------------------------------------------------
+ * NVLink one-shot exchange: the vocab-sharded output
+ * layer (Alg. 6; the reduce of P:244-251 applied to the
+ * (max, sum, k-best) partial states of P:232-242) with the exchange done by
+ * the library's own kernel over peer memory instead of a collective call.
+ * After this rank's fused kernel, one cooperative kernel combines the rank's
+ * per-CTA records into one record per row, stores it into slot [rank] of
+ * EVERY rank's receive buffer (CUDA IPC mappings: NVLink stores), signals
+ * each rank (system-scope release), waits for all G ranks' signals
+ * (acquire), and runs the per-sentence top-k_s over the G records of each
+ * row. Every rank returns the same result as amun_output_layer_partial on
+ * each shard + an all-gather + amun_merge_partials.
+ *
+ * Buffer: one per rank, from amun_oneshot_alloc (a whole cudaMalloc
+ * allocation, zeroed, the one place the library allocates: IPC exports whole
+ * allocations), amun_oneshot_buffer_bytes(plan, G) bytes: a 256-byte control
+ * block (monotonic per-source signal counters, the rank's call epoch) and
+ * fp32 receive records [2][G][max_rows][stride], double-buffered by epoch
+ * parity. The counters are never reset: every rank must make the same
+ * sequence of calls with the same G (the epochs stay in lockstep), CUDA-graph
+ * replays included. The calling processes must be on one node with
+ * peer access between their GPUs (NVLink / NVSwitch).
+ *
+ * amun_oneshot_alloc: *buf = device buffer of this plan's device; if
+ *   ipc_handle != NULL, 64 bytes (cudaIpcMemHandle_t) are written there for
+ *   the other ranks. Synchronises the device (zeroing). EINVAL / ECUDA.
+ * amun_oneshot_open: maps another process's buffer (ipc_handle from its
+ *   amun_oneshot_alloc) into this process on `device`; *peer is that
+ *   mapping. amun_oneshot_close unmaps it; amun_oneshot_free frees an own
+ *   buffer. A process never opens its own handle (use its own pointer).
+ * amun_output_layer_oneshot:
+ *   plan, X, W, b, prev_cost, beam_offsets, N, S, k_per_sentence, k,
+ *   out_idx, out_cost, workspace: as amun_output_layer for this rank's vocab
+ *   shard (plan's v_offset / V_local / V_total); N, S, prev_cost,
+ *   beam_offsets, k_per_sentence and k are the same on every rank.
+ *   bufs    host array [G] of device pointers: bufs[p] = rank p's buffer as
+ *           mapped in this process (bufs[rank] = the own buffer), 256-byte
+ *           aligned; 1 <= G <= 8, 0 <= rank < G.
+ *   Enqueues 2 kernels (fused, then the one-shot kernel) on `stream`. The
+ *   call returns before the peers have signalled; a rank whose peers never
+ *   make the matching call waits forever (as in any collective).
+ *   EINVAL on argument errors (nothing enqueued).
+ * amun_output_layer_oneshot_emulated (test / measurement hook): G ranks on
+ *   ONE GPU. Runs the G shards' fused kernels one after another, then ONE
+ *   cooperative launch with a grid row per rank (ranks whose blocks wait on
+ *   one another must share a kernel on one GPU). plans[p] / W[p] / b[p] /
+ *   workspaces[p] / bufs[p] / out_idx[p] / out_cost[p] are rank p's; the
+ *   plans must agree in k_max, max_rows, max_sentences, V_total and device. */
+size_t amun_oneshot_buffer_bytes(const amun_ol* plan, int G);
+amun_status amun_oneshot_alloc(const amun_ol* plan, int G, void** buf, void* ipc_handle);
+amun_status amun_oneshot_free(void* buf);
+amun_status amun_oneshot_open(const void* ipc_handle, int device, void** peer);
+amun_status amun_oneshot_close(void* peer);
+amun_status amun_output_layer_oneshot(amun_ol* plan, const void* X, const void* W, const float* b,
+                                      const float* prev_cost, const int32_t* beam_offsets, int N,
+                                      int S, const int32_t* k_per_sentence, int k,
+                                      void* const* bufs, int G, int rank, int64_t* out_idx,
+                                      float* out_cost, void* workspace, void* stream);
+amun_status amun_output_layer_oneshot_emulated(amun_ol* const* plans, int G, const void* X,
+                                               const void* const* W, const float* const* b,
+                                               const float* prev_cost, const int32_t* beam_offsets,
+                                               int N, int S, const int32_t* k_per_sentence, int k,
+                                               void* const* bufs, int64_t* const* out_idx,
+                                               float* const* out_cost, void* const* workspaces,
+                                               void* stream);
+
 #ifdef __cplusplus
 }
 #endif

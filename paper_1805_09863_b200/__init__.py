@@ -56,7 +56,9 @@ class OutputLayer:
 
     def __init__(self, H: int, V_local: int, *, v_offset: int = 0, V_total: int | None = None,
                  dtype: str = "bf16", k_max: int = 16, max_rows: int = 1 << 16,
-                 max_sentences: int = 1 << 16, device: int | torch.device = 0):
+                 max_sentences: int = 1 << 16, device: int | torch.device | None = 0):
+        if device is None:
+            device = torch.cuda.current_device()
         dev = torch.device("cuda", device) if isinstance(device, int) else torch.device(device)
         self.device = dev
         self.H, self.V_local, self.v_offset = H, V_local, v_offset
@@ -118,6 +120,22 @@ class OutputLayer:
                                    _ptr(beam_offsets), N, S, _ptr(k_per_sentence), k,
                                    _ptr(out_idx), _ptr(out_cost), _ptr(self.workspace),
                                    _stream(self.device)))
+        return out_idx, out_cost
+
+    def oneshot(self, X, W, b, prev_cost, beam_offsets, k: int, bufs, rank: int,
+                k_per_sentence=None, out_idx=None, out_cost=None):
+        """Steps 1-4 of this rank's vocab shard with the NVLink one-shot
+        exchange + merge (amun_output_layer_oneshot, NEXT f3). bufs: every
+        rank's one-shot buffer as mapped here (device pointers, rank order;
+        sharded.OneShotExchange). Every rank makes the same call."""
+        N = self._check_scores(X, W, b)
+        S = self._check_select(prev_cost, beam_offsets, N, k_per_sentence)
+        out_idx, out_cost = self._outputs(S, k, out_idx, out_cost)
+        arr = (ctypes.c_void_p * len(bufs))(*[int(p) for p in bufs])
+        check(_L.amun_output_layer_oneshot(self._h, _ptr(X), _ptr(W), _ptr(b), _ptr(prev_cost),
+                                           _ptr(beam_offsets), N, S, _ptr(k_per_sentence), k,
+                                           arr, len(bufs), rank, _ptr(out_idx), _ptr(out_cost),
+                                           _ptr(self.workspace), _stream(self.device)))
         return out_idx, out_cost
 
     def call_dev(self, X, W, b, prev_cost, beam_offsets, N_dev, k: int, k_per_sentence=None,

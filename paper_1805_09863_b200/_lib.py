@@ -24,8 +24,11 @@ EXPORTS = [
     "amun_merge_partials", "amun_argmax", "amun_debug_logits", "amun_bench_variant", "amun_compact",
     "amun_beam_advance_workspace_bytes", "amun_beam_advance", "amun_output_layer_e4m3",
     "amun_ol_scores_e4m3", "amun_quantize_e4m3", "amun_output_layer_partial_e4m3",
-    "amun_argmax_e4m3", "amun_split_tf32x3",
+    "amun_argmax_e4m3", "amun_split_tf32x3", "amun_oneshot_buffer_bytes", "amun_oneshot_alloc",
+    "amun_oneshot_free", "amun_oneshot_open", "amun_oneshot_close", "amun_output_layer_oneshot",
+    "amun_output_layer_oneshot_emulated",
 ]
+AMUN_ONESHOT_MAX_G = 8
 
 
 class amun_column(ctypes.Structure):
@@ -78,6 +81,17 @@ def load() -> ctypes.CDLL:
         "amun_output_layer_partial_e4m3": (st, [vp, vp, vp, vp, vp, vp, i32, vp, vp, vp]),
         "amun_argmax_e4m3": (st, [vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, vp]),
         "amun_split_tf32x3": (st, [vp, i32, i32, i32, vp, vp]),
+        "amun_oneshot_buffer_bytes": (sz, [vp, i32]),
+        "amun_oneshot_alloc": (st, [vp, i32, ctypes.POINTER(vp), vp]),
+        "amun_oneshot_free": (st, [vp]),
+        "amun_oneshot_open": (st, [vp, i32, ctypes.POINTER(vp)]),
+        "amun_oneshot_close": (st, [vp]),
+        "amun_output_layer_oneshot": (st, [vp, vp, vp, vp, vp, vp, i32, i32, vp, i32,
+                                           ctypes.POINTER(vp), i32, i32, vp, vp, vp, vp]),
+        "amun_output_layer_oneshot_emulated": (st, [ctypes.POINTER(vp), i32, vp, ctypes.POINTER(vp),
+                                                    ctypes.POINTER(vp), vp, vp, i32, i32, vp, i32,
+                                                    ctypes.POINTER(vp), ctypes.POINTER(vp),
+                                                    ctypes.POINTER(vp), ctypes.POINTER(vp), vp]),
         "amun_beam_advance": (st, [vp, vp, i32, i32, ctypes.c_int64, i32, i32,
                                    ctypes.POINTER(amun_column), i32, vp, vp, vp, vp, vp, vp, vp,
                                    vp]),

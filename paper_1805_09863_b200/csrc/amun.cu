@@ -20,6 +20,7 @@
 #include "ol_simt.cuh"
 #include "ol_tc.cuh"
 #include "ol_tc2.cuh"
+#include "oneshot.cuh"
 #include "quant.cuh"
 
 using namespace amun;
@@ -911,6 +912,206 @@ amun_status amun_split_tf32x3(const float* src, int R, int H, int role, float* d
   split_tf32x3_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(src, n, H, role, dst);
   CUDA_TRY(cudaGetLastError());
   return AMUN_OK;
+}
+
+
+// ------------------------------------------------------------ NVLink one-shot (NEXT f3)
+}  // extern "C"
+
+namespace {
+
+size_t oneshot_recv_elems(const amun_ol* pl, int G) {
+  return (size_t)G * (size_t)std::max(pl->max_rows, 1) * (size_t)pl->stride;
+}
+
+// CTAs per rank: all co-resident (cooperative launch); the count may differ
+// between calls and ranks (the signal counters count calls, not CTAs).
+template <int KB>
+amun_status oneshot_launch(const amun_ol* pl, OneShotParams& q, int ranks, cudaStream_t st) {
+  int occ = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, oneshot_kernel<KB>, MS_WARPS * 32, 0));
+  // as many CTAs as there are rows (one warp each) or sentences (one CTA
+  // each), up to what is co-resident (<= 4 per SM)
+  if (occ < 1) return fail(AMUN_ECUDA, "one-shot kernel does not fit on an SM");
+  const int cap = std::max(1, pl->num_sms * std::min(occ, 4) / ranks);
+  const int want = std::max((int)cdiv(q.dst.N, MS_WARPS), q.dst.S);
+  q.nb = std::max(1, std::min(cap, want));
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3((unsigned)q.nb, (unsigned)ranks, 1);
+  cfg.blockDim = dim3(MS_WARPS * 32, 1, 1);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, oneshot_kernel<KB>, q));
+  return AMUN_OK;
+}
+
+amun_status oneshot_run(const amun_ol* pl, OneShotParams& q, int ranks, cudaStream_t st) {
+#define OS_CALL(K) oneshot_launch<K>(pl, q, ranks, st)
+  AMUN_KB_SWITCH(pl->kb, OS_CALL)
+#undef OS_CALL
+}
+
+MergeParams oneshot_src(amun_ol* pl, void* workspace, int N) {
+  MergeParams mp = base_merge(pl);
+  int grid_unused;
+  mp.part = static_cast<const float*>(workspace);
+  mp.layout = use_pairs(pl, N > 0 ? N : 1) ? 2 : 0;
+  mp.sch = make_schedule(pl, N > 0 ? N : 1, &grid_unused);
+  mp.N = N;
+  return mp;
+}
+
+MergeParams oneshot_dst(const amun_ol* pl, int G, const float* prev_cost,
+                        const int32_t* beam_offsets, int N, int S, const int32_t* k_s, int k) {
+  MergeParams mp = base_merge(pl);
+  mp.layout = 1;
+  mp.G = G;
+  mp.N = N;
+  mp.S = S;
+  mp.prev_cost = prev_cost;
+  mp.offsets = beam_offsets;
+  mp.k_s = k_s;
+  mp.k = k;
+  return mp;
+}
+
+amun_status check_bufs(void* const* bufs, int G) {
+  if (G < 1 || G > OS_MAX_G) return fail(AMUN_EINVAL, "G=%d out of [1, %d]", G, OS_MAX_G);
+  if (!bufs) return fail(AMUN_EINVAL, "NULL bufs");
+  for (int p = 0; p < G; ++p)
+    if (!bufs[p] || (reinterpret_cast<uintptr_t>(bufs[p]) & 255) != 0)
+      return fail(AMUN_EINVAL, "bufs[%d] NULL or not 256-byte aligned", p);
+  return AMUN_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t amun_oneshot_buffer_bytes(const amun_ol* plan, int G) {
+  if (!plan || G < 1 || G > OS_MAX_G) return 0;
+  return OS_CTRL_BYTES + 2 * oneshot_recv_elems(plan, G) * sizeof(float);
+}
+
+amun_status amun_oneshot_alloc(const amun_ol* plan, int G, void** buf, void* ipc_handle) {
+  if (!plan || !buf) return fail(AMUN_EINVAL, "NULL plan or buf");
+  const size_t bytes = amun_oneshot_buffer_bytes(plan, G);
+  if (!bytes) return fail(AMUN_EINVAL, "G=%d out of [1, %d]", G, OS_MAX_G);
+  CUDA_TRY(cudaSetDevice(plan->device));
+  *buf = nullptr;
+  CUDA_TRY(cudaMalloc(buf, bytes));
+  cudaError_t e = cudaMemset(*buf, 0, bytes);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e == cudaSuccess && ipc_handle)
+    e = cudaIpcGetMemHandle(static_cast<cudaIpcMemHandle_t*>(ipc_handle), *buf);
+  if (e != cudaSuccess) {
+    cudaFree(*buf);
+    *buf = nullptr;
+    return fail(AMUN_ECUDA, "one-shot buffer: %s", cudaGetErrorString(e));
+  }
+  return AMUN_OK;
+}
+
+amun_status amun_oneshot_free(void* buf) {
+  if (buf) CUDA_TRY(cudaFree(buf));
+  return AMUN_OK;
+}
+
+amun_status amun_oneshot_open(const void* ipc_handle, int device, void** peer) {
+  if (!ipc_handle || !peer) return fail(AMUN_EINVAL, "NULL handle or peer");
+  CUDA_TRY(cudaSetDevice(device));
+  cudaIpcMemHandle_t h;
+  memcpy(&h, ipc_handle, sizeof(h));
+  CUDA_TRY(cudaIpcOpenMemHandle(peer, h, cudaIpcMemLazyEnablePeerAccess));
+  return AMUN_OK;
+}
+
+amun_status amun_oneshot_close(void* peer) {
+  if (peer) CUDA_TRY(cudaIpcCloseMemHandle(peer));
+  return AMUN_OK;
+}
+
+amun_status amun_output_layer_oneshot(amun_ol* plan, const void* X, const void* W, const float* b,
+                                      const float* prev_cost, const int32_t* beam_offsets, int N,
+                                      int S, const int32_t* k_per_sentence, int k,
+                                      void* const* bufs, int G, int rank, int64_t* out_idx,
+                                      float* out_cost, void* workspace, void* stream) {
+  if (!plan) return fail(AMUN_EINVAL, "NULL plan");
+  amun_status s = check_bufs(bufs, G);
+  if (s != AMUN_OK) return s;
+  if (rank < 0 || rank >= G) return fail(AMUN_EINVAL, "rank=%d out of [0, G=%d)", rank, G);
+  s = check_score_args(plan, X, W, b, N, workspace);
+  if (s != AMUN_OK) return s;
+  s = check_select_args(plan, prev_cost, beam_offsets, N, S, k, out_idx, out_cost);
+  if (s != AMUN_OK) return s;
+  CUDA_TRY(cudaSetDevice(plan->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (N > 0) {
+    s = run_scores(plan, X, W, b, N, workspace, nullptr, st, 0);
+    if (s != AMUN_OK) return s;
+  }
+  OneShotParams q;
+  memset(&q, 0, sizeof(q));
+  q.src[0] = oneshot_src(plan, workspace, N);
+  q.dst = oneshot_dst(plan, G, prev_cost, beam_offsets, N, S, k_per_sentence, k);
+  for (int p = 0; p < G; ++p) q.buf[p] = static_cast<char*>(bufs[p]);
+  q.out_idx[0] = reinterpret_cast<long long*>(out_idx);
+  q.out_cost[0] = out_cost;
+  q.G = G;
+  q.rank = rank;
+  q.emulate = 0;
+  q.recv_elems = (long long)oneshot_recv_elems(plan, G);
+  return oneshot_run(plan, q, 1, st);
+}
+
+amun_status amun_output_layer_oneshot_emulated(amun_ol* const* plans, int G, const void* X,
+                                               const void* const* W, const float* const* b,
+                                               const float* prev_cost, const int32_t* beam_offsets,
+                                               int N, int S, const int32_t* k_per_sentence, int k,
+                                               void* const* bufs, int64_t* const* out_idx,
+                                               float* const* out_cost, void* const* workspaces,
+                                               void* stream) {
+  amun_status s = check_bufs(bufs, G);
+  if (s != AMUN_OK) return s;
+  if (!plans || !W || !b || !out_idx || !out_cost || !workspaces)
+    return fail(AMUN_EINVAL, "NULL array argument");
+  for (int p = 0; p < G; ++p) {
+    if (!plans[p]) return fail(AMUN_EINVAL, "NULL plans[%d]", p);
+    if (plans[p]->k_max != plans[0]->k_max || plans[p]->max_rows != plans[0]->max_rows ||
+        plans[p]->V_total != plans[0]->V_total || plans[p]->device != plans[0]->device ||
+        plans[p]->max_sentences != plans[0]->max_sentences)
+      return fail(AMUN_EINVAL, "plans differ in k_max / max_rows / V_total / device");
+    s = check_score_args(plans[p], X, W[p], b[p], N, workspaces[p]);
+    if (s != AMUN_OK) return s;
+    s = check_select_args(plans[p], prev_cost, beam_offsets, N, S, k, out_idx[p], out_cost[p]);
+    if (s != AMUN_OK) return s;
+  }
+  CUDA_TRY(cudaSetDevice(plans[0]->device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  OneShotParams q;
+  memset(&q, 0, sizeof(q));
+  for (int p = 0; p < G; ++p) {
+    // the ranks' fused kernels do not wait on anything: sequential launches
+    if (N > 0) {
+      s = run_scores(plans[p], X, W[p], b[p], N, workspaces[p], nullptr, st, 0);
+      if (s != AMUN_OK) return s;
+    }
+    q.src[p] = oneshot_src(plans[p], workspaces[p], N);
+    q.buf[p] = static_cast<char*>(bufs[p]);
+    q.out_idx[p] = reinterpret_cast<long long*>(out_idx[p]);
+    q.out_cost[p] = out_cost[p];
+  }
+  q.dst = oneshot_dst(plans[0], G, prev_cost, beam_offsets, N, S, k_per_sentence, k);
+  q.G = G;
+  q.rank = 0;
+  q.emulate = 1;
+  q.recv_elems = (long long)oneshot_recv_elems(plans[0], G);
+  return oneshot_run(plans[0], q, G, st);
 }
 
 }  // extern "C"

@@ -399,12 +399,8 @@ __global__ void __launch_bounds__(32) argmax_rows_kernel(const MergeParams p,
 // rows' candidates are ranked by counting better ones (ranks are unique), and
 // the best k stay at the front for the next batch.
 template <int KB>
-__global__ void __launch_bounds__(MS_WARPS * 32) merge_sentences_kernel(const MergeParams p0) {
-  const MergeParams p = merge_dyn(p0);
-  __shared__ Cand pool[KB + MS_CAP];
-  __shared__ Cand best[KB];
-  __shared__ int s_valid;
-  const int s = blockIdx.x;
+__device__ __forceinline__ void merge_sentence(const MergeParams& p, int s, Cand* pool, Cand* best,
+                                               int& s_valid) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r0 = p.offsets[s], r1 = p.offsets[s + 1];
   const int ks = p.k_s ? min(p.k_s[s], p.k) : p.k;
@@ -452,6 +448,15 @@ __global__ void __launch_bounds__(MS_WARPS * 32) merge_sentences_kernel(const Me
     p.out_idx[(long long)s * p.k + i] = ok ? (long long)pool[i].r * p.V_total + pool[i].v : -1LL;
     p.out_cost[(long long)s * p.k + i] = ok ? pool[i].cost : kNegInf;
   }
+}
+
+template <int KB>
+__global__ void __launch_bounds__(MS_WARPS * 32) merge_sentences_kernel(const MergeParams p0) {
+  const MergeParams p = merge_dyn(p0);
+  __shared__ Cand pool[KB + MS_CAP];
+  __shared__ Cand best[KB];
+  __shared__ int s_valid;
+  merge_sentence<KB>(p, blockIdx.x, pool, best, s_valid);
 }
 
 }  // namespace amun

@@ -85,3 +85,65 @@ def test_shard_range_partition(V, world):
     covered = [x for a, b in r for x in range(a, b)]
     assert covered == list(range(V))
     assert all(a % 16 == 0 for a, b in r if b > a)
+
+
+class _FakeBuffers:
+    """Stands in for the library's one-shot buffer calls (no GPU here): the
+    'pointer' of rank r's buffer is 0x1000 * (r + 1), its 64-byte handle
+    encodes r, opening a handle yields 0x100000 + that pointer."""
+
+    def __init__(self, rank):
+        self.rank, self.log = rank, []
+
+    def alloc(self, plan, world):
+        self.log.append(("alloc", world))
+        return 0x1000 * (self.rank + 1), bytes([self.rank]) * 64
+
+    def open(self, handle, device):
+        assert len(handle) == 64 and len(set(handle)) == 1
+        self.log.append(("open", handle[0]))
+        return 0x100000 + 0x1000 * (handle[0] + 1)
+
+    def close(self, ptr):
+        self.log.append(("close", ptr))
+
+    def free(self, ptr):
+        self.log.append(("free", ptr))
+
+
+def _oneshot_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1805_09863_b200.sharded import OneShotExchange
+    fake = _FakeBuffers(rank)
+    ex = OneShotExchange(None, world, rank, 0, lib=fake)
+    ptrs = list(ex.ptrs)
+    ex.close()
+    q.put((rank, ptrs, fake.log))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_oneshot_handle_exchange(world):
+    """OneShotExchange (NEXT f3 host logic) over gloo: every rank ends with
+    the rank-ordered buffer list, its own allocation at its own index and
+    every peer's buffer opened from that peer's handle; close() unmaps the
+    peers and frees the own buffer."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_oneshot_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=120)
+    assert all(p.exitcode == 0 for p in procs), [p.exitcode for p in procs]
+    got = dict((r, (ptrs, log)) for r, ptrs, log in (q.get(timeout=10) for _ in range(world)))
+    for r in range(world):
+        ptrs, log = got[r]
+        assert ptrs == [0x1000 * (p + 1) if p == r else 0x100000 + 0x1000 * (p + 1)
+                        for p in range(world)]
+        assert log[0] == ("alloc", world)
+        assert sorted(e[1] for e in log if e[0] == "open") == [p for p in range(world) if p != r]
+        assert log[-1] == ("free", 0x1000 * (r + 1))
+        assert len([e for e in log if e[0] == "close"]) == world - 1
