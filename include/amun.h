@@ -261,6 +261,20 @@ amun_status amun_debug_logits(amun_ol* plan, const void* X, const void* W, const
 amun_status amun_bench_variant(amun_ol* plan, const void* X, const void* W, const float* b,
                                int N, int variant, void* workspace, void* stream);
 
+/* Sentence-level state after a row compaction (optional
+ * part: compact the per-sentence encoder-context columns too). Alg. 2
+ * removes finished hypotheses; a sentence none of whose rows
+ * survived is finished, and its sentence-level state (encoder context,
+ * source length, ...) can go as well. Writes
+ *   alive_s      [S] uint8 device: 1 iff new_beam_offsets[s+1] > new_beam_offsets[s];
+ *   unit_offsets [S+1] int32 device: 0, 1, ..., S;
+ * from new_beam_offsets [S+1] (device, the output of amun_compact /
+ * amun_beam_advance). Then amun_compact(sentence columns, alive_s, N = S,
+ * unit_offsets, S, ...) gathers them stably (its src_row = the old sentence
+ * of each kept sentence). One kernel, no sync; EINVAL on argument errors. */
+amun_status amun_sentence_alive(const int32_t* new_beam_offsets, int S, uint8_t* alive_s,
+                                int32_t* unit_offsets, void* stream);
+
 /* Mini-batching (Alg. 2 "Remove h from b"): stable compaction.
  * One column = one per-hypothesis state array of N rows of row_bytes bytes:
  *   src  [N, row_bytes] device, dst [>= N', row_bytes] device (must not

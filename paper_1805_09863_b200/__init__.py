@@ -20,7 +20,7 @@ from ._lib import AMUN_MAX_COLUMNS, AMUN_MAX_K, AmunError, check
 
 _L = _lib.load()
 
-__all__ = ["OutputLayer", "compact", "beam_advance", "quantize_e4m3", "split_tf32x3", "AmunError", "AMUN_MAX_K",
+__all__ = ["OutputLayer", "compact", "compact_sentences", "beam_advance", "quantize_e4m3", "split_tf32x3", "AmunError", "AMUN_MAX_K",
            "AMUN_MAX_COLUMNS", "lib_path"]
 
 lib_path = _lib.LIB_PATH
@@ -309,6 +309,22 @@ def compact(columns, alive, beam_offsets, new_offsets=None, src_row=None, counts
     if sync:
         return int(host[0]), int(host[1]), new_offsets, src_row, counts
     return None, None, new_offsets, src_row, counts
+
+
+def compact_sentences(columns, new_offsets, sync: bool = True):
+    """Sentence-level columns (one row per sentence: encoder context, source
+    lengths) after a row compaction: keep the sentences that still have rows
+    (new_offsets [S+1] from compact / beam_advance), stably
+    (amun_sentence_alive + amun_compact). Returns (S_kept, src_sentence,
+    counts); with sync=False S_kept is None (no host sync)."""
+    dev = new_offsets.device
+    S = new_offsets.shape[0] - 1
+    _need(new_offsets, "new_offsets", torch.int32, dev, (S + 1,))
+    alive_s = torch.empty(max(S, 1), dtype=torch.uint8, device=dev)
+    unit = torch.empty(S + 1, dtype=torch.int32, device=dev)
+    check(_L.amun_sentence_alive(_ptr(new_offsets), S, _ptr(alive_s), _ptr(unit), _stream(dev)))
+    n, _, _, src, counts = compact(columns, alive_s[:S], unit, sync=sync)
+    return n, src, counts
 
 
 def beam_advance(out_idx, out_cost, V_total: int, eos: int, N: int, columns=(), sync: bool = True,

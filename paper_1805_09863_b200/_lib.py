@@ -26,7 +26,7 @@ EXPORTS = [
     "amun_ol_scores_e4m3", "amun_quantize_e4m3", "amun_output_layer_partial_e4m3",
     "amun_argmax_e4m3", "amun_split_tf32x3", "amun_oneshot_buffer_bytes", "amun_oneshot_alloc",
     "amun_oneshot_free", "amun_oneshot_open", "amun_oneshot_close", "amun_output_layer_oneshot",
-    "amun_output_layer_oneshot_emulated",
+    "amun_output_layer_oneshot_emulated", "amun_sentence_alive",
 ]
 AMUN_ONESHOT_MAX_G = 8
 
@@ -82,6 +82,7 @@ def load() -> ctypes.CDLL:
         "amun_argmax_e4m3": (st, [vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, vp]),
         "amun_split_tf32x3": (st, [vp, i32, i32, i32, vp, vp]),
         "amun_oneshot_buffer_bytes": (sz, [vp, i32]),
+        "amun_sentence_alive": (st, [vp, i32, vp, vp, vp]),
         "amun_oneshot_alloc": (st, [vp, i32, ctypes.POINTER(vp), vp]),
         "amun_oneshot_free": (st, [vp]),
         "amun_oneshot_open": (st, [vp, i32, ctypes.POINTER(vp)]),

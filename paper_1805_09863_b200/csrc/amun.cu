@@ -828,6 +828,18 @@ long long a256(long long n) { return (n + 255) / 256 * 256; }
 
 extern "C" {
 
+amun_status amun_sentence_alive(const int32_t* new_beam_offsets, int S, uint8_t* alive_s,
+                                int32_t* unit_offsets, void* stream) {
+  if (S < 0) return fail(AMUN_EINVAL, "negative S");
+  if (!new_beam_offsets || !unit_offsets || (S > 0 && !alive_s))
+    return fail(AMUN_EINVAL, "NULL new_beam_offsets / alive_s / unit_offsets");
+  const int grid = (int)std::min<long long>(cdiv(S + 1, 256), 1024);
+  sentence_alive_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      new_beam_offsets, S, alive_s, unit_offsets);
+  CUDA_TRY(cudaGetLastError());
+  return AMUN_OK;
+}
+
 amun_status amun_compact(const amun_column* cols, int n_cols, const uint8_t* alive, int N,
                          const int32_t* beam_offsets, int S, int32_t* new_beam_offsets,
                          int32_t* src_row, int32_t* counts, int32_t* counts_host, void* stream) {

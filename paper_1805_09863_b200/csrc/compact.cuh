@@ -270,4 +270,19 @@ __global__ void __launch_bounds__(CP_THREADS, 6) compact_kernel(const CompactPar
   }
 }
 
+// Sentence-level state (encoder context, source lengths: one entry per
+// sentence, not per hypothesis) follows its sentence: a sentence stays while
+// at least one of its rows survived the row compaction (P:61-65 removes
+// hypotheses; a sentence without hypotheses is finished). alive_s[s] =
+// new_offsets[s+1] > new_offsets[s]; unit_offsets = 0..S (one "row" per
+// sentence) so amun_compact gathers the sentence columns.
+__global__ void sentence_alive_kernel(const int* __restrict__ new_offsets, int S,
+                                      unsigned char* __restrict__ alive_s,
+                                      int* __restrict__ unit_offsets) {
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s <= S; s += gridDim.x * blockDim.x) {
+    unit_offsets[s] = s;
+    if (s < S) alive_s[s] = new_offsets[s + 1] > new_offsets[s] ? 1 : 0;
+  }
+}
+
 }  // namespace amun

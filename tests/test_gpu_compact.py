@@ -91,3 +91,34 @@ def test_large_ragged(N, B):
     sizes = [B] * (N // B) + ([N % B] if N % B else [])
     alive = torch.from_numpy((rng.random(N) < 0.3).astype(np.uint8))
     run(N, sizes, alive, [16, 4])
+
+
+@pytest.mark.parametrize("S,B,p", [(1, 1, 0.0), (7, 3, 0.5), (300, 5, 0.3), (1280, 5, 0.9)])
+def test_sentence_columns_follow_their_rows(S, B, p):
+    """f1 (optional part): after the row compaction, the sentence-level
+    columns (here an encoder context [S, 64, 32] bf16-sized bytes and a source
+    length [S] int32) keep exactly the sentences with surviving rows, stably
+    (amun_sentence_alive + amun_compact), bit-exact with the oracle's
+    compaction under alive_s[s] = new_off[s+1] > new_off[s]."""
+    import paper_1805_09863_b200 as m
+    dev = torch.device("cuda", 0)
+    g = torch.Generator().manual_seed(S * 7 + B)
+    N = S * B
+    alive = (torch.rand(N, generator=g) >= p).to(torch.uint8)
+    off = torch.arange(0, N + 1, B, dtype=torch.int32)
+    ctx = torch.randint(0, 256, (S, 64 * 32 * 2), generator=g, dtype=torch.uint8)
+    slen = torch.randint(1, 100, (S,), generator=g, dtype=torch.int32)
+    x = torch.randint(0, 256, (N, 16), generator=g, dtype=torch.uint8)
+    xd = torch.empty_like(x, device=dev)
+    n_rows, s_alive, new_off, _, _ = m.compact([(x.to(dev), xd)], alive.to(dev), off.to(dev))
+    ctx_d, slen_d = torch.empty_like(ctx, device=dev), torch.empty_like(slen, device=dev)
+    S_kept, src_s, counts = m.compact_sentences([(ctx.to(dev), ctx_d), (slen.to(dev), slen_d)], new_off)
+    torch.cuda.synchronize()
+    _, o_new_off, _, _, o_S_alive = O.compact([x.numpy()], alive.numpy(), off.numpy())
+    alive_s = (o_new_off[1:] > o_new_off[:-1]).astype(np.uint8)
+    (o_ctx, o_slen), _, o_src, o_n, _ = O.compact([ctx.numpy(), slen.numpy().view(np.uint8).reshape(S, 4)],
+                                                  alive_s, np.arange(S + 1))
+    assert S_kept == o_n == o_S_alive == s_alive
+    assert np.array_equal(src_s[:S_kept].cpu().numpy(), o_src)
+    assert np.array_equal(ctx_d[:S_kept].cpu().numpy(), o_ctx)
+    assert np.array_equal(slen_d[:S_kept].cpu().numpy().view(np.uint8).reshape(-1, 4), o_slen)

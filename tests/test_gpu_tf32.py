@@ -184,3 +184,36 @@ def test_device_n_and_partial_merge():
     i1, c1 = ol.call_dev(Xs, Ws, b.to(DEV), pc, off, nd, w.k)
     torch.cuda.synchronize()
     assert torch.equal(i0, i1) and torch.equal(c0, c1)
+
+
+@pytest.mark.parametrize("G", [2, 3])
+def test_vocab_shards_partial_merge_and_oneshot(G):
+    """tf32x3 plans on vocab shards: per-shard partial records + merge (the
+    collective path) and the one-shot emulation give the same result, which
+    passes the oracle comparator at the fp32 tolerance."""
+    from paper_1805_09863_b200.sharded import EmulatedOneShot, shard_range
+    w = synth.Workload("t3s", H=128, V=7001, S=10, B=3, k=4, dtype="f32", seed=synth.BASE_SEED + 120 + G)
+    X, W, b = synth.gen_X(w), synth.gen_W(w), synth.gen_b(w)
+    pc, off = synth.gen_prev_cost(w).to(DEV), synth.gen_offsets(w).to(DEV)
+    m = amun()
+    Xs = m.split_tf32x3(X.to(DEV), "X")
+    layers, Ws, bs = [], [], []
+    for g in range(G):
+        v0, v1 = shard_range(w.V, G, g)
+        layers.append(m.OutputLayer(w.H, v1 - v0, v_offset=v0, V_total=w.V, dtype="tf32x3",
+                                    k_max=w.k, max_rows=w.N, max_sentences=w.S))
+        Ws.append(m.split_tf32x3(W[v0:v1].contiguous().to(DEV), "W"))
+        bs.append(b[v0:v1].contiguous().to(DEV))
+    parts = torch.stack([ol.partial(Xs, Wg, bg) for ol, Wg, bg in zip(layers, Ws, bs)])
+    idx, cost = layers[0].merge(parts, pc, off, w.k)
+    em = EmulatedOneShot(layers)
+    for i, c in em(Xs, Ws, bs, pc, off, w.k):
+        assert torch.equal(i, idx) and torch.equal(c, cost)
+    em.close()
+    torch.cuda.synchronize()
+    L = O.add_bias(O.gemm(O.as_f64(X), O.as_f64(W)), O.as_f64(b))
+    logp = O.log_softmax(L)
+    _, _, oc64, nxt = O.kbest_sentences(logp, O.as_f64(synth.gen_prev_cost(w)), off.cpu().numpy(), w.k)
+    pcd = O.as_f64(synth.gen_prev_cost(w))
+    compare_kbest(idx.cpu().numpy(), cost.cpu().numpy(), lambda s, r, v: pcd[r] + logp[r, v],
+                  oc64, np.full(w.S, w.k), "f32", w.V, o_next=nxt)
