@@ -94,13 +94,19 @@ class OneShotExchange:
             dist.barrier(group=group)
 
     def close(self):
-        if self.ptrs is None:
+        if getattr(self, "ptrs", None) is None:
             return
         for p, ptr in enumerate(self.ptrs):
             if p != self.rank:
                 self.lib.close(ptr)
         self.lib.free(self.own)
         self.ptrs = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:   # interpreter shutdown: the library may be gone
+            pass
 
 
 class ShardedOutputLayer:
@@ -195,6 +201,12 @@ class EmulatedOneShot:
 
     def close(self):
         import ctypes
-        for p in self.bufs:
+        for p in getattr(self, "bufs", []):
             self._check(self._L.amun_oneshot_free(ctypes.c_void_p(p)))
         self.bufs = []
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:   # interpreter shutdown: the library may be gone
+            pass
