@@ -99,8 +99,26 @@ amun_status amun_ol_create(amun_ol** plan, int H, int V_local, int v_offset, int
 amun_status amun_ol_destroy(amun_ol* plan);
 
 /* Bytes of device workspace the caller must pass to the calls below
- * (per-CTA partial states of the fused kernel). 256-byte aligned. */
+ * (per-CTA partial states of the fused kernel, then the cross-CTA hint
+ * words, the launch-generation counters and the fused tail's per-CTA
+ * arrival words). 256-byte aligned.
+ *
+ * The workspace is STATE of the plan, not scratch: it must be dedicated to
+ * one plan and keep its contents between that plan's calls (the generation
+ * counter and the arrival words tag every launch, CUDA-graph replays
+ * included, so nothing is reset per call). A buffer the plan has not used
+ * before must be initialised once: the library does so itself (a
+ * stream-ordered memset) the first time it sees a workspace ADDRESS; a
+ * caller that hands the plan memory at an address it already used, after
+ * the memory served something else, calls amun_ol_workspace_init first.
+ * A fused tail that finds the arrival words inconsistent (never a silent
+ * wrong result) traps after 10 s. */
 size_t amun_ol_workspace_bytes(const amun_ol* plan);
+
+/* Zero the hint / counter / arrival region of `workspace` on `stream` and
+ * register it as initialised for `plan` (see amun_ol_workspace_bytes).
+ * Errors: AMUN_EINVAL (NULL, misaligned), AMUN_ECUDA. */
+amun_status amun_ol_workspace_init(amun_ol* plan, void* workspace, void* stream);
 
 /* Floats per row of a partial record: 2 + 2*k_max, laid out as
  *   { m, s, l[0..k_max-1], v[0..k_max-1] }
@@ -127,7 +145,11 @@ int amun_ol_partial_stride(const amun_ol* plan);
  *                Each sentence's entries are sorted by cost, descending.
  *   workspace    amun_ol_workspace_bytes(plan) bytes, 256-byte aligned.
  * 0 <= N <= max_rows, 0 <= S <= max_sentences. X and W must be 16-byte
- * aligned (TMA). Enqueues 2 kernels (fused GEMM/epilogue, then select). */
+ * aligned (TMA). Enqueues ONE kernel for tcgen05 plans: the fused
+ * GEMM/epilogue whose tail (after a grid-wide arrival, cooperative launch)
+ * runs the merge/select (AMUN_TAIL=off in the environment at plan creation:
+ * 2 kernels, the fused kernel then the separate select kernel); fp32 SIMT
+ * plans and N = 0 enqueue the 2-kernel form. */
 amun_status amun_output_layer(amun_ol* plan, const void* X, const void* W, const float* b,
                               const float* prev_cost, const int32_t* beam_offsets, int N, int S,
                               const int32_t* k_per_sentence, int k, int64_t* out_idx,
@@ -260,6 +282,17 @@ amun_status amun_debug_logits(amun_ol* plan, const void* X, const void* W, const
  * Results are meaningless scratch in `workspace`; bf16 plans only. */
 amun_status amun_bench_variant(amun_ol* plan, const void* X, const void* W, const float* b,
                                int N, int variant, void* workspace, void* stream);
+
+/* Measurement hook: when `timeline` (device memory, >= #SMs x 16 u64,
+ * caller-owned) is non-NULL, every later fused launch of the single-CTA
+ * tcgen05 kernel through `plan` writes per-CTA %globaltimer stamps (ns):
+ * [cta][0] entry, [1] after setup (barriers, TMEM), [2] first TMA issue,
+ * [3] first stage landed at the MMA warp, [4] last MMA issued, [5] last
+ * accumulator ready at the epilogue, [6] epilogue done, [7] final barrier,
+ * [8] tail released (all CTAs arrived), [9] tail merge done, [10..15]
+ * accumulator-ready time of tiles 0..5. NULL switches it off. Not
+ * synchronised; for tools/timeline.py. */
+amun_status amun_debug_timeline(amun_ol* plan, unsigned long long* timeline);
 
 /* Sentence-level state after a row compaction (optional
  * part: compact the per-sentence encoder-context columns too). Alg. 2

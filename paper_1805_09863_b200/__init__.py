@@ -77,6 +77,8 @@ class OutputLayer:
         self.stride = _L.amun_ol_partial_stride(h)
         nbytes = _L.amun_ol_workspace_bytes(h)
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        # the workspace is plan state (amun.h): initialised once, kept between calls
+        check(_L.amun_ol_workspace_init(h, _ptr(self.workspace), _stream(dev)))
 
     def __del__(self):
         h = getattr(self, "_h", None)

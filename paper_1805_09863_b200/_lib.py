@@ -26,7 +26,8 @@ EXPORTS = [
     "amun_ol_scores_e4m3", "amun_quantize_e4m3", "amun_output_layer_partial_e4m3",
     "amun_argmax_e4m3", "amun_split_tf32x3", "amun_oneshot_buffer_bytes", "amun_oneshot_alloc",
     "amun_oneshot_free", "amun_oneshot_open", "amun_oneshot_close", "amun_output_layer_oneshot",
-    "amun_output_layer_oneshot_emulated", "amun_sentence_alive",
+    "amun_output_layer_oneshot_emulated", "amun_sentence_alive", "amun_ol_workspace_init",
+    "amun_debug_timeline",
 ]
 AMUN_ONESHOT_MAX_G = 8
 
@@ -63,6 +64,8 @@ def load() -> ctypes.CDLL:
         "amun_ol_destroy": (st, [vp]),
         "amun_ol_workspace_bytes": (sz, [vp]),
         "amun_ol_partial_stride": (i32, [vp]),
+        "amun_ol_workspace_init": (st, [vp, vp, vp]),
+        "amun_debug_timeline": (st, [vp, vp]),
         "amun_output_layer": (st, [vp, vp, vp, vp, vp, vp, i32, i32, vp, i32, vp, vp, vp, vp]),
         "amun_output_layer_dev": (st, [vp, vp, vp, vp, vp, vp, vp, i32, vp, i32, vp, vp, vp, vp]),
         "amun_ol_scores": (st, [vp, vp, vp, vp, i32, vp, vp]),

@@ -18,8 +18,8 @@
 #include "compact.cuh"
 #include "merge.cuh"
 #include "ol_simt.cuh"
-#include "ol_tc.cuh"
-#include "ol_tc2.cuh"
+#include "launch_tc.cuh"
+#include "tail.cuh"
 #include "oneshot.cuh"
 #include "quant.cuh"
 
@@ -38,6 +38,20 @@ amun_status fail(amun_status s, const char* fmt, ...) {
   g_err = buf;
   return s;
 }
+
+}  // namespace
+
+amun_status amun::launch_fail(const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return AMUN_ECUDA;
+}
+
+namespace {
 
 #define CUDA_TRY(expr)                                                                  \
   do {                                                                                  \
@@ -101,7 +115,12 @@ struct amun_ol {
   size_t slots_bytes;          // partial-record slots at the start of the workspace
   size_t hint_bytes;               // per-row hint words after the slots, then 2 x u32
                                    // {generation, CTAs done} (device-side counters)
-  const void* hint_ws = nullptr;   // workspace whose hint region is initialised
+  size_t flags_bytes;              // (reserved after the counters; 0)
+  const void* hint_ws = nullptr;   // workspace whose hint / counter / flag region is initialised
+  int tail_mode = 0;    // env AMUN_TAIL: 0 fused tail (one launch per call), 1 "off" (separate merge kernel)
+  long long pf_bytes = 0;   // env AMUN_PF_BYTES: entry L2 prefetch of W per CTA (0 = off;
+                            // measured slower at greedy and beam)
+  unsigned long long* tl = nullptr;   // amun_debug_timeline buffer (device), else NULL
   int ng_override = 0;  // env AMUN_NG: 2 or 4 epilogue warpgroups (experiments)
   int pairs_mode = 0;   // env AMUN_PAIRS: 0 auto, 1 never ("off"), 2 always ("force"; tests)
   MapEntry xmaps[4];
@@ -182,93 +201,6 @@ Schedule make_schedule(const amun_ol* pl, int N, int* grid) {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-// Launch one fused-kernel instantiation; the warpgroup register hand-off
-// needs the full launch pool (see TcCfg), checked here.
-template <int NG>
-amun_status launch_kernel(void (*kern)(const CUtensorMap, const CUtensorMap, const TcParams),
-                          const CUtensorMap* mx, const CUtensorMap* mw, const TcParams& tp,
-                          int grid, cudaStream_t st, int smem_bytes) {
-  cudaFuncAttributes fa;
-  CUDA_TRY(cudaFuncGetAttributes(&fa, kern));
-  if (fa.numRegs < TcCfg<NG>::kLaunchRegs)
-    return fail(AMUN_ECUDA, "fused kernel compiled with %d registers/thread, needs %d for its "
-                "setmaxnreg budget", fa.numRegs, TcCfg<NG>::kLaunchRegs);
-  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
-  kern<<<grid, TcCfg<NG>::kThreads, smem_bytes, st>>>(*mx, *mw, tp);
-  CUDA_TRY(cudaGetLastError());
-  return AMUN_OK;
-}
-
-template <int KB, int NG>
-amun_status launch_tc_ng(const CUtensorMap* mx, const CUtensorMap* mw, const TcParams& tp,
-                         int grid, cudaStream_t st, int mode, bool pairs) {
-  void (*kern)(const CUtensorMap, const CUtensorMap, const TcParams);
-  if (pairs)
-    kern = mode == 0 ? ol_tc2_kernel<KB, 0, NG>
-         : mode == 2 ? ol_tc2_kernel<KB, 2, NG>
-         : mode == 3 ? ol_tc2_kernel<KB, 3, NG>
-         : mode == 4 ? ol_tc2_kernel<1, 4, NG>
-                     : ol_tc2_kernel<1, 1, NG>;
-  else
-    kern = mode == 0 ? ol_tc_kernel<KB, 0, NG>
-         : mode == 2 ? ol_tc_kernel<KB, 2, NG>
-         : mode == 3 ? ol_tc_kernel<KB, 3, NG>
-         : mode == 4 ? ol_tc_kernel<1, 4, NG>
-                     : ol_tc_kernel<1, 1, NG>;
-  return launch_kernel<NG>(kern, mx, mw, tp, grid, st, pairs ? TC2_SMEM : TC_SMEM);
-}
-
-// e4m3 plans: single CTAs; the full path and the two benchmark builds.
-template <int KB, int NG>
-amun_status launch_tc_f8(const CUtensorMap* mx, const CUtensorMap* mw, const TcParams& tp,
-                         int grid, cudaStream_t st, int mode) {
-  void (*kern)(const CUtensorMap, const CUtensorMap, const TcParams) =
-      mode == 0 ? ol_tc_kernel<KB, 0, NG, 1>
-    : mode == 2 ? ol_tc_kernel<KB, 2, NG, 1>
-    : mode == 4 ? ol_tc_kernel<1, 4, NG, 1>
-                : ol_tc_kernel<KB, 3, NG, 1>;
-  return launch_kernel<NG>(kern, mx, mw, tp, grid, st, TC_SMEM_F8);
-}
-
-// tf32x3 plans: single CTAs; every mode (the fused path, the test/bench
-// builds and the argmax kernel).
-template <int KB, int NG>
-amun_status launch_tc_t3(const CUtensorMap* mx, const CUtensorMap* mw, const TcParams& tp,
-                         int grid, cudaStream_t st, int mode) {
-  void (*kern)(const CUtensorMap, const CUtensorMap, const TcParams) =
-      mode == 0 ? ol_tc_kernel<KB, 0, NG, 2>
-    : mode == 1 ? ol_tc_kernel<1, 1, NG, 2>
-    : mode == 2 ? ol_tc_kernel<KB, 2, NG, 2>
-    : mode == 3 ? ol_tc_kernel<KB, 3, NG, 2>
-                : ol_tc_kernel<1, 4, NG, 2>;
-  return launch_kernel<NG>(kern, mx, mw, tp, grid, st, TC_SMEM);
-}
-
-// Two epilogue warpgroups. bf16: measured faster than three or four (their
-// extra warps cost issue slots and registers while the tensor pipe bounds;
-// DESIGN.md §6.1). e4m3: four measured within run-to-run noise of two
-// (cfg beam fused 80-85 vs 80-83 us). Building with -DAMUN_WITH_NG3 /
-// -DAMUN_WITH_NG4 adds the other counts (env AMUN_NG).
-template <int KB>
-amun_status launch_tc(amun_ol* pl, const CUtensorMap* mx, const CUtensorMap* mw,
-                      const TcParams& tp, int grid, cudaStream_t st, int mode, bool pairs) {
-  if (pl->dtype == AMUN_TF32X3) return launch_tc_t3<KB, 2>(mx, mw, tp, grid, st, mode);
-  if (pl->dtype == AMUN_E4M3) {
-#ifdef AMUN_WITH_NG4
-    if (pl->ng_override == 4) return launch_tc_f8<KB, 4>(mx, mw, tp, grid, st, mode);
-#endif
-    return launch_tc_f8<KB, 2>(mx, mw, tp, grid, st, mode);
-  }
-#ifdef AMUN_WITH_NG4
-  if (pl->ng_override == 4) return launch_tc_ng<KB, 4>(mx, mw, tp, grid, st, mode, pairs);
-#endif
-#ifdef AMUN_WITH_NG3
-  if (pl->ng_override == 3) return launch_tc_ng<KB, 3>(mx, mw, tp, grid, st, mode, pairs);
-#endif
-  (void)pl;
-  return launch_tc_ng<KB, 2>(mx, mw, tp, grid, st, mode, pairs);
-}
-
 template <int KB>
 amun_status launch_simt(const SimtParams& sp, int grid, cudaStream_t st, int mode) {
   if (mode == 0)
@@ -289,10 +221,14 @@ bool dev_pairs(const amun_ol* pl) {
   return pl->pairs_mode == 2 || cdiv(pl->max_rows, 128) >= 9;
 }
 
+// tail != TAIL_NONE (modes 0 / 4, tcgen05 plans): the merge runs in the same
+// launch (tail.cuh) with the parameters in *tmp; its part / layout / schedule
+// / N are filled in here.
 amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b, int N,
                        void* workspace, float* logits, cudaStream_t st, int mode,
                        const int* N_dev = nullptr, const float* x_scale = nullptr,
-                       const float* w_scale = nullptr) {
+                       const float* w_scale = nullptr, int tail = TAIL_NONE,
+                       const MergeParams* tmp = nullptr) {
   if (N == 0) return AMUN_OK;
   CUDA_TRY(cudaSetDevice(pl->device));
   int grid;
@@ -316,6 +252,7 @@ amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b
     s = get_map(pl, pl->wmaps, 8, pl->wnext, W, pl->V_local, pairs ? TC_BN / 2 : TC_BN, &mw);
     if (s != AMUN_OK) return s;
     TcParams tp;
+    memset(&tp, 0, sizeof(tp));
     tp.N = N;
     tp.V_local = pl->V_local;
     tp.v_offset = pl->v_offset;
@@ -340,13 +277,36 @@ amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b
     tp.use_hint = sch.C >= 4 * TC_BN ? 1 : 0;
     tp.N_dev = N_dev;
     tp.num_sms = pl->num_sms;
+    tp.arrive = reinterpret_cast<unsigned int*>(static_cast<char*>(workspace) + pl->slots_bytes +
+                                                pl->hint_bytes + 8);   // after {generation, count}
+    if ((mode == 0 || mode == 4) && tail != TAIL_NONE) {
+      tp.tail = tail | (pl->tail_mode == 2 ? TAIL_X_NOWORK : 0) | (pl->tail_mode == 3 ? TAIL_X_NOCOOP : 0) |
+                (pl->tail_mode == 4 ? TAIL_X_FENCE : 0) | (pl->tail_mode == 5 ? TAIL_X_SLEEP : 0) |
+                (pl->tail_mode == 6 ? TAIL_X_NOWORK | TAIL_X_NOCOOP : 0) |
+                (pl->tail_mode == 7 ? TAIL_X_NOWORK | TAIL_X_FENCE : 0);
+      tp.mp = *tmp;
+      tp.mp.part = static_cast<const float*>(workspace);
+      tp.mp.layout = pairs ? 2 : 0;
+      tp.mp.sch = sch;
+      tp.mp.N = N;
+      tp.mp.N_dev = nullptr;   // the kernel passes its own resolved N / schedule (TcDyn)
+      tp.mp.num_sms = pl->num_sms;
+    }
+    tp.tl = pl->tl;
+    if (pl->pf_bytes > 0 && !N_dev) {
+      tp.pf_w = static_cast<const char*>(W);
+      tp.pf_row_bytes = pl->dtype == AMUN_E4M3 ? pl->H : pl->dtype == AMUN_TF32X3 ? 12LL * pl->H
+                                                                                  : 2LL * pl->H;
+      tp.pf_max_bytes = pl->pf_bytes;
+    }
     if ((mode == 0 || mode == 4) && pl->hint_ws != workspace) {
       // hint words carry the launch generation (advanced on the device by the
-      // kernel itself); zero words + counters once per workspace
-      CUDA_TRY(cudaMemsetAsync(tp.hint, 0, pl->hint_bytes + 256, st));
+      // kernel itself); zero words + counters + tail flags once per workspace
+      // (amun_ol_workspace_init does the same on request)
+      CUDA_TRY(cudaMemsetAsync(tp.hint, 0, pl->hint_bytes + 256 + pl->flags_bytes, st));
       pl->hint_ws = workspace;
     }
-#define TC_CALL(K) launch_tc<K>(pl, mx, mw, tp, grid, st, mode, pairs)
+#define TC_CALL(K) launch_tc<K>((int)pl->dtype, pl->ng_override, mx, mw, tp, grid, st, mode, pairs)
     AMUN_KB_SWITCH(mode == 1 || mode == 4 ? 1 : pl->kb, TC_CALL)
 #undef TC_CALL
   } else {
@@ -426,6 +386,28 @@ MergeParams base_merge(const amun_ol* pl) {
   return mp;
 }
 
+// The sentence-phase parameters of one call (merge kernel or fused tail).
+MergeParams sent_merge(const amun_ol* pl, const float* prev_cost, const int32_t* beam_offsets,
+                       int N, int S, const int32_t* k_s, int k, int64_t* out_idx, float* out_cost) {
+  MergeParams mp = base_merge(pl);
+  mp.N = N;
+  mp.S = S;
+  mp.prev_cost = prev_cost;
+  mp.offsets = beam_offsets;
+  mp.k_s = k_s;
+  mp.k = k;
+  mp.out_idx = reinterpret_cast<long long*>(out_idx);
+  mp.out_cost = out_cost;
+  return mp;
+}
+
+// The merge runs in the fused kernel's tail (one launch per call) for the
+// tcgen05 plans, unless AMUN_TAIL=off; N = 0 still needs the merge kernel
+// (no fused launch happens, the outputs are padded by the merge).
+bool use_tail(const amun_ol* pl, int N) {
+  return pl->tail_mode != 1 && pl->dtype != AMUN_F32 && N > 0;
+}
+
 }  // namespace
 
 namespace {
@@ -438,6 +420,13 @@ amun_status partial_impl(amun_ol* plan, const void* X, const void* W, const floa
   if (s != AMUN_OK) return s;
   if (N == 0) return AMUN_OK;
   if (!partial) return fail(AMUN_EINVAL, "NULL partial");
+  if (use_tail(plan, N)) {
+    MergeParams mp = base_merge(plan);
+    mp.N = N;
+    mp.out_part = partial;
+    return run_scores(plan, X, W, b, N, workspace, nullptr, static_cast<cudaStream_t>(stream), 0,
+                      nullptr, x_scale, w_scale, TAIL_ROWS, &mp);
+  }
   s = run_scores(plan, X, W, b, N, workspace, nullptr, static_cast<cudaStream_t>(stream), 0,
                  nullptr, x_scale, w_scale);
   if (s != AMUN_OK) return s;
@@ -516,11 +505,20 @@ amun_status amun_ol_create(amun_ol** plan, int H, int V_local, int v_offset, int
   {
     const char* e = getenv("AMUN_PAIRS");
     pl->pairs_mode = !e ? 0 : (strcmp(e, "off") == 0 ? 1 : (strcmp(e, "force") == 0 ? 2 : 0));
+    // experiments: off | wait (no merge work) | nocoop | fence | sleep
+    const char* t = getenv("AMUN_TAIL");
+    pl->tail_mode = !t ? 0 : strcmp(t, "off") == 0 ? 1 : strcmp(t, "wait") == 0 ? 2
+                  : strcmp(t, "nocoop") == 0 ? 3 : strcmp(t, "fence") == 0 ? 4
+                  : strcmp(t, "sleep") == 0 ? 5 : strcmp(t, "waitnocoop") == 0 ? 6
+                  : strcmp(t, "arriveonly") == 0 ? 7 : 0;
+    const char* f = getenv("AMUN_PF_BYTES");
+    if (f) pl->pf_bytes = atoll(f);
   }
   const long long slots = pl->num_sms + cdiv(max_rows > 0 ? max_rows : 1, 128) + 1;
   pl->slots_bytes = (size_t)cdiv(slots * 128LL * pl->stride * 4, 256) * 256;
   pl->hint_bytes = (size_t)cdiv((long long)(max_rows > 0 ? max_rows : 1) * 8, 256) * 256;
-  pl->ws_bytes = pl->slots_bytes + pl->hint_bytes + 256;
+  pl->flags_bytes = 0;   // the 256-byte counter block holds {generation, count, arrive[2]}
+  pl->ws_bytes = pl->slots_bytes + pl->hint_bytes + 256 + pl->flags_bytes;
   *plan = pl;
   return AMUN_OK;
 }
@@ -531,6 +529,18 @@ amun_status amun_ol_destroy(amun_ol* plan) {
 }
 
 size_t amun_ol_workspace_bytes(const amun_ol* plan) { return plan ? plan->ws_bytes : 0; }
+
+amun_status amun_ol_workspace_init(amun_ol* plan, void* workspace, void* stream) {
+  if (!plan || !workspace) return fail(AMUN_EINVAL, "NULL plan or workspace");
+  if ((reinterpret_cast<uintptr_t>(workspace) & 255) != 0)
+    return fail(AMUN_EINVAL, "workspace must be 256-byte aligned");
+  CUDA_TRY(cudaSetDevice(plan->device));
+  CUDA_TRY(cudaMemsetAsync(static_cast<char*>(workspace) + plan->slots_bytes, 0,
+                           plan->hint_bytes + 256 + plan->flags_bytes,
+                           static_cast<cudaStream_t>(stream)));
+  plan->hint_ws = workspace;
+  return AMUN_OK;
+}
 
 int amun_ol_partial_stride(const amun_ol* plan) { return plan ? plan->stride : 0; }
 
@@ -577,6 +587,12 @@ amun_status amun_output_layer(amun_ol* plan, const void* X, const void* W, const
   if (s != AMUN_OK) return s;
   s = check_select_args(plan, prev_cost, beam_offsets, N, S, k, out_idx, out_cost);
   if (s != AMUN_OK) return s;
+  if (plan->dtype != AMUN_E4M3 && use_tail(plan, N)) {
+    const MergeParams mp = sent_merge(plan, prev_cost, beam_offsets, N, S, k_per_sentence, k,
+                                      out_idx, out_cost);
+    return run_scores(plan, X, W, b, N, workspace, nullptr, static_cast<cudaStream_t>(stream), 0,
+                      nullptr, nullptr, nullptr, TAIL_SENT, &mp);
+  }
   s = amun_ol_scores(plan, X, W, b, N, workspace, stream);
   if (s != AMUN_OK) return s;
   return amun_ol_select(plan, workspace, prev_cost, beam_offsets, N, S, k_per_sentence, k,
@@ -598,6 +614,12 @@ amun_status amun_output_layer_dev(amun_ol* plan, const void* X, const void* W, c
   s = check_select_args(plan, prev_cost, beam_offsets, Nmax, S, k, out_idx, out_cost);
   if (s != AMUN_OK) return s;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (use_tail(plan, Nmax)) {
+    const MergeParams mp = sent_merge(plan, prev_cost, beam_offsets, Nmax, S, k_per_sentence, k,
+                                      out_idx, out_cost);
+    return run_scores(plan, X, W, b, Nmax, workspace, nullptr, st, 0, N_dev, nullptr, nullptr,
+                      TAIL_SENT, &mp);
+  }
   s = run_scores(plan, X, W, b, Nmax, workspace, nullptr, st, 0, N_dev);
   if (s != AMUN_OK) return s;
   if (S == 0) return AMUN_OK;
@@ -685,6 +707,14 @@ amun_status argmax_impl(amun_ol* plan, const void* X, const void* W, const float
   if (N > 0 && (!out_token || !out_logit)) return fail(AMUN_EINVAL, "NULL out_token / out_logit");
   if (N == 0) return AMUN_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (use_tail(plan, N)) {
+    MergeParams mp = base_merge(plan);
+    mp.N = N;
+    mp.out_idx = reinterpret_cast<long long*>(out_token);
+    mp.out_cost = out_logit;
+    return run_scores(plan, X, W, b, N, workspace, nullptr, st, 4, nullptr, x_scale, w_scale,
+                      TAIL_ARGMAX, &mp);
+  }
   s = run_scores(plan, X, W, b, N, workspace, nullptr, st, 4, nullptr, x_scale, w_scale);
   if (s != AMUN_OK) return s;
   MergeParams mp = base_merge(plan);
@@ -740,6 +770,17 @@ amun_status amun_output_layer_e4m3(amun_ol* plan, const uint8_t* X8, const float
   if (!plan) return fail(AMUN_EINVAL, "NULL plan");
   amun_status s = check_select_args(plan, prev_cost, beam_offsets, N, S, k, out_idx, out_cost);
   if (s != AMUN_OK) return s;
+  if (use_tail(plan, N)) {
+    s = check_score_args(plan, X8, W8, b, N, workspace);
+    if (s != AMUN_OK) return s;
+    if (plan->dtype != AMUN_E4M3) return fail(AMUN_EINVAL, "plan dtype is not AMUN_E4M3");
+    if (!x_scale || !w_scale) return fail(AMUN_EINVAL, "NULL x_scale / w_scale");
+    if (!aligned16(w_scale)) return fail(AMUN_EINVAL, "w_scale must be 16-byte aligned");
+    const MergeParams mp = sent_merge(plan, prev_cost, beam_offsets, N, S, k_per_sentence, k,
+                                      out_idx, out_cost);
+    return run_scores(plan, X8, W8, b, N, workspace, nullptr, static_cast<cudaStream_t>(stream), 0,
+                      nullptr, x_scale, w_scale, TAIL_SENT, &mp);
+  }
   s = amun_ol_scores_e4m3(plan, X8, x_scale, W8, w_scale, b, N, 0, workspace, stream);
   if (s != AMUN_OK) return s;
   return amun_ol_select(plan, workspace, prev_cost, beam_offsets, N, S, k_per_sentence, k,
@@ -761,6 +802,12 @@ amun_status amun_quantize_e4m3(const void* src, amun_dtype src_dtype, int R, int
   else
     quantize_e4m3_kernel<false><<<grid, QZ_THREADS, 0, st>>>(src, R, H, dst, scale);
   CUDA_TRY(cudaGetLastError());
+  return AMUN_OK;
+}
+
+amun_status amun_debug_timeline(amun_ol* plan, unsigned long long* timeline) {
+  if (!plan) return fail(AMUN_EINVAL, "NULL plan");
+  plan->tl = timeline;
   return AMUN_OK;
 }
 

@@ -332,11 +332,10 @@ __device__ __forceinline__ void row_topk(const MergeParams& p, int r, int lane, 
 constexpr int MS_WARPS = 8;
 constexpr int MS_CAP = 256;   // candidates ranked per batch of rows
 
+// Row r (one full warp): the merged record {M, Z, top-k_max} over the row's
+// partial records, written to out_part (ROW mode; the vocab-shard output).
 template <int KB>
-__global__ void __launch_bounds__(MS_WARPS * 32) merge_rows_kernel(const MergeParams p) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r = blockIdx.x * MS_WARPS + warp;
-  if (r >= p.N) return;
+__device__ __forceinline__ void merged_row_record(const MergeParams& p, int r, int lane) {
   float lse, M, Z, l;
   int v;
   row_topk<KB>(p, r, lane, lse, M, Z, l, v);
@@ -351,14 +350,19 @@ __global__ void __launch_bounds__(MS_WARPS * 32) merge_rows_kernel(const MergePa
   }
 }
 
-// Alg. 5 reduce (P:244-251 with k = 1, no normalisation): one warp per row,
-// the best (l desc, v asc) entry 0 over the row's vocab-split records.
-__global__ void __launch_bounds__(32) argmax_rows_kernel(const MergeParams p,
-                                                                    long long* __restrict__ tok,
-                                                                    float* __restrict__ logit) {
+template <int KB>
+__global__ void __launch_bounds__(MS_WARPS * 32) merge_rows_kernel(const MergeParams p) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r = blockIdx.x * (blockDim.x >> 5) + warp;
+  const int r = blockIdx.x * MS_WARPS + warp;
   if (r >= p.N) return;
+  merged_row_record<KB>(p, r, lane);
+}
+
+// Alg. 5 reduce (P:244-251 with k = 1, no normalisation), row r, one full
+// warp: the best (l desc, v asc) entry 0 over the row's vocab-split records,
+// written to tok[r] / logit[r].
+__device__ __forceinline__ void argmax_row(const MergeParams& p, int r, int lane,
+                                           long long* __restrict__ tok, float* __restrict__ logit) {
   const float* base;
   long long js;
   int n;
@@ -393,14 +397,37 @@ __global__ void __launch_bounds__(32) argmax_rows_kernel(const MergeParams p,
   }
 }
 
+#ifndef AMUN_TC_DEFINE   // (non-template kernel: defined once, in amun.cu's unit)
+__global__ void __launch_bounds__(32) argmax_rows_kernel(const MergeParams p,
+                                                         long long* __restrict__ tok,
+                                                         float* __restrict__ logit) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (r >= p.N) return;
+  argmax_row(p, r, lane, tok, logit);
+}
+#endif
+
 // Sentence phase. CTA = one sentence. Warps take rows; each row's top-k_max
 // (already scored cost = prev_cost + l - lse: only the winners are
 // normalised) goes to shared memory; the carried best-k plus a batch of
 // rows' candidates are ranked by counting better ones (ranks are unique), and
 // the best k stay at the front for the next batch.
-template <int KB>
+// `sync` is the barrier of the MS_WARPS warps doing the merge (threads
+// 0 .. MS_WARPS*32-1 of the CTA): __syncthreads in the merge kernels, a named
+// barrier in the fused kernel's tail (tail.cuh), where other warps exist.
+struct CtaSync {
+  __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+struct MergeWarpsSync {   // named barrier 10 over the MS_WARPS merge warps
+  __device__ __forceinline__ void operator()() const {
+    asm volatile("bar.sync 10, %0;" ::"n"(MS_WARPS * 32) : "memory");
+  }
+};
+
+template <int KB, class Sync = CtaSync>
 __device__ __forceinline__ void merge_sentence(const MergeParams& p, int s, Cand* pool, Cand* best,
-                                               int& s_valid) {
+                                               int& s_valid, Sync sync = Sync()) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r0 = p.offsets[s], r1 = p.offsets[s + 1];
   const int ks = p.k_s ? min(p.k_s[s], p.k) : p.k;
@@ -424,7 +451,7 @@ __device__ __forceinline__ void merge_sentence(const MergeParams& p, int s, Cand
       }
     }
     if (threadIdx.x == 0) s_valid = 0;
-    __syncthreads();
+    sync();
     const int n = keep + (re - rb) * p.k_max;
     int valid = 0;
     for (int e = threadIdx.x; e < n; e += MS_WARPS * 32) {
@@ -436,10 +463,10 @@ __device__ __forceinline__ void merge_sentence(const MergeParams& p, int s, Cand
       if (rank < p.k) best[rank] = c;
     }
     if (valid) atomicAdd(&s_valid, valid);
-    __syncthreads();
+    sync();
     keep = min(s_valid, p.k);
     if (threadIdx.x < keep) pool[threadIdx.x] = best[threadIdx.x];
-    __syncthreads();
+    sync();
     if (nrows == 0) break;
   }
   if (threadIdx.x < p.k) {

@@ -19,7 +19,7 @@
 // 2 = bare GEMM (the epilogue only drains TMEM), 3 = GEMM + bias + online
 // softmax statistics without the k-best.
 #pragma once
-#include "tc_epi.cuh"
+#include "tail.cuh"
 
 namespace amun {
 
@@ -76,6 +76,10 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
   constexpr int kCtrl = 4 * NG;                    // first control warp
   const int role = warp - kCtrl;                   // 0 = TMA, 1 = MMA, 2-3 idle, < 0 epilogue
 
+  if (threadIdx.x == 0) tl_mark(p.tl, TL_ENTRY);
+  if (role == 0 && lane == 0 && !p.N_dev)   // W to L2 before the prologue (tail.cuh)
+    entry_prefetch_w(p, (long long)blockIdx.x * p.sch.C,
+                     min((long long)(blockIdx.x + 1) * p.sch.C, p.sch.total), p.sch);
   for (int i = threadIdx.x; i < 4 * 128; i += blockDim.x) sts_u64(smem_u32(thr_x + i), 0ull);   // no stale tags
   if (role == 0 && lane == 0) {
     prefetch_tmap(&tmX);
@@ -91,6 +95,8 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
     for (int i = 0; i < TC_NBIAS; ++i) mbar_init(&bfull[i], 1);
     fence_barrier_init();
     *gen_smem = (MODE == 0 || MODE == 4) ? read_generation(p.gen_ctr) : 0u;
+    // the next launch's tail counter (tail.cuh "Counters")
+    if ((MODE == 0 || MODE == 4) && blockIdx.x == 0) p.arrive[(*gen_smem + 1u) & 1u] = 0u;
   }
   if (role == 1) {
     tmem_alloc(tmem_holder, 512);
@@ -101,6 +107,7 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
   const uint32_t gen = *gen_smem;   // this launch's hint tag
+  if (threadIdx.x == 0) tl_mark(p.tl, TL_SETUP);
 
   const TcDyn dyn = tc_dyn<false>(p);      // N (and the schedule) from the device in _dev mode
   const long long start = (long long)blockIdx.x * dyn.sch.C;
@@ -122,6 +129,7 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
         for (int kb = 0; kb < p.n_kblk; ++kb) {
           mbar_wait_spin(&empty[stage], phase ^ 1);
           if (lane == 0) {
+            if (tile == 0 && kb == 0) tl_mark(p.tl, TL_TMA0);
             mbar_arrive_expect_tx(&full[stage], p.a_box_bytes + TC_B_BYTES);
             // 128 bytes of K per block: 64 bf16, 128 e4m3 or 32 fp32 (tf32x3)
             constexpr int kBlockElems = ELT == 1 ? 2 * TC_BK : ELT == 2 ? TC_BK / 2 : TC_BK;
@@ -159,6 +167,7 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
           mbar_wait_spin(&full[stage], phase);
           tc_fence_after();
           if (lane == 0) {
+            if (kb == 0 && acc == 0 && acc_phase == 0) tl_mark(p.tl, TL_FULL0);
             const uint64_t ad = sdesc_k_sw128(smem_u32(sA + stage * TC_A_BYTES));
             const uint64_t bd = sdesc_k_sw128(smem_u32(sB + stage * TC_B_BYTES));
 #pragma unroll
@@ -183,6 +192,7 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
+      if (lane == 0) tl_mark(p.tl, TL_MMA_END);
     }
   } else {
     reg_alloc<Cfg::kEpiRegs>();
@@ -191,13 +201,20 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
                                      sscale);
   }
 
+  if (threadIdx.x == 0) tl_mark(p.tl, TL_EPI_END);
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) tl_mark(p.tl, TL_BARRIER);
   if (role == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, 512);
   }
-  if ((MODE == 0 || MODE == 4) && threadIdx.x == 0) finish_generation(p.gen_ctr);
+  if constexpr (MODE == 0 || MODE == 4) {
+    if (p.tail)   // the merge in this launch (tail.cuh); the exchange area is free now
+      grid_tail<KB>(p, dyn, reinterpret_cast<uint8_t*>(xch), gen);
+    else if (threadIdx.x == 0)
+      finish_generation(p.gen_ctr);
+  }
 }
 
 }  // namespace amun

@@ -15,7 +15,7 @@
 //   * each CTA's TMEM holds its own 128 rows x N columns, so the epilogue is
 //     the single-CTA one.
 #pragma once
-#include "tc_epi.cuh"
+#include "tail.cuh"
 
 namespace amun {
 
@@ -62,6 +62,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<NG>::kThreads,
   const uint32_t rank = cluster_ctarank();          // 0 = leader, 1 = peer
   const int pair = blockIdx.x >> 1;
 
+  if (role == 0 && lane == 0 && rank == 0 && !p.N_dev)   // W to L2 before the prologue (tail.cuh)
+    entry_prefetch_w(p, (long long)pair * p.sch.C,
+                     min((long long)(pair + 1) * p.sch.C, p.sch.total), p.sch);
   for (int i = threadIdx.x; i < 4 * 128; i += blockDim.x) sts_u64(smem_u32(thr_x + i), 0ull);   // no stale tags
   if (role == 0 && lane == 0) {
     prefetch_tmap(&tmX);
@@ -77,6 +80,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<NG>::kThreads,
     for (int i = 0; i < TC_NBIAS; ++i) mbar_init(&bfull[i], 1);
     fence_barrier_init();
     *gen_smem = (MODE == 0 || MODE == 4) ? read_generation(p.gen_ctr) : 0u;
+    // the next launch's tail counter (tail.cuh "Counters")
+    if ((MODE == 0 || MODE == 4) && blockIdx.x == 0) p.arrive[(*gen_smem + 1u) & 1u] = 0u;
   }
   if (role == 1) {
     tmem_alloc_2sm(tmem_holder, 512);
@@ -171,7 +176,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<NG>::kThreads,
     tc_fence_after();
     tmem_dealloc_2sm(tmem_base, 512);
   }
-  if ((MODE == 0 || MODE == 4) && threadIdx.x == 0) finish_generation(p.gen_ctr);
+  if constexpr (MODE == 0 || MODE == 4) {
+    if (p.tail)   // the merge in this launch (tail.cuh); the exchange area is free now
+      grid_tail<KB>(p, dyn, reinterpret_cast<uint8_t*>(xch), gen);
+    else if (threadIdx.x == 0)
+      finish_generation(p.gen_ctr);
+  }
 }
 
 }  // namespace amun

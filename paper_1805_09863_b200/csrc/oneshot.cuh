@@ -33,7 +33,7 @@
 // wait on one another"): gridDim.y = G, me = blockIdx.y, all buffers local,
 // one cooperative launch.
 #pragma once
-#include "merge.cuh"
+#include "tail.cuh"   // (atomics / acquire-release helpers)
 
 namespace amun {
 
@@ -52,11 +52,6 @@ struct OneShotParams {
 
 __device__ __forceinline__ void red_release_sys_add(unsigned int* p, unsigned int v) {
   asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ unsigned int atom_add_acq_rel_gpu(unsigned int* p, unsigned int v) {
-  unsigned int old;
-  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-  return old;
 }
 __device__ __forceinline__ unsigned int ld_acquire_sys(const unsigned int* p) {
   unsigned int v;

@@ -11,7 +11,7 @@
 // of a CTA's range in an M-tile the NG groups' states are combined in NG-1
 // rounds through one exchange area and group 0 writes the partial record.
 #pragma once
-#include "epilogue.cuh"
+#include "merge.cuh"
 
 namespace amun {
 
@@ -31,7 +31,31 @@ struct TcParams {
   const float* __restrict__ w_scale;       // e4m3 plans: [V_local] per-row scales of W
   int a_box_bytes;                         // bytes of one X box (rows x 128; single-CTA kernel)
   int num_sms;                             // the device schedule's CTA count
+  // Fused tail (tail.cuh): after every CTA of the grid has emitted its
+  // partial records, the epilogue warps of all CTAs run the merge, so the
+  // whole path is ONE launch. TAIL_NONE leaves the records in the workspace
+  // (amun_ol_scores; a separate merge kernel follows).
+  int tail;                                // TAIL_NONE / TAIL_SENT / TAIL_ROWS / TAIL_ARGMAX
+  MergeParams mp;                          // the merge's parameters (outputs, offsets, ...)
+  unsigned int* __restrict__ arrive;       // [2] tail arrival counters, by tag parity (tail.cuh)
+  const char* __restrict__ pf_w;           // W base for the entry L2 prefetch (else NULL)
+  long long pf_row_bytes;                  // bytes of one W row (K elements)
+  long long pf_max_bytes;                  // prefetch at most this many bytes of a CTA's W range
+  unsigned long long* __restrict__ tl;     // timeline probe [grid][TL_N] (amun_debug_timeline), else NULL
 };
+// Timeline probe points (globaltimer ns; per CTA; see amun_debug_timeline).
+enum { TL_ENTRY = 0, TL_SETUP = 1, TL_TMA0 = 2, TL_FULL0 = 3, TL_MMA_END = 4, TL_EPI_LAST = 5,
+       TL_EPI_END = 6, TL_BARRIER = 7, TL_RELEASED = 8, TL_TAIL_END = 9, TL_TILE0 = 10, TL_N = 16 };
+__device__ __forceinline__ void tl_mark(const unsigned long long* tl_base, int point) {
+  if (tl_base) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const_cast<unsigned long long*>(tl_base)[(long long)blockIdx.x * TL_N + point] = t;
+  }
+}
+enum { TAIL_NONE = 0, TAIL_SENT = 1, TAIL_ROWS = 2, TAIL_ARGMAX = 3,
+       TAIL_X_NOWORK = 16, TAIL_X_NOCOOP = 32,      // experiment flags (env AMUN_TAIL)
+       TAIL_X_FENCE = 64, TAIL_X_SLEEP = 128 };
 
 // Per-launch values that amun_output_layer_dev only knows on the device:
 // the row count, the schedule derived from it and the hint switch.
@@ -97,12 +121,11 @@ __device__ __forceinline__ uint32_t read_generation(const unsigned int* gen_ctr)
 // one finishes, and the next launch sees the new value (and the reset count)
 // across the kernel boundary; a fence here only delayed each CTA's exit
 // behind its partial-record stores (ncu: ~6% of greedy's stall samples).
+// atomicInc wraps the count to 0 at the last CTA itself, so a count left at
+// any value (e.g. by a caller reusing memory) heals after one launch.
 __device__ __forceinline__ void finish_generation(unsigned int* gen_ctr) {
-  const unsigned int prev = atomicAdd(gen_ctr + 1, 1u);
-  if (prev == gridDim.x - 1) {   // every CTA has read the generation and finished
-    gen_ctr[1] = 0u;
-    atomicAdd(gen_ctr, 1u);
-  }
+  const unsigned int prev = atomicInc(gen_ctr + 1, gridDim.x - 1);
+  if (prev == gridDim.x - 1) atomicAdd(gen_ctr, 1u);   // every CTA has read the generation
 }
 
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
@@ -184,6 +207,10 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
     mbar_wait(&bfull[tile % TC_NBIAS], (uint32_t)(tile / TC_NBIAS) & 1u);
     mbar_wait(&tfull[acc], acc_phase);
     tc_fence_after();
+    if (warp == 0 && lane == 0 && p.tl) {
+      if (tile < TL_N - TL_TILE0) tl_mark(p.tl, TL_TILE0 + tile);
+      tl_mark(p.tl, TL_EPI_LAST);
+    }
     const uint32_t tbase = tmem_base + t_lane + acc * TC_BN;
     // biased (and, e4m3, scaled) logits of 32-column chunk c from its TMEM words
     auto build_x = [&](const uint32_t (&r)[32], int c, float (&x)[32]) {

@@ -1,0 +1,101 @@
+"""A/B device times of the whole output-layer path (amun_output_layer) under
+plan-creation switches (env read by amun_ol_create): the fused tail
+(AMUN_TAIL=off: separate merge kernel) and the entry L2 prefetch of W
+(AMUN_PF_BYTES). CUDA graph of K calls, W rotated over enough copies that
+L2 never serves W across calls (as bench.py). Interleaved repetitions.
+
+  python tools/ab_path.py [workload ...]     (JSON lines)
+"""
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import synth  # noqa: E402
+import paper_1805_09863_b200 as amun  # noqa: E402
+
+VARIANTS = {
+    "tail+pf": {"AMUN_TAIL": "on", "AMUN_PF_BYTES": str(1 << 20)},
+    "tail": {"AMUN_TAIL": "on", "AMUN_PF_BYTES": "0"},
+    "sep+pf": {"AMUN_TAIL": "off", "AMUN_PF_BYTES": str(1 << 20)},
+    "sep": {"AMUN_TAIL": "off", "AMUN_PF_BYTES": "0"},
+    "tailwait": {"AMUN_TAIL": "wait", "AMUN_PF_BYTES": "0"},     # tail without merge work
+    "tailnocoop": {"AMUN_TAIL": "nocoop", "AMUN_PF_BYTES": "0"},
+}
+VARIANTS["tailfence"] = {"AMUN_TAIL": "fence", "AMUN_PF_BYTES": "0"}
+VARIANTS["tailsleep"] = {"AMUN_TAIL": "sleep", "AMUN_PF_BYTES": "0"}
+VARIANTS["waitnocoop"] = {"AMUN_TAIL": "waitnocoop", "AMUN_PF_BYTES": "0"}
+VARIANTS["arriveonly"] = {"AMUN_TAIL": "arriveonly", "AMUN_PF_BYTES": "0"}
+VARIANTS["scores"] = {"AMUN_TAIL": "off", "AMUN_PF_BYTES": "0"}   # the fused kernel alone
+NOCHECK = {"tailwait", "scores", "waitnocoop", "arriveonly"}
+
+
+def graph_us(fn, K, reps=5):
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        fn(0)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            for i in range(K):
+                fn(i)
+        g.replay()
+        torch.cuda.synchronize()
+        out = []
+        for _ in range(reps):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            g.replay()
+            e.record()
+            torch.cuda.synchronize()
+            out.append(s.elapsed_time(e) * 1e3 / K)
+    return out
+
+
+def main():
+    names = sys.argv[1:] or ["greedy", "beam"]
+    variants = os.environ.get("AB_VARIANTS", ",".join(VARIANTS)).split(",")
+    dev = torch.device("cuda", 0)
+    for name in names:
+        w = synth.CONFIGS[name]
+        X, W, b = synth.gen_X(w).to(dev), synth.gen_W(w).to(dev), synth.gen_b(w).to(dev)
+        pc, off = synth.gen_prev_cost(w).to(dev), synth.gen_offsets(w).to(dev)
+        wbytes = W.numel() * W.element_size()
+        ncopy = max(2, -(-2 * 126 * 2 ** 20 // wbytes))
+        Ws = [W] + [W.clone() for _ in range(ncopy - 1)]
+        K = int(os.environ.get("AB_K", "100" if w.N < 2000 else "10"))
+        layers = {}
+        for v in variants:
+            os.environ.update(VARIANTS[v])
+            layers[v] = amun.OutputLayer(w.H, w.V, dtype=w.dtype, k_max=w.k, max_rows=w.N,
+                                         max_sentences=w.S)
+        ref = None
+        res = {v: [] for v in variants}
+        for rnd in range(3):
+            for v in variants:
+                ol = layers[v]
+                oi = torch.empty((w.S, w.k), dtype=torch.int64, device=dev)
+                oc = torch.empty((w.S, w.k), dtype=torch.float32, device=dev)
+
+                def fn(i, ol=ol, oi=oi, oc=oc, v=v):
+                    if v == "scores":
+                        ol.scores(X, Ws[i % ncopy], b)
+                    else:
+                        ol(X, Ws[i % ncopy], b, pc, off, w.k, out_idx=oi, out_cost=oc)
+                res[v] += graph_us(fn, K)
+                if v in NOCHECK:
+                    pass
+                elif ref is None:
+                    ref = (oi.clone(), oc.clone())
+                else:
+                    assert torch.equal(ref[0], oi) and torch.equal(ref[1], oc), v
+        for v in variants:
+            xs = sorted(res[v])
+            print(json.dumps({"workload": name, "variant": v, "us_min": xs[0],
+                              "us_med": xs[len(xs) // 2], "K": K, "w_copies": ncopy}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
