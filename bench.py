@@ -1,23 +1,33 @@
 """Benchmark of the NMT output-layer hot path (arXiv 1805.09863) on B200.
 
 Metric (BASELINE.json): hypothesis-rows/s through GEMM + softmax + k-best at
-V = 90k; % of roofline. One step = one pass of the whole path over one batch:
-fused GEMM/bias/softmax-stats/row-k-best kernel + merge/select kernel
-(amun_output_layer) on the 'beam' config (H=1024, V=90000, 128 x 5, k=5).
+V = 90k; % of roofline. One step = one pass of the whole path over one batch
+(amun_output_layer: the fused GEMM/bias/softmax-stats/row-k-best kernel whose
+tail runs the merge/select) on the 'beam' config (H=1024, V=90000, 128 x 5,
+k=5).
 
-N=1: one GPU, the whole vocabulary. N>1 (torchrun, one rank per GPU, NCCL):
-vocab-sharded — rank g owns V/N rows of W; each step = partial kernel +
-all_gather_into_tensor of the per-row partial records + merge on every rank
-(strong scaling: the batch is fixed).
+N=1: one GPU, the whole vocabulary. N>1: one process per GPU (NCCL),
+vocab-sharded as north_star states: rank g owns V/N rows of W and b; each step
+= the partial kernel (per-row {m, s, top-k} record of the shard) + ONE
+all_gather_into_tensor of the records + the exact merge on every rank (strong
+scaling: the batch is fixed). `python bench.py --gpus N` without a launcher
+re-executes itself under torch.distributed.run with N ranks, and fails (exit
+2) when fewer than N GPUs are visible — it never silently runs fewer.
+
+Beside the headline the line carries, at every N, the vocab-sharded scaling
+config of BASELINE.json (cfg5 'shard': H=1024, V=256k, 1024 x 12, k=12) and,
+at N=1, the greedy config (cfg2, HBM-bound), the fp32 (3xTF32) and FP8 paths
+of the same beam workload — each with its own oracle parity sample.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 """
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
-import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -34,6 +44,7 @@ import synth  # noqa: E402
 
 METRIC = "hypothesis-rows/sec through GEMM+softmax+k-best at V=90k"
 UNIT = "rows/s"
+L2_BYTES = 126 * 2 ** 20
 
 
 def load_peaks():
@@ -114,22 +125,43 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-# ---------------------------------------------------------------------- oracle arm
+# ---------------------------------------------------------------------- oracle
 def oracle_sample(w: synth.Workload, X, W, b, pc, n_sent: int):
-    """The oracle, as it stands, on the first n_sent sentences (all V)."""
+    """The oracle, as it stands, on the first n_sent sentences (all V).
+    W may be a callable yielding (v0, W block) pieces of the full W (the
+    logits' columns are independent, so they are computed block by block
+    to bound host memory for the V = 256k config)."""
     import oracle as O
     rows = n_sent * w.B
     Xs = O.as_f64(X[:rows])
-    Wd = O.as_f64(W)
-    bd = O.as_f64(b)
     pcs = O.as_f64(pc[:rows])
     off = np.arange(n_sent + 1) * w.B
     t0 = time.perf_counter()
-    L = O.add_bias(O.gemm(Xs, Wd), bd)
+    if callable(W):
+        L = np.empty((rows, w.V), np.float64)
+        for v0, Wb in W():
+            L[:, v0:v0 + Wb.shape[0]] = O.gemm(Xs, O.as_f64(Wb))
+        L = O.add_bias(L, O.as_f64(b))
+    else:
+        L = O.add_bias(O.gemm(Xs, O.as_f64(W)), O.as_f64(b))
     logp = O.log_softmax(L)
     res = O.kbest_sentences(logp, pcs, off, w.k)
     dt = time.perf_counter() - t0
     return dt, rows, res, logp, pcs
+
+
+def parity_sample(w, idx, cost, X_h, W_h, b_h, pc_h, n_sent):
+    """Our first n_sent sentences' (idx, cost) against the oracle on the
+    same seeded inputs (tests/compare.py comparator, north_star tolerance)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from tests.compare import compare_kbest
+    dt, rows, res, logp, pcs = oracle_sample(w, X_h, W_h, b_h, pc_h, n_sent)
+    gi, gc = idx.cpu().numpy()[:n_sent], cost.cpu().numpy()[:n_sent]
+    oi, oc32, oc64, nxt = res
+    rep = compare_kbest(gi, gc, lambda s, r, v: pcs[r] + logp[r, v], oc64,
+                        np.full(n_sent, w.k), "f32" if w.dtype == "f32" else "bf16", w.V,
+                        o_next=nxt)
+    return {"sentences": n_sent, "rows": rows, **rep, "status": "pass"}, dt
 
 
 def blas_threads():
@@ -142,12 +174,20 @@ def blas_threads():
         return os.cpu_count() or 1
 
 
+def config_of(w, world, extra=None):
+    d = {"workload": f"{w.name}: H={w.H}, V={w.V}, {w.S} sentences x beam {w.B}, k={w.k}",
+         "H": w.H, "V": w.V, "sentences": w.S, "beam": w.B, "k": w.k, "rows": w.N,
+         "global_batch": w.N, "parallelism": f"vocab{world}" if world > 1 else "none",
+         "seed": w.seed, "dist": w.dist}
+    d.update(extra or {})
+    return d
+
+
 def run_reference(args, w):
-    """--impl reference: the oracle timed on host cores, bounded sample/step."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return
-    torch.manual_seed(0)
+    """--impl reference: the oracle timed on host cores, bounded sample/step.
+    Rank 0 only (the other ranks of a torchrun launch exit without work)."""
+    if int(os.environ.get("RANK", "0")) != 0:
+        return 0
     X, W, b, pc = synth.gen_X(w), synth.gen_W(w), synth.gen_b(w), synth.gen_prev_cost(w)
     n_sent = int(os.environ.get("AMUN_REF_SENTENCES", "4"))
     for _ in range(args.warmup):
@@ -165,196 +205,265 @@ def run_reference(args, w):
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": config_of(w, args),
+        "data": "synthetic", "config": config_of(w, args.gpus),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                          "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
+    return 0
 
 
-def config_of(w, args):
-    return {"workload": f"{w.name}: H={w.H}, V={w.V}, {w.S} sentences x beam {w.B}, k={w.k}",
-            "H": w.H, "V": w.V, "sentences": w.S, "beam": w.B, "k": w.k, "rows": w.N,
-            "global_batch": w.N, "parallelism": f"vocab{args.gpus}" if args.gpus > 1 else "none",
-            "l2": "W rotated over 2 resident copies (2 x 184 MB > 126 MB L2) between steps",
-            "seed": w.seed, "dist": w.dist}
+# ---------------------------------------------------------------------- launcher
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def spawn_ranks(args) -> int:
+    """--gpus N > 1 without a launcher: re-execute under torch.distributed.run
+    with N ranks on this node; fewer than N visible GPUs is an error."""
+    n = torch.cuda.device_count()
+    if n < args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but only {n} CUDA device(s) visible; "
+                         f"refusing to run on fewer GPUs\n")
+        return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    sys.stderr.write("bench.py: launching " + " ".join(cmd) + "\n")
+    return subprocess.call(cmd)
+
+
+class Ctx:
+    def __init__(self, world, rank, local):
+        self.world, self.rank, self.local = world, rank, local
+        self.dev = torch.device("cuda", local)
+
+    def max(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        t = torch.tensor([x], device=self.dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    def gather(self, xs):
+        """[world][len(xs)] of every rank's floats (rank order)."""
+        t = torch.tensor(xs, device=self.dev, dtype=torch.float64)
+        if self.world == 1:
+            return [xs]
+        out = torch.empty((self.world, len(xs)), device=self.dev, dtype=torch.float64)
+        torch.distributed.all_gather_into_tensor(out, t)
+        return out.cpu().tolist()
+
+    def barrier(self):
+        if self.world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
 
 
 # ---------------------------------------------------------------------- our arm
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="beam", choices=list(synth.CONFIGS))
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-e4m3", action="store_true", help="skip the FP8 context measurement")
-    ap.add_argument("--eager", action="store_true", help="launch steps eagerly (no CUDA graph)")
-    args = ap.parse_args()
-    args.warmup = max(args.warmup, 3)
-    w = synth.CONFIGS[args.workload]
+def w_copies(nbytes: int) -> int:
+    """Resident copies of W so that consecutive steps never find W in L2."""
+    return max(2, -(-2 * L2_BYTES // max(nbytes, 1)))
 
-    if args.impl == "reference":
-        return run_reference(args, w)
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
-    import paper_1805_09863_b200 as amun
-    from paper_1805_09863_b200 import sharded
+class Problem:
+    """One workload on this rank: inputs generated on the host by the seeded
+    generator (bit-identical to what the oracle reads), made resident in HBM;
+    W (this rank's vocab shard) rotated over enough copies to defeat L2."""
 
-    # inputs: generated on the host by the seeded generator (bit-identical to
-    # what the oracle reads), then made resident in HBM
-    X_h, pc_h, off_h = synth.gen_X(w), synth.gen_prev_cost(w), synth.gen_offsets(w)
-    v0, v1 = sharded.shard_range(w.V, world, rank)
-    W_h, b_h = synth.gen_W(w, v0, v1 - v0), synth.gen_b(w, v0, v1 - v0)
-    X, pc, off = X_h.to(dev), pc_h.to(dev), off_h.to(dev)
-    Ws = [W_h.to(dev)]
-    Ws.append(Ws[0].clone())            # 2 copies: W never served from L2 across steps
-    b = b_h.to(dev)
-    layer = sharded.ShardedOutputLayer(w.H, w.V, world, rank, dtype=w.dtype, k_max=w.k,
-                                       max_rows=w.N, max_sentences=w.S, device=dev)
+    def __init__(self, w, ctx, exchange="nccl", max_copies=None):
+        from paper_1805_09863_b200 import sharded
+        self.w, self.ctx = w, ctx
+        dev = ctx.dev
+        self.X_h, self.pc_h, self.off_h = synth.gen_X(w), synth.gen_prev_cost(w), synth.gen_offsets(w)
+        self.v0, self.v1 = sharded.shard_range(w.V, ctx.world, ctx.rank)
+        self.W_h = synth.gen_W(w, self.v0, self.v1 - self.v0)
+        self.b_h = synth.gen_b(w, self.v0, self.v1 - self.v0)
+        self.X, self.pc, self.off = self.X_h.to(dev), self.pc_h.to(dev), self.off_h.to(dev)
+        W0 = self.W_h.to(dev)
+        n = w_copies(W0.numel() * W0.element_size())
+        if max_copies:
+            n = min(n, max_copies)
+        self.Ws = [W0] + [W0.clone() for _ in range(n - 1)]
+        self.b = self.b_h.to(dev)
+        self.layer = sharded.ShardedOutputLayer(w.H, w.V, ctx.world, ctx.rank, dtype=w.dtype,
+                                                k_max=w.k, max_rows=w.N, max_sentences=w.S,
+                                                device=dev, exchange=exchange)
+        self.idx = torch.empty((w.S, w.k), dtype=torch.int64, device=dev)
+        self.cost = torch.empty((w.S, w.k), dtype=torch.float32, device=dev)
 
-    def step(i, with_events=None):
-        Wc = Ws[i % 2]
-        return layer(X, Wc, b, pc, off, w.k, events=with_events)
+    def step(self, i, stage_events=None):
+        return self.layer(self.X, self.Ws[i % len(self.Ws)], self.b, self.pc, self.off, self.w.k,
+                          out_idx=self.idx, out_cost=self.cost, stage_events=stage_events)
 
-    for i in range(args.warmup):
-        step(i)
+    def full_W(self):
+        """The whole W on the host (rank 0's parity at N > 1), block by block."""
+        if self.ctx.world == 1:
+            return self.W_h
+        w = self.w
+
+        def blocks(step=32768):
+            for v0 in range(0, w.V, step):
+                yield v0, synth.gen_W(w, v0, min(step, w.V - v0))
+        return blocks
+
+    def full_b(self):
+        return self.b_h if self.ctx.world == 1 else synth.gen_b(self.w)
+
+
+def capture(fn, K, stream):
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(stream):
+        with torch.cuda.graph(g, stream=stream):
+            for i in range(K):
+                fn(i)
+    return g
+
+
+def replay_ms(g, stream):
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        s.record()
+        g.replay()
+        e.record()
     torch.cuda.synchronize()
+    return s.elapsed_time(e)
 
-    # ---------------- device-timed region
-    # world == 1: the K steps are captured once into a CUDA graph (each step's
-    # own event pair around the fused kernel, W copy alternating) and replayed
-    # once, so host launch overhead does not starve short steps. world > 1:
-    # eager steps (the NCCL all-gather sits between the kernels).
-    K = args.steps
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(K)]
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    use_graph = world == 1 and not args.eager
-    if use_graph:
-        gstream = torch.cuda.Stream(dev)
-        with torch.cuda.stream(gstream):
-            step(0)
+
+def measure(p: Problem, ctx: Ctx, K: int, warmup: int, eager=False, clk=None):
+    """Whole-path device time per step (max over ranks) and the fused
+    kernel's mean duration (amun_ol_scores alone, a graph of K launches on
+    the same W rotation). Steps are captured into one CUDA graph (the NCCL
+    all-gather included at N > 1) unless eager or capture fails."""
+    for i in range(warmup):
+        p.step(i)
+    torch.cuda.synchronize()
+    st = torch.cuda.Stream(ctx.dev)
+    timing, graph = "eager launches", None
+    if not eager:
+        try:
+            with torch.cuda.stream(st):
+                p.step(0)
             torch.cuda.synchronize()
-            graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph, stream=gstream):
-                for i in range(K):
-                    idx, cost = step(i)
-            # the fused kernel alone, K launches, for its average duration
-            kgraph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(kgraph, stream=gstream):
-                for i in range(K):
-                    layer.ol.scores(X, Ws[i % 2], b)
-        graph.replay()                     # untimed warm-up replays
-        kgraph.replay()
-        torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
+            graph = capture(p.step, K, st)
+            timing = "CUDA graph of the K steps, replayed once"
+            if ctx.world > 1:
+                timing += " (NCCL all-gather captured)"
+            replay_ms(graph, st)               # untimed warm-up replay
+        except Exception as e:   # noqa: BLE001 (capture unsupported: time eager steps)
+            graph = None
+            timing = f"eager launches (graph capture failed: {type(e).__name__})"
+            torch.cuda.synchronize()
+    ctx.barrier()
+    if clk:
         clk.wait_first()
         clk.mark("t_start")
-        if use_graph:
-            with torch.cuda.stream(gstream):
-                start.record()
-                graph.replay()
-                end.record()
-        else:
-            start.record()
-            for i in range(K):
-                idx, cost = step(i, with_events=ev[i])
-            end.record()
-        torch.cuda.synchronize()
-        clk.mark("t_end")
-    if world > 1:
-        torch.distributed.barrier()
-    ms = start.elapsed_time(end)
-    if use_graph:
-        ks, ke = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(gstream):
-            ks.record()
-            kgraph.replay()
-            ke.record()
-        torch.cuda.synchronize()
-        kern_ms = [ks.elapsed_time(ke) / K]
+    if graph is not None:
+        ms = replay_ms(graph, st)
     else:
-        kern_ms = [a.elapsed_time(c) for a, c in ev]
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
-    ms_per_step = ms / K
-    value = w.N / (ms_per_step * 1e-3)
-
-    # ---------------- the FP8 path (NEXT f4) on the same workload (context,
-    # not the headline: the bench dtype is bf16). W quantised once per copy,
-    # X quantised inside every timed step; one CUDA graph of K steps.
-    e4m3 = None
-    if use_graph and w.dtype == "bf16" and w.H % 16 == 0 and not args.no_e4m3:
-        W8s = [amun.quantize_e4m3(Wc) for Wc in Ws]
-        X8 = torch.empty((w.N, w.H), dtype=torch.uint8, device=dev)
-        xs = torch.empty(w.N, dtype=torch.float32, device=dev)
-        o8 = amun.OutputLayer(w.H, v1 - v0, v_offset=v0, V_total=w.V, dtype="e4m3", k_max=w.k,
-                              max_rows=w.N, max_sentences=w.S, device=dev)
-        oi8 = torch.empty((w.S, w.k), dtype=torch.int64, device=dev)
-        oc8 = torch.empty((w.S, w.k), dtype=torch.float32, device=dev)
-
-        def f8_step(i):
-            amun.quantize_e4m3(X, out=X8, scale=xs)
-            o8.call_e4m3(X8, xs, W8s[i % 2][0], W8s[i % 2][1], b, pc, off, w.k, out_idx=oi8,
-                         out_cost=oc8)
-        with torch.cuda.stream(gstream):
-            f8_step(0)
-            torch.cuda.synchronize()
-            g8 = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g8, stream=gstream):
-                for i in range(K):
-                    f8_step(i)
-            g8.replay()
-            torch.cuda.synchronize()
-            s8, e8 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s8.record()
-            g8.replay()
-            e8.record()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for i in range(K):
+            p.step(i)
+        e.record()
         torch.cuda.synchronize()
-        ms8 = s8.elapsed_time(e8) / K
-        e4m3 = {"value": w.N / (ms8 * 1e-3), "unit": UNIT, "ms_per_step": ms8,
-                "note": "same workload with X and W as OCP E4M3 + per-row fp32 scales on "
-                        "tcgen05 kind::f8f6f4 (amun_output_layer_e4m3); X quantised inside "
-                        "every step; parity vs the oracle on the dequantised values in "
-                        "tests/test_gpu_e4m3.py"}
-        del W8s
+        ms = s.elapsed_time(e)
+    if clk:
+        clk.mark("t_end")
+    ctx.barrier()
+    ms = ctx.max(ms)
+    # the fused kernel alone (the roofline's kernel)
+    ol = p.layer.ol
+    kg = capture(lambda i: ol.scores(p.X, p.Ws[i % len(p.Ws)], p.b), K, st)
+    replay_ms(kg, st)
+    kern_ms = replay_ms(kg, st) / K
+    out = {"ms": ms, "ms_per_step": ms / K, "kernel_ms": kern_ms, "timing": timing,
+           "launches_per_step": p.layer.launches_per_step, "w_copies": len(p.Ws)}
+    if ctx.world > 1:
+        # per-rank stage times (eager, events on the launching stream):
+        # partial kernel | all-gather | merge
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
+        for i in range(K):
+            p.step(i, stage_events=evs[i])
+        torch.cuda.synchronize()
+        st_ms = [statistics.mean(e[j].elapsed_time(e[j + 1]) for e in evs) for j in range(3)]
+        per_rank = ctx.gather(st_ms + [kern_ms])
+        out["stages_ms_per_rank"] = [
+            {"rank": r, "partial_kernel": v[0], "all_gather": v[1], "merge": v[2],
+             "fused_kernel_alone": v[3]} for r, v in enumerate(per_rank)]
+    del kg, graph
+    return out
 
-    # ---------------- end-to-end through the public API with host buffers
-    # Every step: X, prev_cost, beam_offsets pinned host -> HBM, the call,
-    # idx/cost HBM -> pinned host. Serving-style pipeline: H2D on a copy
-    # stream into double-buffered device inputs, overlapping the previous
-    # step's compute; the D2H of each step's result stays on the compute stream.
-    # One contiguous pinned staging buffer per direction, so each step is ONE
-    # H2D copy (X | prev_cost | beam_offsets, 16-byte aligned parts) and ONE
-    # D2H copy (idx | cost); the call writes straight into the output views.
+
+def roofline(w, V_local, kern_ms, peaks, label, traffic=None, plan_dtype=None):
+    """Algorithmic work of ONE fused-kernel launch over its time: FLOP =
+    2*N*H*V_local; bytes = W + X + b once (the logits never reach HBM)."""
+    dt = plan_dtype or w.dtype
+    esz = {"bf16": 2, "f32": 4, "e4m3": 1, "tf32x3": 12}[dt]
+    flops = 2.0 * w.N * w.H * V_local
+    alg_bytes = V_local * w.H * esz + w.N * w.H * esz + V_local * 4
+    tc_peak = peaks["bf16_tflops"] * {"bf16": 1.0, "e4m3": 2.0, "tf32x3": 1.0 / 6.0}.get(dt, 1.0)
+    t_tc = flops / (tc_peak * 1e12)
+    t_hbm = alg_bytes / (peaks["hbm_gbs"] * 1e9)
+    common = {"traffic": traffic, "kernel": label, "kernel_ms_mean": kern_ms,
+              "algorithmic": f"{flops:.4g} FLOP and {alg_bytes:.4g} B per launch "
+                             f"(2*N*H*V_local; W + X + b once)"}
+    if t_tc >= t_hbm:
+        achieved = flops / (kern_ms * 1e-3) / 1e12
+        r = {"bound": "tensor", "achieved": achieved, "peak": tc_peak, "unit": "TFLOP/s",
+             "frac": achieved / tc_peak, **common,
+             "peak_source": peaks["source"] + " bf16_tflops (burst)"
+             + ("" if dt == "bf16" else f" x {tc_peak / peaks['bf16_tflops']:.4g} (nominal "
+                                        f"{dt} / bf16 ratio)")}
+        if peaks.get("bf16_tflops_sustained"):
+            r["frac_vs_sustained"] = achieved / (peaks["bf16_tflops_sustained"]
+                                                 * tc_peak / peaks["bf16_tflops"])
+        return r
+    achieved = alg_bytes / (kern_ms * 1e-3) / 1e9
+    return {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": achieved / peaks["hbm_gbs"], **common,
+            "peak_source": peaks["source"] + " hbm_gbs"}
+
+
+def ranks_identical(ctx, idx, cost):
+    """Every rank must hold the same merged outputs (rank-ordered merge)."""
+    if ctx.world == 1:
+        return True
+    a = torch.cat([idx.view(-1).to(torch.float64), cost.view(-1).to(torch.float64)])
+    lo, hi = a.clone(), a.clone()
+    torch.distributed.all_reduce(lo, op=torch.distributed.ReduceOp.MIN)
+    torch.distributed.all_reduce(hi, op=torch.distributed.ReduceOp.MAX)
+    return bool(torch.equal(lo, hi))
+
+
+def e2e_measure(p: Problem, ctx: Ctx, K: int, warmup: int, eager: bool):
+    """Same metric through the public API with host buffers. Every step: X |
+    prev_cost | beam_offsets as ONE pinned host -> HBM copy (copy stream,
+    double-buffered, overlapping the previous step), the call writing into
+    preallocated outputs, idx | cost as ONE HBM -> pinned host copy; W, b
+    resident. World 1: each buffer's copy and call + copy-back replayed as
+    CUDA graphs (the API is capturable; a serving loop replays captured
+    steps)."""
+    w, dev = p.w, ctx.dev
+
     def a16(n):
         return (n + 15) // 16 * 16
-    xb, pb, ob = (X_h.numel() * X_h.element_size(), pc_h.numel() * 4, off_h.numel() * 4)
+    xb, pb, ob = (p.X_h.numel() * p.X_h.element_size(), p.pc_h.numel() * 4, p.off_h.numel() * 4)
     in_bytes = a16(xb) + a16(pb) + a16(ob)
     ib, cb = w.S * w.k * 8, w.S * w.k * 4
     out_bytes = a16(ib) + a16(cb)
     in_p = torch.empty(in_bytes, dtype=torch.uint8).pin_memory()
-    in_p[:xb].copy_(X_h.contiguous().view(-1).view(torch.uint8))
-    in_p[a16(xb):a16(xb) + pb].copy_(pc_h.contiguous().view(torch.uint8))
-    in_p[a16(xb) + a16(pb):a16(xb) + a16(pb) + ob].copy_(off_h.contiguous().view(torch.uint8))
+    in_p[:xb].copy_(p.X_h.contiguous().view(-1).view(torch.uint8))
+    in_p[a16(xb):a16(xb) + pb].copy_(p.pc_h.contiguous().view(torch.uint8))
+    in_p[a16(xb) + a16(pb):a16(xb) + a16(pb) + ob].copy_(p.off_h.contiguous().view(torch.uint8))
     out_p = torch.empty(out_bytes, dtype=torch.uint8).pin_memory()
 
     def views(buf):
-        Xv = buf[:xb].view(X.dtype).view(X.shape)
+        Xv = buf[:xb].view(p.X.dtype).view(p.X.shape)
         pv = buf[a16(xb):a16(xb) + pb].view(torch.float32)
         ov = buf[a16(xb) + a16(pb):a16(xb) + a16(pb) + ob].view(torch.int32)
         return Xv, pv, ov
@@ -366,10 +475,11 @@ def main():
     s_copy, s_comp = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
     h2d_done = [torch.cuda.Event() for _ in range(2)]
     comp_done = [torch.cuda.Event() for _ in range(2)]
+    nW = len(p.Ws)
     for e in comp_done:
         e.record(s_comp)
 
-    def e2e_step(i):
+    def step(i):
         j = i % 2
         Xd, pcd, offd = bufs[j]
         with torch.cuda.stream(s_copy):
@@ -378,37 +488,39 @@ def main():
             h2d_done[j].record(s_copy)
         with torch.cuda.stream(s_comp):
             s_comp.wait_event(h2d_done[j])
-            layer(Xd, Ws[i % 2], b, pcd, offd, w.k, out_idx=idx_v, out_cost=cost_v)
+            p.layer(Xd, p.Ws[i % nW], p.b, pcd, offd, w.k, out_idx=idx_v, out_cost=cost_v)
             out_p.copy_(out_d, non_blocking=True)
             comp_done[j].record(s_comp)
 
-    for i in range(args.warmup):
-        e2e_step(i)
+    for i in range(warmup):
+        step(i)
     torch.cuda.synchronize()
-    # World 1: the same pipeline with each buffer's H2D copy and each buffer's
-    # call + D2H copy captured as CUDA graphs (the API is capturable; a serving
-    # loop replays captured steps), so the host only replays them on the copy
-    # and compute streams with the same event ordering. Inputs still travel
-    # from pinned host memory and results back, every step.
-    e2e_graphs = world == 1 and not args.eager
-    if e2e_graphs:
-        g_copy, g_comp = [], []
+    graphs = ctx.world == 1 and not eager
+    if graphs:
+        # one graph per (input buffer, W copy) pair: steps i with i % 2 = j
+        # and i % nW = c; nW copies rotate as in the device-timed region
+        period = 2 * nW // (2 if nW % 2 == 0 else 1)
+        g_copy, g_comp = [], {}
         for j in range(2):
-            Xd, pcd, offd = bufs[j]
             gc = torch.cuda.CUDAGraph()
             with torch.cuda.graph(gc, stream=s_copy):
                 in_d[j].copy_(in_p, non_blocking=True)
+            g_copy.append(gc)
+        for i in range(period):
+            j, c = i % 2, i % nW
+            if (j, c) in g_comp:
+                continue
+            Xd, pcd, offd = bufs[j]
             gm = torch.cuda.CUDAGraph()
             with torch.cuda.graph(gm, stream=s_comp):
-                layer(Xd, Ws[j], b, pcd, offd, w.k, out_idx=idx_v, out_cost=cost_v)
+                p.layer(Xd, p.Ws[c], p.b, pcd, offd, w.k, out_idx=idx_v, out_cost=cost_v)
                 out_p.copy_(out_d, non_blocking=True)
-            g_copy.append(gc)
-            g_comp.append(gm)
+            g_comp[(j, c)] = gm
         torch.cuda.synchronize()
         for e in comp_done:
             e.record(s_comp)
 
-        def e2e_step(i):   # noqa: F811  (graph-replay version of the step above)
+        def step(i):   # noqa: F811  (graph-replay version of the step above)
             j = i % 2
             with torch.cuda.stream(s_copy):
                 s_copy.wait_event(comp_done[j])
@@ -416,115 +528,261 @@ def main():
                 h2d_done[j].record(s_copy)
             with torch.cuda.stream(s_comp):
                 s_comp.wait_event(h2d_done[j])
-                g_comp[j].replay()
+                g_comp[(j, i % nW)].replay()
                 comp_done[j].record(s_comp)
 
-        for i in range(args.warmup):
-            e2e_step(i)
+        for i in range(warmup):
+            step(i)
         torch.cuda.synchronize()
-    if world > 1:
-        torch.distributed.barrier()
+    ctx.barrier()
     s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s2.record(s_copy)
     for i in range(K):
-        e2e_step(i)
+        step(i)
     e2.record(s_comp)
     torch.cuda.synchronize()
-    e2e_ms = s2.elapsed_time(e2)
+    ms = ctx.max(s2.elapsed_time(e2))
+    return {"value": w.N / (ms / K * 1e-3), "unit": UNIT, "h2d_bytes_per_step": in_bytes,
+            "d2h_bytes_per_step": out_bytes,
+            "note": "every step: X | prev_cost | beam_offsets as ONE pinned host -> HBM copy "
+                    "(copy stream, double-buffered, overlapping the previous step), the "
+                    "public-API call writing into preallocated outputs, idx | cost as ONE "
+                    "HBM -> pinned host copy; W, b resident; "
+                    + ("each buffer's copy and call + copy-back replayed as CUDA graphs"
+                       if graphs else "eager calls")}
+
+
+def side_workload(name, w, ctx, K, warmup, peaks, n_sent, eager):
+    """A further config as its own object: rows/s, fused-kernel roofline and
+    an oracle parity sample (rank 0)."""
+    p = Problem(w, ctx)
+    m = measure(p, ctx, K, warmup, eager)
+    res = {"workload": config_of(w, ctx.world)["workload"], "value": w.N / (m["ms_per_step"] * 1e-3),
+           "unit": UNIT, "ms_per_step": m["ms_per_step"], "steps": K, "timing": m["timing"],
+           "w_copies": len(p.Ws),
+           "roofline": roofline(w, p.v1 - p.v0, m["kernel_ms"], peaks, "ol_tc_kernel / ol_tc2_kernel")}
+    if "stages_ms_per_rank" in m:
+        res["stages_ms_per_rank"] = m["stages_ms_per_rank"]
+    p.step(0)
+    torch.cuda.synchronize()
+    res["ranks_identical"] = ranks_identical(ctx, p.idx, p.cost)
+    if ctx.rank == 0 and n_sent > 0:
+        res["parity"], _ = parity_sample(w, p.idx, p.cost, p.X_h, p.full_W(), p.full_b(), p.pc_h,
+                                         n_sent)
+    del p
+    torch.cuda.empty_cache()
+    return res
+
+
+def f32_object(ctx, K, warmup, peaks, n_sent):
+    """fp32 (the paper's baseline precision) on the beam shape via
+    the 3xTF32 tensor-core plan: X split inside every step, W split once."""
+    import paper_1805_09863_b200 as amun
+    w = dataclasses.replace(synth.CONFIGS["beam"], dtype="f32")
+    dev = ctx.dev
+    X_h, W_h, b_h, pc_h = synth.gen_X(w), synth.gen_W(w), synth.gen_b(w), synth.gen_prev_cost(w)
+    X, b, pc, off = X_h.to(dev), b_h.to(dev), pc_h.to(dev), synth.gen_offsets(w, dev)
+    W3 = amun.split_tf32x3(W_h.to(dev), "W")         # 1.1 GB > L2: one copy suffices
+    X3 = torch.empty((w.N, 3 * w.H), dtype=torch.float32, device=dev)
+    ol = amun.OutputLayer(w.H, w.V, dtype="tf32x3", k_max=w.k, max_rows=w.N, max_sentences=w.S,
+                          device=dev)
+    oi = torch.empty((w.S, w.k), dtype=torch.int64, device=dev)
+    oc = torch.empty((w.S, w.k), dtype=torch.float32, device=dev)
+
+    def step(i):
+        amun.split_tf32x3(X, "X", out=X3)
+        ol(X3, W3, b, pc, off, w.k, out_idx=oi, out_cost=oc)
+    for i in range(warmup):
+        step(i)
+    st = torch.cuda.Stream(dev)
+    with torch.cuda.stream(st):
+        step(0)
+    torch.cuda.synchronize()
+    g = capture(step, K, st)
+    replay_ms(g, st)
+    ms = replay_ms(g, st) / K
+    kg = capture(lambda i: ol.scores(X3, W3, b), K, st)
+    replay_ms(kg, st)
+    kms = replay_ms(kg, st) / K
+    res = {"workload": "beam shape with fp32 X, W (3xTF32 on tcgen05 kind::tf32, "
+                       "amun_split_tf32x3 of X inside every step)",
+           "value": w.N / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "steps": K,
+           "dtype": "f32 (3xTF32)",
+           "roofline": roofline(w, w.V, kms, peaks, "ol_tc_kernel<.., ELT=2> (tf32x3)",
+                                plan_dtype="tf32x3")}
+    if n_sent > 0:
+        res["parity"], _ = parity_sample(w, oi, oc, X_h, W_h, b_h, pc_h, n_sent)
+    del W3, g, kg
+    torch.cuda.empty_cache()
+    return res
+
+
+def e4m3_object(p: Problem, ctx, K):
+    """The FP8 path on the same workload (context, not the headline): W
+    quantised once per copy, X quantised inside every step, one graph."""
+    import paper_1805_09863_b200 as amun
+    w, dev = p.w, ctx.dev
+    W8s = [amun.quantize_e4m3(Wc) for Wc in p.Ws]
+    X8 = torch.empty((w.N, w.H), dtype=torch.uint8, device=dev)
+    xs = torch.empty(w.N, dtype=torch.float32, device=dev)
+    o8 = amun.OutputLayer(w.H, w.V, dtype="e4m3", k_max=w.k, max_rows=w.N, max_sentences=w.S,
+                          device=dev)
+    oi8 = torch.empty((w.S, w.k), dtype=torch.int64, device=dev)
+    oc8 = torch.empty((w.S, w.k), dtype=torch.float32, device=dev)
+
+    def f8_step(i):
+        amun.quantize_e4m3(p.X, out=X8, scale=xs)
+        c = W8s[i % len(W8s)]
+        o8.call_e4m3(X8, xs, c[0], c[1], p.b, p.pc, p.off, w.k, out_idx=oi8, out_cost=oc8)
+    st = torch.cuda.Stream(dev)
+    with torch.cuda.stream(st):
+        f8_step(0)
+    torch.cuda.synchronize()
+    g8 = capture(f8_step, K, st)
+    replay_ms(g8, st)
+    ms8 = replay_ms(g8, st) / K
+    del W8s, g8
+    return {"value": w.N / (ms8 * 1e-3), "unit": UNIT, "ms_per_step": ms8,
+            "note": "same workload with X and W as OCP E4M3 + per-row fp32 scales on tcgen05 "
+                    "kind::f8f6f4 (amun_output_layer_e4m3); X quantised inside every step; "
+                    "parity vs the oracle on the dequantised values in tests/test_gpu_e4m3.py"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="beam", choices=list(synth.CONFIGS))
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "oneshot"],
+                    help="N > 1: NCCL all-gather + merge, or the NVLink one-shot kernel")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e4m3", action="store_true", help="skip the FP8 context measurement")
+    ap.add_argument("--no-side", action="store_true",
+                    help="skip the side objects (shard, greedy, f32, e4m3)")
+    ap.add_argument("--eager", action="store_true", help="launch steps eagerly (no CUDA graph)")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    w = synth.CONFIGS[args.workload]
+
+    env_world = os.environ.get("WORLD_SIZE")
+    if args.impl == "reference":
+        return run_reference(args, w)
+    if env_world is None and args.gpus > 1:
+        return spawn_ranks(args)
+    world = int(env_world or "1")
+    if world != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}\n")
+        return 2
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if local >= torch.cuda.device_count():
+        sys.stderr.write(f"bench.py: LOCAL_RANK {local} but {torch.cuda.device_count()} GPUs\n")
+        return 2
+    torch.cuda.set_device(local)
+    ctx = Ctx(world, rank, local)
+    comm = None
     if world > 1:
-        t = torch.tensor([e2e_ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_ms = float(t.item())
-    e2e_value = w.N / (e2e_ms / K * 1e-3)
-    h2d = in_bytes
-    d2h = out_bytes
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=ctx.dev)
+        comm = {"backend": dist.get_backend(), "world": dist.get_world_size(),
+                "nranks_ok": dist.get_world_size() == args.gpus,
+                "nccl_version": ".".join(map(str, torch.cuda.nccl.version()))}
+    import paper_1805_09863_b200 as amun  # noqa: F401  (loads libamun.so; raises if missing)
 
-    if rank != 0:
-        if world > 1:
-            torch.distributed.destroy_process_group()
-        return
-
-    # ---------------- roofline of the dominant kernel (the fused GEMM kernel)
-    # algorithmic work per launch: FLOP = 2*N*H*V_local (tensor cores);
-    # bytes = W + X + b once (the N x V logits never exist in HBM).
+    K = args.steps
     peaks = load_peaks()
-    Vl = v1 - v0
-    flops = 2.0 * w.N * w.H * Vl
-    esz = 2 if w.dtype == "bf16" else 4
-    alg_bytes = Vl * w.H * esz + w.N * w.H * esz + Vl * 4
-    kern_mean_ms = statistics.mean(kern_ms)
-    t_tc = flops / (peaks["bf16_tflops"] * 1e12)
-    t_hbm = alg_bytes / (peaks["hbm_gbs"] * 1e9)
+    p = Problem(w, ctx, exchange=args.exchange)
+    with ClockSampler(local) as clk:
+        m = measure(p, ctx, K, args.warmup, args.eager, clk)
+    ms_per_step = m["ms_per_step"]
+    value = w.N / (ms_per_step * 1e-3)
+    p.step(0)
+    torch.cuda.synchronize()
+    identical = ranks_identical(ctx, p.idx, p.cost)
+
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
+    if os.path.exists(tp) and world == 1:
         try:
             traffic = json.load(open(tp)).get(w.name)
         except Exception:
             traffic = None
-    common = {"traffic": traffic,
-              "kernel": "ol_tc_kernel / ol_tc2_kernel (fused GEMM + bias + online softmax + row k-best)",
-              "kernel_ms_mean": kern_mean_ms, "kernel_share_of_step": kern_mean_ms / ms_per_step,
-              "algorithmic": f"{flops:.4g} FLOP and {alg_bytes:.4g} B per launch "
-                             f"(2*N*H*V_local; W + X + b once)"}
-    if t_tc >= t_hbm:
-        achieved = flops / (kern_mean_ms * 1e-3) / 1e12
-        roof = {"bound": "tensor", "achieved": achieved, "peak": peaks["bf16_tflops"],
-                "unit": "TFLOP/s", "frac": achieved / peaks["bf16_tflops"], **common,
-                "peak_source": peaks["source"] + " bf16_tflops (burst)",
-                "frac_vs_sustained": (achieved / peaks["bf16_tflops_sustained"])
-                if peaks.get("bf16_tflops_sustained") else None}
-    else:
-        achieved = alg_bytes / (kern_mean_ms * 1e-3) / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / peaks["hbm_gbs"], **common,
-                "peak_source": peaks["source"] + " hbm_gbs"}
+    roof = roofline(w, p.v1 - p.v0, m["kernel_ms"], peaks,
+                    "ol_tc_kernel / ol_tc2_kernel (fused GEMM + bias + online softmax + row "
+                    "k-best; amun_ol_scores alone)" if w.dtype != "f32" else "ol_simt_kernel",
+                    traffic)
+    roof["kernel_share_of_step"] = m["kernel_ms"] / ms_per_step
 
-    # ---------------- CPU baseline (oracle) + sampled parity, rank 0, N=1 only
-    cpu = None
-    parity = None
-    if world == 1 and not args.no_cpu_baseline:
-        n_sent = int(os.environ.get("AMUN_CPU_SENTENCES", "128"))
-        dt, rows, res, logp, pcs = oracle_sample(w, X_h, W_h, b_h, pc_h, n_sent)
-        cpu = {"value": rows / dt, "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
-               "sample": f"first {n_sent} sentences ({rows} rows) x full V={w.V}, one pass, "
-                         f"{dt:.1f} s"}
-        sys.path.insert(0, os.path.join(ROOT, "tests"))
-        from tests.compare import compare_kbest
-        ii, cc = step(0)
-        torch.cuda.synchronize()
-        gi, gc = ii.cpu().numpy()[:n_sent], cc.cpu().numpy()[:n_sent]
-        oi, oc32, oc64, nxt = res
-        rep = compare_kbest(gi, gc, lambda s, r, v: pcs[r] + logp[r, v], oc64,
-                            np.full(n_sent, w.k), w.dtype, w.V, o_next=nxt)
-        parity = {"sentences": n_sent, **rep, "status": "pass"}
+    e2e = e2e_measure(p, ctx, K, args.warmup, args.eager)
 
+    # ---- CPU baseline (oracle, rank 0, N = 1) and oracle parity (rank 0, every N)
+    cpu, parity = None, None
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            n_sent = int(os.environ.get("AMUN_CPU_SENTENCES", str(w.S)))
+            parity, dt = parity_sample(w, p.idx, p.cost, p.X_h, p.W_h, p.b_h, p.pc_h, n_sent)
+            cpu = {"value": parity["rows"] / dt, "unit": UNIT, "cores": blas_threads(),
+                   "kind": "oracle", "sample": f"first {n_sent} sentences ({parity['rows']} rows)"
+                                               f" x full V={w.V}, one pass, {dt:.1f} s"}
+        elif not args.no_cpu_baseline:
+            parity, _ = parity_sample(w, p.idx, p.cost, p.X_h, p.full_W(), p.full_b(), p.pc_h,
+                                      int(os.environ.get("AMUN_PARITY_SENTENCES", "16")))
+    if parity is not None:
+        parity["ranks_identical"] = identical
+
+    # ---- side objects
+    side = {}
+    e4m3 = None
+    if not args.no_side and w.name == "beam":
+        if world == 1 and not args.no_e4m3 and w.dtype == "bf16":
+            e4m3 = e4m3_object(p, ctx, K)
+        del p
+        torch.cuda.empty_cache()
+        Ks = max(3, min(K, 50))
+        side["shard"] = side_workload("shard", synth.CONFIGS["shard"], ctx, Ks, args.warmup,
+                                      peaks, 4 if not args.no_cpu_baseline else 0, args.eager)
+        side["shard"]["note"] = ("north_star's vocab-sharded scaling config (cfg5) at this N, "
+                                 "strong scaling; the headline is cfg3")
+        if world == 1:
+            side["greedy"] = side_workload("greedy", synth.CONFIGS["greedy"], ctx, K,
+                                           args.warmup, peaks,
+                                           128 if not args.no_cpu_baseline else 0, args.eager)
+            side["f32"] = f32_object(ctx, max(3, min(K, 50)), args.warmup, peaks,
+                                     4 if not args.no_cpu_baseline else 0)
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return 0
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": config_of(w, args),
+        "scaling": "strong", "vs_baseline": None, "dtype": w.dtype, "data": "synthetic",
+        "config": config_of(w, world, {
+            "l2": f"W rotated over {m['w_copies']} resident copies (> 2 x 126 MB "
+                  f"L2 in total) between steps",
+            "exchange": args.exchange if world > 1 else None}),
         "roofline": roof,
         "cpu_baseline": cpu,
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h,
-                "note": "every step: X | prev_cost | beam_offsets as ONE pinned host -> HBM copy "
-                        "(copy stream, double-buffered, overlapping the previous step), the "
-                        "public-API call writing into preallocated outputs, idx | cost as ONE "
-                        "HBM -> pinned host copy; W, b resident; "
-                        + ("each buffer's copy and call + copy-back replayed as CUDA graphs"
-                           if e2e_graphs else "eager calls")},
-        "gpu_launches": K * layer.launches_per_step,
-        "e4m3": e4m3,
-        "timing": "CUDA graph of the K steps, replayed once" if use_graph else "eager launches",
+        "e2e": e2e,
+        "gpu_launches": K * m["launches_per_step"],
+        "timing": m["timing"],
         "clocks": clk.summary(),
         "parity": parity,
-        "gpu": torch.cuda.get_device_name(dev),
+        "comm": comm,
+        "e4m3": e4m3,
+        **side,
+        "gpu": torch.cuda.get_device_name(ctx.dev),
     }
+    if "stages_ms_per_rank" in m:
+        out["stages_ms_per_rank"] = m["stages_ms_per_rank"]
     print(json.dumps(out))
     if world > 1:
         torch.distributed.destroy_process_group()
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

@@ -120,6 +120,14 @@ size_t amun_ol_workspace_bytes(const amun_ol* plan);
  * Errors: AMUN_EINVAL (NULL, misaligned), AMUN_ECUDA. */
 amun_status amun_ol_workspace_init(amun_ol* plan, void* workspace, void* stream);
 
+/* Kernels of this library one call enqueues (for launch accounting in
+ * benchmarks): `call` = 0 amun_output_layer / _dev / _e4m3 / amun_argmax,
+ * 1 amun_output_layer_partial, 2 amun_merge_partials. With the fused tail
+ * (the default for tcgen05 plans, see amun_output_layer) calls 0 and 1 are
+ * ONE launch; otherwise two. N = 0 calls may enqueue fewer. Returns -1 for
+ * a NULL plan or an unknown `call`. */
+int amun_ol_launches_per_call(const amun_ol* plan, int call);
+
 /* Floats per row of a partial record: 2 + 2*k_max, laid out as
  *   { m, s, l[0..k_max-1], v[0..k_max-1] }
  * m = max biased logit of the covered vocabulary, s = sum exp(l - m) over it,
@@ -366,17 +374,26 @@ amun_status amun_beam_advance(const int64_t* out_idx, const float* out_cost, int
                               int32_t* new_token, float* new_cost, int32_t* counts,
                               int32_t* counts_host, void* workspace, void* stream);
 
+/* 1 in *err if a one-shot wait on `buf` (this rank's own buffer) ever timed
+ * out: a peer did not signal a call within 4 s (it failed validation, used
+ * another N / G, or never called). The call that timed out wrote no outputs
+ * and the exchange is out of step from then on. Synchronous (a blocking
+ * device read). Errors: AMUN_EINVAL (NULL), AMUN_ECUDA. */
+amun_status amun_oneshot_error(const void* buf, int* err);
+
 /* ------------------------------------------------------------------------
  * NVLink one-shot exchange: the vocab-sharded output
  * layer (Alg. 6; the reduce of P:244-251 applied to the
  * (max, sum, k-best) partial states of P:232-242) with the exchange done by
  * the library's own kernel over peer memory instead of a collective call.
- * After this rank's fused kernel, one cooperative kernel combines the rank's
- * per-CTA records into one record per row, stores it into slot [rank] of
- * EVERY rank's receive buffer (CUDA IPC mappings: NVLink stores), signals
- * each rank (system-scope release), waits for all G ranks' signals
- * (acquire), and runs the per-sentence top-k_s over the G records of each
- * row. Every rank returns the same result as amun_output_layer_partial on
+ * In the fused kernel's tail (one cooperative launch; N > 0, tcgen05 plans,
+ * AMUN_TAIL not "off"), after every CTA has emitted its partial records, the
+ * CTAs combine them into one record per row, store it into slot [rank] of
+ * EVERY rank's receive buffer (CUDA IPC mappings: NVLink stores), signal
+ * each rank (system-scope release, once per peer from the rank's last CTA),
+ * wait for all G ranks' signals (acquire), and run the per-sentence top-k_s
+ * over the G records of each row. (N = 0 or AMUN_TAIL=off: the fused kernel,
+ * then a separate cooperative one-shot kernel doing the same.) Every rank returns the same result as amun_output_layer_partial on
  * each shard + an all-gather + amun_merge_partials.
  *
  * Buffer: one per rank, from amun_oneshot_alloc (a whole cudaMalloc
@@ -404,9 +421,11 @@ amun_status amun_beam_advance(const int64_t* out_idx, const float* out_cost, int
  *   bufs    host array [G] of device pointers: bufs[p] = rank p's buffer as
  *           mapped in this process (bufs[rank] = the own buffer), 256-byte
  *           aligned; 1 <= G <= 8, 0 <= rank < G.
- *   Enqueues 2 kernels (fused, then the one-shot kernel) on `stream`. The
- *   call returns before the peers have signalled; a rank whose peers never
- *   make the matching call waits forever (as in any collective).
+ *   Enqueues 1 kernel on `stream` (2 in the fallback forms above). The
+ *   call returns before the peers have signalled. A wait is bounded: if a
+ *   peer does not signal within 4 s the kernel sets the buffer's error word
+ *   (amun_oneshot_error), writes no outputs for that call and exits — the
+ *   GPU is never left spinning.
  *   EINVAL on argument errors (nothing enqueued).
  * amun_output_layer_oneshot_emulated (test / measurement hook): G ranks on
  *   ONE GPU. Runs the G shards' fused kernels one after another, then ONE

@@ -27,7 +27,7 @@ EXPORTS = [
     "amun_argmax_e4m3", "amun_split_tf32x3", "amun_oneshot_buffer_bytes", "amun_oneshot_alloc",
     "amun_oneshot_free", "amun_oneshot_open", "amun_oneshot_close", "amun_output_layer_oneshot",
     "amun_output_layer_oneshot_emulated", "amun_sentence_alive", "amun_ol_workspace_init",
-    "amun_debug_timeline",
+    "amun_debug_timeline", "amun_ol_launches_per_call", "amun_oneshot_error",
 ]
 AMUN_ONESHOT_MAX_G = 8
 
@@ -66,6 +66,8 @@ def load() -> ctypes.CDLL:
         "amun_ol_partial_stride": (i32, [vp]),
         "amun_ol_workspace_init": (st, [vp, vp, vp]),
         "amun_debug_timeline": (st, [vp, vp]),
+        "amun_ol_launches_per_call": (i32, [vp, i32]),
+        "amun_oneshot_error": (st, [vp, vp]),
         "amun_output_layer": (st, [vp, vp, vp, vp, vp, vp, i32, i32, vp, i32, vp, vp, vp, vp]),
         "amun_output_layer_dev": (st, [vp, vp, vp, vp, vp, vp, vp, i32, vp, i32, vp, vp, vp, vp]),
         "amun_ol_scores": (st, [vp, vp, vp, vp, i32, vp, vp]),

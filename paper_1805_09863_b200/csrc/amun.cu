@@ -228,7 +228,7 @@ amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b
                        void* workspace, float* logits, cudaStream_t st, int mode,
                        const int* N_dev = nullptr, const float* x_scale = nullptr,
                        const float* w_scale = nullptr, int tail = TAIL_NONE,
-                       const MergeParams* tmp = nullptr) {
+                       const MergeParams* tmp = nullptr, const OneShotTail* os = nullptr) {
   if (N == 0) return AMUN_OK;
   CUDA_TRY(cudaSetDevice(pl->device));
   int grid;
@@ -292,6 +292,7 @@ amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b
       tp.mp.N_dev = nullptr;   // the kernel passes its own resolved N / schedule (TcDyn)
       tp.mp.num_sms = pl->num_sms;
     }
+    if (os) tp.os = *os;
     tp.tl = pl->tl;
     if (pl->pf_bytes > 0 && !N_dev) {
       tp.pf_w = static_cast<const char*>(W);
@@ -543,6 +544,12 @@ amun_status amun_ol_workspace_init(amun_ol* plan, void* workspace, void* stream)
 }
 
 int amun_ol_partial_stride(const amun_ol* plan) { return plan ? plan->stride : 0; }
+
+int amun_ol_launches_per_call(const amun_ol* plan, int call) {
+  if (!plan || call < 0 || call > 2) return -1;
+  if (call == 2) return 1;
+  return use_tail(plan, 1) ? 1 : 2;
+}
 
 amun_status amun_ol_scores(amun_ol* plan, const void* X, const void* W, const float* b, int N,
                            void* workspace, void* stream) {
@@ -1090,6 +1097,15 @@ amun_status amun_oneshot_open(const void* ipc_handle, int device, void** peer) {
   return AMUN_OK;
 }
 
+amun_status amun_oneshot_error(const void* buf, int* err) {
+  if (!buf || !err) return fail(AMUN_EINVAL, "NULL buf or err");
+  unsigned int w = 0;
+  CUDA_TRY(cudaMemcpy(&w, static_cast<const unsigned int*>(buf) + OS_ERR, sizeof(w),
+                      cudaMemcpyDeviceToHost));
+  *err = (int)w;
+  return AMUN_OK;
+}
+
 amun_status amun_oneshot_close(void* peer) {
   if (peer) CUDA_TRY(cudaIpcCloseMemHandle(peer));
   return AMUN_OK;
@@ -1110,6 +1126,20 @@ amun_status amun_output_layer_oneshot(amun_ol* plan, const void* X, const void* 
   if (s != AMUN_OK) return s;
   CUDA_TRY(cudaSetDevice(plan->device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (use_tail(plan, N)) {
+    // ONE launch: the fused kernel whose tail runs the row phase, the peer
+    // stores, the signal, the wait and the sentence phase (tail.cuh)
+    OneShotTail os;
+    memset(&os, 0, sizeof(os));
+    for (int p = 0; p < G; ++p) os.buf[p] = static_cast<char*>(bufs[p]);
+    os.G = G;
+    os.rank = rank;
+    os.recv_elems = (long long)oneshot_recv_elems(plan, G);
+    const MergeParams mp = sent_merge(plan, prev_cost, beam_offsets, N, S, k_per_sentence, k,
+                                      out_idx, out_cost);
+    return run_scores(plan, X, W, b, N, workspace, nullptr, st, 0, nullptr, nullptr, nullptr,
+                      TAIL_ONESHOT, &mp, &os);
+  }
   if (N > 0) {
     s = run_scores(plan, X, W, b, N, workspace, nullptr, st, 0);
     if (s != AMUN_OK) return s;

@@ -11,7 +11,13 @@
 //   TAIL_SENT   sentences s = cta, cta + grid, ...: the per-sentence top-k_s
 //               of prev_cost + l - lse (merge.cuh merge_sentence);
 //   TAIL_ROWS   rows: one merged record per row (vocab-shard output);
-//   TAIL_ARGMAX rows: Alg. 5's argmax over the row's records.
+//   TAIL_ARGMAX rows: Alg. 5's argmax over the row's records;
+//   TAIL_ONESHOT the vocab-sharded exchange (peer.cuh):
+//               rows as TAIL_ROWS, each merged record stored into slot
+//               [rank] of every rank's receive buffer (NVLink stores), one
+//               system-scope signal per peer from the rank's last CTA, a
+//               bounded wait for every rank's signal, then sentences as
+//               TAIL_SENT over the G records of each row.
 // Waiting on other CTAs is safe because the launch is cooperative (every CTA
 // of the <= #SM grid co-resident, launch_tc.cuh launch_kernel); a count that
 // overshoots or a wait longer than 10 s traps (loud failure, never a silent
@@ -134,6 +140,41 @@ __device__ __forceinline__ void grid_tail(const TcParams& p, const TcDyn& dyn, u
   } else if (kind == TAIL_ARGMAX) {
     for (int r = c + G * warp; r < mp.N; r += G * MS_WARPS)
       argmax_row(mp, r, lane, mp.out_idx, mp.out_cost);
+  } else if (kind == TAIL_ONESHOT) {
+    Cand* pool = reinterpret_cast<Cand*>(scratch);
+    Cand* best = pool + KB + MS_CAP;
+    int* s_valid = reinterpret_cast<int*>(best + KB);
+    int* s_os = s_valid + 1;          // {failed wait, epoch}
+    const OneShotTail& os = p.os;
+    // the epoch: read before this CTA's done-arrival (os_signal), which the
+    // rank's last CTA waits for before it advances the epoch
+    if (tid == 0) {
+      s_os[0] = 0;
+      s_os[1] = (int)os_epoch(os.buf[os.rank]);
+    }
+    MergeWarpsSync()();
+    const unsigned int epoch = (unsigned int)s_os[1];
+    for (int r = c + G * warp; r < mp.N; r += G * MS_WARPS) {
+      float lse, M, Z, l;
+      int v;
+      row_topk<KB>(mp, r, lane, lse, M, Z, l, v);
+      os_store_record(os.buf, os.G, os_record_off(epoch, os.recv_elems, os.rank, mp.N, r, mp.stride),
+                      mp.k_max, lane, M, Z, l, v);
+    }
+    MergeWarpsSync()();
+    if (tid == 0) os_signal(os.buf, os.G, os.rank, G, epoch);
+    if (!os_wait(os.buf[os.rank], os.G, epoch)) s_os[0] = 1;
+    MergeWarpsSync()();
+    if (s_os[0]) return;
+    MergeParams dp = mp;              // sentence phase over [G][N][stride]
+    dp.layout = 1;
+    dp.G = os.G;
+    dp.part = reinterpret_cast<const float*>(os.buf[os.rank] + OS_CTRL_BYTES) +
+              (long long)(epoch & 1u) * os.recv_elems;
+    for (int s = c; s < dp.S; s += G) {
+      merge_sentence<KB, MergeWarpsSync>(dp, s, pool, best, *s_valid);
+      MergeWarpsSync()();
+    }
   }
   if (p.tl) {
     MergeWarpsSync()();

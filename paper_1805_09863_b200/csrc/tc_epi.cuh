@@ -12,6 +12,7 @@
 // rounds through one exchange area and group 0 writes the partial record.
 #pragma once
 #include "merge.cuh"
+#include "peer.cuh"
 
 namespace amun {
 
@@ -42,6 +43,7 @@ struct TcParams {
   long long pf_row_bytes;                  // bytes of one W row (K elements)
   long long pf_max_bytes;                  // prefetch at most this many bytes of a CTA's W range
   unsigned long long* __restrict__ tl;     // timeline probe [grid][TL_N] (amun_debug_timeline), else NULL
+  OneShotTail os;                          // TAIL_ONESHOT: the peer buffers (peer.cuh)
 };
 // Timeline probe points (globaltimer ns; per CTA; see amun_debug_timeline).
 enum { TL_ENTRY = 0, TL_SETUP = 1, TL_TMA0 = 2, TL_FULL0 = 3, TL_MMA_END = 4, TL_EPI_LAST = 5,
@@ -53,7 +55,7 @@ __device__ __forceinline__ void tl_mark(const unsigned long long* tl_base, int p
     const_cast<unsigned long long*>(tl_base)[(long long)blockIdx.x * TL_N + point] = t;
   }
 }
-enum { TAIL_NONE = 0, TAIL_SENT = 1, TAIL_ROWS = 2, TAIL_ARGMAX = 3,
+enum { TAIL_NONE = 0, TAIL_SENT = 1, TAIL_ROWS = 2, TAIL_ARGMAX = 3, TAIL_ONESHOT = 4,
        TAIL_X_NOWORK = 16, TAIL_X_NOCOOP = 32,      // experiment flags (env AMUN_TAIL)
        TAIL_X_FENCE = 64, TAIL_X_SLEEP = 128 };
 

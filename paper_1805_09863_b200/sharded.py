@@ -32,10 +32,11 @@ def shard_range(V: int, world: int, rank: int, align: int = 16):
 
 def exchange(partial: torch.Tensor, world: int, group=None) -> torch.Tensor:
     """All-gather the [N, stride] partial records of every rank into
-    [world, N, stride] in rank order (the only collective of the path)."""
-    if world == 1:
-        return partial.unsqueeze(0)
+    [world, N, stride] in rank order (the only collective of the path). With a
+    process group initialised the collective runs even at world 1."""
     import torch.distributed as dist
+    if world == 1 and not (dist.is_available() and dist.is_initialized()):
+        return partial.unsqueeze(0)
     N = partial.shape[0]
     out = torch.empty((world * N,) + tuple(partial.shape[1:]), dtype=partial.dtype,
                       device=partial.device)
@@ -93,6 +94,15 @@ class OneShotExchange:
         if world > 1:   # every buffer zeroed and mapped before anyone signals
             dist.barrier(group=group)
 
+    def error(self) -> bool:
+        """True if a wait of this rank ever timed out (amun_oneshot_error;
+        synchronous)."""
+        import ctypes
+        from . import _L, check
+        e = ctypes.c_int(0)
+        check(_L.amun_oneshot_error(ctypes.c_void_p(self.own), ctypes.byref(e)))
+        return bool(e.value)
+
     def close(self):
         if getattr(self, "ptrs", None) is None:
             return
@@ -114,11 +124,15 @@ class ShardedOutputLayer:
     (exchange="nccl") or the NVLink one-shot kernel (exchange="oneshot")."""
 
     def __init__(self, H, V, world, rank, *, dtype="bf16", k_max=16, max_rows=1 << 16,
-                 max_sentences=1 << 16, device=None, group=None, exchange="nccl"):
+                 max_sentences=1 << 16, device=None, group=None, exchange="nccl",
+                 force_sharded=False):
+        """force_sharded: run partial + exchange + merge even at world 1 (the
+        multi-rank code path on one rank; tests)."""
         from . import OutputLayer
         if exchange not in ("nccl", "oneshot"):
             raise ValueError(f"exchange must be 'nccl' or 'oneshot', not {exchange!r}")
         self.world, self.rank, self.group, self.exchange = world, rank, group, exchange
+        self.sharded = world > 1 or force_sharded
         self.v0, self.v1 = shard_range(V, world, rank)
         if self.v1 <= self.v0:
             raise ValueError(f"rank {rank} owns no vocabulary (V={V}, world={world})")
@@ -126,40 +140,52 @@ class ShardedOutputLayer:
                               k_max=k_max, max_rows=max_rows, max_sentences=max_sentences,
                               device=device)
         # kernels of ours per step (the NCCL all-gather kernel is not counted)
-        self.launches_per_step = 2 if world == 1 else 3
+        L = self.ol.launches
+        self.launches_per_step = L["partial"] + L["merge"] if self.sharded else L["call"]
         self.oneshot = None
         if exchange == "oneshot":
             dev = self.ol.device.index or 0
             self.oneshot = OneShotExchange(self.ol._h, world, rank, dev, group)
-            self.launches_per_step = 2
+            self.launches_per_step = L["call"]   # the exchange runs in the fused kernel's tail
+        self._part = None
 
     def __call__(self, X, W, b, prev_cost, beam_offsets, k, k_per_sentence=None, events=None,
-                 out_idx=None, out_cost=None):
+                 out_idx=None, out_cost=None, stage_events=None):
         """W, b: this rank's shard. events: optional (start, stop) CUDA events
         recorded around the fused GEMM kernel (stage 1) on the current stream.
+        stage_events (sharded path): 4 events recorded before the partial
+        kernel, after it, after the exchange and after the merge.
         out_idx / out_cost: optional preallocated [S, k] outputs."""
         if self.oneshot is not None:
             return self.ol.oneshot(X, W, b, prev_cost, beam_offsets, k, self.oneshot.ptrs,
                                    self.rank, k_per_sentence, out_idx=out_idx, out_cost=out_cost)
-        if self.world == 1 and not events:   # one C-ABI call (amun_output_layer)
+        if not self.sharded and not events:   # one C-ABI call (amun_output_layer)
             return self.ol(X, W, b, prev_cost, beam_offsets, k, k_per_sentence,
                            out_idx=out_idx, out_cost=out_cost)
-        if self.world == 1:
-            if events:
-                events[0].record()
+        if not self.sharded:
+            events[0].record()
             self.ol.scores(X, W, b)
-            if events:
-                events[1].record()
+            events[1].record()
             return self.ol.select(X.shape[0], prev_cost, beam_offsets, k, k_per_sentence,
                                   out_idx=out_idx, out_cost=out_cost)
-        if events:
-            events[0].record()
-        part = self.ol.partial(X, W, b)
-        if events:
-            events[1].record()
+        ev = stage_events or ((events[0], events[1]) + (None, None) if events else None)
+        N = X.shape[0]
+        if self._part is None or self._part.shape[0] != N:
+            self._part = torch.empty((N, self.ol.stride), dtype=torch.float32,
+                                     device=self.ol.device)
+        if ev and ev[0] is not None:
+            ev[0].record()
+        part = self.ol.partial(X, W, b, out=self._part)
+        if ev and ev[1] is not None:
+            ev[1].record()
         allp = exchange(part, self.world, self.group)
-        return self.ol.merge(allp, prev_cost, beam_offsets, k, k_per_sentence,
-                             out_idx=out_idx, out_cost=out_cost)
+        if ev and ev[2] is not None:
+            ev[2].record()
+        res = self.ol.merge(allp, prev_cost, beam_offsets, k, k_per_sentence,
+                            out_idx=out_idx, out_cost=out_cost)
+        if ev and ev[3] is not None:
+            ev[3].record()
+        return res
 
 
 class EmulatedOneShot:

@@ -149,12 +149,15 @@ def test_emulated_empty():
 def test_real_mode_single_rank_ipc_buffer():
     """amun_output_layer_oneshot itself (rank parameter, IPC-exported buffer)
     at world 1 through ShardedOutputLayer(exchange="oneshot"): equals the
-    single-GPU path over repeated calls."""
+    single-GPU path over repeated calls. With the fused tail (default) the
+    whole exchange runs inside the fused kernel (one launch); AMUN_TAIL=off
+    gives the fused kernel + the separate one-shot kernel."""
     from paper_1805_09863_b200.sharded import ShardedOutputLayer
     w = synth.CONFIGS["beam"]
     sh = ShardedOutputLayer(w.H, w.V, 1, 0, k_max=w.k, max_rows=w.N, max_sentences=w.S,
                             exchange="oneshot")
-    assert sh.launches_per_step == 2
+    assert sh.launches_per_step == sh.ol.launches["call"]
+    assert not sh.oneshot.error()
     X, W, b = synth.gen_X(w).to(DEV), synth.gen_W(w).to(DEV), synth.gen_b(w).to(DEV)
     pc, off = synth.gen_prev_cost(w).to(DEV), synth.gen_offsets(w).to(DEV)
     ref_i, ref_c = sh.ol(X, W, b, pc, off, w.k)
@@ -162,6 +165,7 @@ def test_real_mode_single_rank_ipc_buffer():
         i, c = sh(X, W, b, pc, off, w.k)
         torch.cuda.synchronize()
         assert torch.equal(i, ref_i) and torch.equal(c, ref_c), call
+    assert not sh.oneshot.error()
     sh.oneshot.close()
 
 
