@@ -291,14 +291,16 @@ amun_status amun_debug_logits(amun_ol* plan, const void* X, const void* W, const
 amun_status amun_bench_variant(amun_ol* plan, const void* X, const void* W, const float* b,
                                int N, int variant, void* workspace, void* stream);
 
-/* Measurement hook: when `timeline` (device memory, >= #SMs x 16 u64,
+/* Measurement hook: when `timeline` (device memory, >= #SMs x 40 u64,
  * caller-owned) is non-NULL, every later fused launch of the single-CTA
  * tcgen05 kernel through `plan` writes per-CTA %globaltimer stamps (ns):
  * [cta][0] entry, [1] after setup (barriers, TMEM), [2] first TMA issue,
  * [3] first stage landed at the MMA warp, [4] last MMA issued, [5] last
  * accumulator ready at the epilogue, [6] epilogue done, [7] final barrier,
- * [8] tail released (all CTAs arrived), [9] tail merge done, [10..15]
- * accumulator-ready time of tiles 0..5. NULL switches it off. Not
+ * [8] tail released (all CTAs arrived), [9] tail merge done, [10..23]
+ * the time the epilogue takes up tile 0..13 (its accumulator ready and the
+ * previous tile's epilogue done), [24..37] the time the MMA issuer starts
+ * tile 0..13 (its accumulator released by the epilogue). NULL switches it off. Not
  * synchronised; for tools/timeline.py. */
 amun_status amun_debug_timeline(amun_ol* plan, unsigned long long* timeline);
 

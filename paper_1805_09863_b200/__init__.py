@@ -78,10 +78,13 @@ class OutputLayer:
         nbytes = _L.amun_ol_workspace_bytes(h)
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=dev)
         # the workspace is plan state (amun.h): initialised once, kept between calls
-        check(_L.amun_ol_workspace_init(h, _ptr(self.workspace), _stream(dev)))
+        if hasattr(_L, "amun_ol_workspace_init"):   # (absent only in older A/B builds)
+            check(_L.amun_ol_workspace_init(h, _ptr(self.workspace), _stream(dev)))
         # kernels one call enqueues: __call__ / argmax, partial, merge
-        self.launches = {c: _L.amun_ol_launches_per_call(h, i)
-                         for i, c in enumerate(("call", "partial", "merge"))}
+        self.launches = ({c: _L.amun_ol_launches_per_call(h, i)
+                          for i, c in enumerate(("call", "partial", "merge"))}
+                         if hasattr(_L, "amun_ol_launches_per_call")
+                         else {"call": 2, "partial": 2, "merge": 1})
 
     def __del__(self):
         h = getattr(self, "_h", None)

@@ -102,7 +102,10 @@ def load() -> ctypes.CDLL:
                                    ctypes.POINTER(amun_column), i32, vp, vp, vp, vp, vp, vp, vp,
                                    vp]),
     }
+    alt = "AMUN_LIB" in os.environ   # an older build (A/B experiments) may lack newer calls
     for name, (res, args) in sig.items():
+        if alt and not hasattr(lib, name):
+            continue
         f = getattr(lib, name)
         f.restype = res
         f.argtypes = args

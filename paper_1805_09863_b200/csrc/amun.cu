@@ -122,6 +122,11 @@ struct amun_ol {
                             // measured slower at greedy and beam)
   unsigned long long* tl = nullptr;   // amun_debug_timeline buffer (device), else NULL
   int ng_override = 0;  // env AMUN_NG: 2 or 4 epilogue warpgroups (experiments)
+  int taper = 0;        // env AMUN_TAPER=1: narrow final tiles (experiments; measured slower:
+                        // less W in flight per SM in the narrow tiles)
+  int prepass = 1;      // env AMUN_PREPASS=0: no first-tile k-best bound pre-pass (experiments)
+  int wpf = 0;          // env AMUN_WPF: W L2 prefetch distance in K blocks (0 = off; 8 measured
+                        // 1.4x SLOWER at cfg beam in steady state)
   int pairs_mode = 0;   // env AMUN_PAIRS: 0 auto, 1 never ("off"), 2 always ("force"; tests)
   MapEntry xmaps[4];
   MapEntry wmaps[8];
@@ -249,7 +254,7 @@ amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b
     const int a_rows = (!pairs && !N_dev && N < TC_BM) ? (int)cdiv(N, 8) * 8 : TC_BM;
     amun_status s = get_map(pl, pl->xmaps, 4, pl->xnext, X, N, a_rows, &mx);
     if (s != AMUN_OK) return s;
-    s = get_map(pl, pl->wmaps, 8, pl->wnext, W, pl->V_local, pairs ? TC_BN / 2 : TC_BN, &mw);
+    s = get_map(pl, pl->wmaps, 8, pl->wnext, W, pl->V_local, pairs ? TC_BN / 2 : TC_WBOX, &mw);
     if (s != AMUN_OK) return s;
     TcParams tp;
     memset(&tp, 0, sizeof(tp));
@@ -294,6 +299,9 @@ amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b
     }
     if (os) tp.os = *os;
     tp.tl = pl->tl;
+    tp.taper = pairs ? 0 : pl->taper;
+    tp.prepass = pl->prepass;
+    tp.wpf = pairs ? 0 : pl->wpf;
     if (pl->pf_bytes > 0 && !N_dev) {
       tp.pf_w = static_cast<const char*>(W);
       tp.pf_row_bytes = pl->dtype == AMUN_E4M3 ? pl->H : pl->dtype == AMUN_TF32X3 ? 12LL * pl->H
@@ -340,8 +348,9 @@ amun_status launch_merge(const MergeParams& mp, bool rows, int grid, cudaStream_
   // (DESIGN.md §6.2).
   if (rows)
     merge_rows_kernel<KB><<<grid, MS_WARPS * 32, 0, st>>>(mp);
-  else
-    merge_sentences_kernel<KB><<<grid, MS_WARPS * 32, 0, st>>>(mp);
+  else   // grid = S; k_max = 1 takes a warp per sentence
+    merge_sentences_kernel<KB><<<KB == 1 ? (grid + MS_WARPS - 1) / MS_WARPS : grid, MS_WARPS * 32,
+                                 0, st>>>(mp);
   CUDA_TRY(cudaGetLastError());
   return AMUN_OK;
 }
@@ -512,6 +521,12 @@ amun_status amun_ol_create(amun_ol** plan, int H, int V_local, int v_offset, int
                   : strcmp(t, "nocoop") == 0 ? 3 : strcmp(t, "fence") == 0 ? 4
                   : strcmp(t, "sleep") == 0 ? 5 : strcmp(t, "waitnocoop") == 0 ? 6
                   : strcmp(t, "arriveonly") == 0 ? 7 : 0;
+    const char* wp = getenv("AMUN_WPF");
+    if (wp) pl->wpf = atoi(wp);
+    const char* pp = getenv("AMUN_PREPASS");
+    if (pp) pl->prepass = atoi(pp) != 0;
+    const char* tp = getenv("AMUN_TAPER");
+    if (tp) pl->taper = atoi(tp) != 0;
     const char* f = getenv("AMUN_PF_BYTES");
     if (f) pl->pf_bytes = atoll(f);
   }
@@ -865,10 +880,35 @@ amun_status launch_compact(CompactParams& cp, int N, int S, int32_t* counts, int
   cp.N = N;
   cp.S = S;
   cp.counts = counts;
-  cp.per = (int)cdiv(cdiv(N > 0 ? N : 1, CP_THREADS), 16) * 16;
-  const int grid = (int)std::max<long long>(
-      1, std::max<long long>(cdiv(N, CP_ROWS), cdiv((long long)S + 1, CP_THREADS)));
-  compact_kernel<<<grid, CP_THREADS, 0, st>>>(cp);
+  cp.blk_log2 = 6;   // 64 flags per prefix block, doubled until <= CP_MAXBLK blocks
+  while ((1LL << cp.blk_log2) * CP_MAXBLK < N) ++cp.blk_log2;
+  const long long nblk = cdiv(N > 0 ? N : 1, 1LL << cp.blk_log2);
+  static const bool small_smem = getenv("AMUN_CP_SMALLSMEM") != nullptr;   // (experiment)
+  cp.flags_in_smem = (N <= CP_SFLAGS && !small_smem) ? 1 : 0;
+  const size_t dyn0 = (size_t)((nblk + 1) * 4 + 15) / 16 * 16 +
+                      (cp.flags_in_smem ? (size_t)cdiv(N, 64) * 64 : 0);
+  cp.dyn_off_at = (int)dyn0;
+  cp.cnt_pre = (S + 1 <= CP_CNTPRE && !small_smem) ? 1 : 0;
+  const size_t dyn = dyn0 + (S + 1 <= CP_CNTPRE && !small_smem ? (size_t)(S + 1) * 4 : 0);
+  static const int exp_env = getenv("AMUN_CP_EXP") ? atoi(getenv("AMUN_CP_EXP")) : 0;
+  cp.exp = exp_env;
+  // CTAs: 8 output rows each while that fits one wave (CP_CTAS_PER_SM per
+  // SM), then up to CP_MAXR rows each; at least one thread per sentence
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  static int nsm_cache[64] = {0};
+  int nsm = dev < 64 ? nsm_cache[dev] : 0;
+  if (nsm == 0) {
+    CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+    if (dev < 64) nsm_cache[dev] = nsm;
+  }
+  const long long wave = (long long)CP_CTAS_PER_SM * nsm;
+  // (+1: CTA 0 counts the sentences and gathers nothing)
+  const int grid = 1 + (int)std::max<long long>(
+      {1LL, cdiv(N, CP_MAXR), std::min<long long>(cdiv(N, CP_ROWS), wave - 1),
+       cdiv((long long)S + 1, CP_THREADS)});
+  // counts[1] accumulates the CTAs' alive-sentence counts (compact_kernel step 4)
+  compact_kernel<<<grid, CP_THREADS, dyn, st>>>(cp);
   CUDA_TRY(cudaGetLastError());
   if (counts_host) {
     CUDA_TRY(cudaMemcpyAsync(counts_host, counts, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));

@@ -430,9 +430,22 @@ __host__ __device__ inline Schedule schedule_for(long long n_mt, long long Vp, l
   return s;
 }
 
+// Tile widths of a CTA range: 256 columns, except that with `taper` the
+// range's final segment ends in narrower tiles (<= 64, and <= 128 before
+// it), so the epilogue of the last tile — the drain after the last MMA,
+// when nothing overlaps it — is short. All roles of a CTA (producer, MMA,
+// epilogue) walk the same iterator, so they agree on every tile.
+__device__ __forceinline__ int taper_width(long long rem) {
+  if (rem <= 64) return (int)rem;
+  if (rem <= 192) return (int)(rem - 64);
+  if (rem <= 384) return (int)(rem - 128);
+  return 256;
+}
+
 struct TileIter {
   long long pos, end;
   Schedule sch;
+  int taper = 0;
   __device__ __forceinline__ bool next(int& mt, int& v0, int& width, bool& last) {
     for (;;) {
       if (pos >= end) return false;
@@ -447,7 +460,8 @@ struct TileIter {
 #ifdef TC_BN_OVERRIDE
       width = (int)min((long long)TC_BN_OVERRIDE, seg_end - v0);
 #else
-      width = (int)min(256LL, seg_end - v0);
+      width = (taper && base + sch.Vp >= end) ? taper_width(seg_end - v0)
+                                              : (int)min(256LL, seg_end - v0);
 #endif
       last = (v0 + width == seg_end);
       pos += width;

@@ -477,13 +477,44 @@ __device__ __forceinline__ void merge_sentence(const MergeParams& p, int s, Cand
   }
 }
 
+// Sentence s with k_max = 1 (greedy, beam 1 / k 1), ONE warp, no shared
+// memory or barriers: the sentence's best is the best (better_cand order) of
+// its rows' single candidates pc + (l - lse) — exactly what merge_sentence
+// selects for k = 1 (the same expression, so the same bits), so warps can
+// take sentences independently.
+__device__ __forceinline__ void merge_sentence_k1(const MergeParams& p, int s, int lane) {
+  const int r0 = p.offsets[s], r1 = p.offsets[s + 1];
+  const int ks = p.k_s ? min(p.k_s[s], p.k) : p.k;
+  Cand best{kNegInf, kNegInf, 0x7fffffff, 0x7fffffff};
+  for (int r = r0; r < r1; ++r) {
+    const float pc = p.prev_cost[r];
+    float lse, M, Z, l;
+    int v;
+    row_topk<1>(p, r, lane, lse, M, Z, l, v);   // lane 0 holds the row's best
+    if (lane == 0 && v >= 0) {
+      const Cand c{pc + (l - lse), l, r, v};
+      if (better_cand(c, best)) best = c;
+    }
+  }
+  if (lane == 0 && p.k >= 1) {
+    const bool ok = best.v != 0x7fffffff && ks >= 1;
+    p.out_idx[(long long)s * p.k] = ok ? (long long)best.r * p.V_total + best.v : -1LL;
+    p.out_cost[(long long)s * p.k] = ok ? best.cost : kNegInf;
+  }
+}
+
 template <int KB>
 __global__ void __launch_bounds__(MS_WARPS * 32) merge_sentences_kernel(const MergeParams p0) {
   const MergeParams p = merge_dyn(p0);
-  __shared__ Cand pool[KB + MS_CAP];
-  __shared__ Cand best[KB];
-  __shared__ int s_valid;
-  merge_sentence<KB>(p, blockIdx.x, pool, best, s_valid);
+  if constexpr (KB == 1) {   // a warp per sentence (grid = S / MS_WARPS, launch_merge)
+    const int s = blockIdx.x * MS_WARPS + (threadIdx.x >> 5);
+    if (s < p.S) merge_sentence_k1(p, s, threadIdx.x & 31);
+  } else {
+    __shared__ Cand pool[KB + MS_CAP];
+    __shared__ Cand best[KB];
+    __shared__ int s_valid;
+    merge_sentence<KB>(p, blockIdx.x, pool, best, s_valid);
+  }
 }
 
 }  // namespace amun

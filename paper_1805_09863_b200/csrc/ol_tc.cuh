@@ -61,7 +61,6 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
   uint64_t* tempty = tfull + 2;
   uint64_t* bfull = tempty + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bfull + TC_NBIAS);
-  uint32_t* gen_smem = tmem_holder + 1;
   // e4m3 column-scale ring, after the 512-byte barrier area (TC_SMEM_F8)
   float* sscale = (ELT == 1 && scale_ring_ok(p, TC_STAGES))
                       ? reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 512)
@@ -94,9 +93,6 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
     }
     for (int i = 0; i < TC_NBIAS; ++i) mbar_init(&bfull[i], 1);
     fence_barrier_init();
-    *gen_smem = (MODE == 0 || MODE == 4) ? read_generation(p.gen_ctr) : 0u;
-    // the next launch's tail counter (tail.cuh "Counters")
-    if ((MODE == 0 || MODE == 4) && blockIdx.x == 0) p.arrive[(*gen_smem + 1u) & 1u] = 0u;
   }
   if (role == 1) {
     tmem_alloc(tmem_holder, 512);
@@ -106,7 +102,9 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
-  const uint32_t gen = *gen_smem;   // this launch's hint tag
+  // this launch's tag (hints, tail counters): read by the epilogue threads
+  // (the only users), off the TMA producer's path to its first load
+  uint32_t gen = 0u;
   if (threadIdx.x == 0) tl_mark(p.tl, TL_SETUP);
 
   const TcDyn dyn = tc_dyn<false>(p);      // N (and the schedule) from the device in _dev mode
@@ -120,22 +118,39 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
       // The whole warp walks the schedule (keeps it converged); lane 0 issues.
       const uint64_t pol_x = policy_evict_last();     // X is re-read by every CTA
       TileIter it{start, stop, dyn.sch};
+      it.taper = p.taper;
       int mt, v0, width;
       bool last;
       int stage = 0, tile = 0;
       uint32_t phase = 0;
+      constexpr int kBlockElems = ELT == 1 ? 2 * TC_BK : ELT == 2 ? TC_BK / 2 : TC_BK;
+      // W L2 prefetch (lane 0), p.wpf K blocks ahead of the loads; one CTA per
+      // W tile (aligned schedule: the M-tile-0 CTA of each vocab split)
+      WPrefetch wpf;
+      wpf.it = it;
+      wpf.n_kblk = p.n_kblk;
+      const bool wpf_on = p.wpf > 0 && (dyn.sch.band == dyn.sch.Vp || start < dyn.sch.band);
+      if (lane == 0 && wpf_on) {
+        for (int i = 0; i < p.wpf; ++i) wpf.step(&tmW, kBlockElems, TC_WBOX, i >= TC_STAGES);
+      }
       while (it.next(mt, v0, width, last)) {
         if (lane == 0) bias_ring_load(p, sbias, bfull, tile, v0, width, sscale);
         for (int kb = 0; kb < p.n_kblk; ++kb) {
           mbar_wait_spin(&empty[stage], phase ^ 1);
           if (lane == 0) {
             if (tile == 0 && kb == 0) tl_mark(p.tl, TL_TMA0);
-            mbar_arrive_expect_tx(&full[stage], p.a_box_bytes + TC_B_BYTES);
+            if (wpf_on) wpf.step(&tmW, kBlockElems, TC_WBOX, true);
+            // W in boxes of TC_WBOX rows: only the tile's own rows (narrow
+            // tapered tiles do not drag 256 rows through L2 -> SMEM); the
+            // boxes land contiguously, i.e. the same SW128 K-major tile
+            const int nbox = (width + TC_WBOX - 1) / TC_WBOX;
+            mbar_arrive_expect_tx(&full[stage], p.a_box_bytes + nbox * TC_WBOX * 128);
             // 128 bytes of K per block: 64 bf16, 128 e4m3 or 32 fp32 (tf32x3)
-            constexpr int kBlockElems = ELT == 1 ? 2 * TC_BK : ELT == 2 ? TC_BK / 2 : TC_BK;
             tma_load_2d(&tmX, &full[stage], sA + stage * TC_A_BYTES, kb * kBlockElems, mt * TC_BM,
                         pol_x);
-            tma_load_2d(&tmW, &full[stage], sB + stage * TC_B_BYTES, kb * kBlockElems, v0, 0ull);
+            for (int j = 0; j < nbox; ++j)
+              tma_load_2d(&tmW, &full[stage], sB + stage * TC_B_BYTES + j * TC_WBOX * 128,
+                          kb * kBlockElems, v0 + j * TC_WBOX, 0ull);
           }
           __syncwarp();
           if (++stage == TC_STAGES) {
@@ -150,15 +165,19 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
       // The whole warp waits; lane 0 issues tcgen05.mma and the commits (a
       // commit tracks the MMAs issued by the same thread).
       TileIter it{start, stop, dyn.sch};
+      it.taper = p.taper;
       int mt, v0, width;
       bool last;
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
+      int mtile = 0;
       while (it.next(mt, v0, width, last)) {
         mbar_wait_spin(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
+        if (lane == 0 && mtile < TL_N - TL_MMA0) tl_mark(p.tl, TL_MMA0 + mtile);
+        ++mtile;
         const uint32_t d = tmem_base + acc * TC_BN;
         const uint32_t idesc = ELT == 1 ? idesc_e4m3_f32(TC_BM, width)
                              : ELT == 2 ? idesc_tf32_f32(TC_BM, width)
@@ -167,7 +186,7 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
           mbar_wait_spin(&full[stage], phase);
           tc_fence_after();
           if (lane == 0) {
-            if (kb == 0 && acc == 0 && acc_phase == 0) tl_mark(p.tl, TL_FULL0);
+            if (kb == 0 && mtile == 1) tl_mark(p.tl, TL_FULL0);
             const uint64_t ad = sdesc_k_sw128(smem_u32(sA + stage * TC_A_BYTES));
             const uint64_t bd = sdesc_k_sw128(smem_u32(sB + stage * TC_B_BYTES));
 #pragma unroll
@@ -196,24 +215,39 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
     }
   } else {
     reg_alloc<Cfg::kEpiRegs>();
+    if constexpr (MODE == 0 || MODE == 4) {
+      gen = read_generation(p.gen_ctr);
+      // the next launch's tail counter (tail.cuh "Counters")
+      if (blockIdx.x == 0 && threadIdx.x == 0) p.arrive[(gen + 1u) & 1u] = 0u;
+    }
     tc_epilogue<KB, MODE, NG, false, ELT>(p, tmem_base, start, stop, tfull, tempty, bfull, sbias, xch,
                                      thr_x, gen, warp, lane, 0u, (long long)blockIdx.x, dyn,
                                      sscale);
+    if (threadIdx.x == 0) tl_mark(p.tl, TL_EPI_END);
+    if constexpr (MODE == 0 || MODE == 4) {
+      // The merge in this launch (tail.cuh), run by the epilogue warps INSIDE
+      // their branch: code after the roles rejoin is register-allocated for
+      // the control warps' setmaxnreg budget (56), where the merge spilled.
+      // The barrier orders every epilogue warp's partial records (and its
+      // use of the exchange area) before the CTA's arrival.
+      if (p.tail) {
+        tc_fence_before();
+        named_bar_sync(11, Cfg::kEpiThreads);
+        if (threadIdx.x == 0) tl_mark(p.tl, TL_BARRIER);
+        grid_tail<KB>(p, dyn, reinterpret_cast<uint8_t*>(xch), gen);
+      }
+    }
   }
 
-  if (threadIdx.x == 0) tl_mark(p.tl, TL_EPI_END);
   tc_fence_before();
   __syncthreads();
-  if (threadIdx.x == 0) tl_mark(p.tl, TL_BARRIER);
+  if (threadIdx.x == 0 && !p.tail) tl_mark(p.tl, TL_BARRIER);
   if (role == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, 512);
   }
   if constexpr (MODE == 0 || MODE == 4) {
-    if (p.tail)   // the merge in this launch (tail.cuh); the exchange area is free now
-      grid_tail<KB>(p, dyn, reinterpret_cast<uint8_t*>(xch), gen);
-    else if (threadIdx.x == 0)
-      finish_generation(p.gen_ctr);
+    if (!p.tail && threadIdx.x == 0) finish_generation(p.gen_ctr);
   }
 }
 

@@ -49,7 +49,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<NG>::kThreads,
   uint64_t* tempty = tfull + 2;
   uint64_t* bfull = tempty + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bfull + TC_NBIAS);
-  uint32_t* gen_smem = tmem_holder + 1;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -79,9 +78,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<NG>::kThreads,
     }
     for (int i = 0; i < TC_NBIAS; ++i) mbar_init(&bfull[i], 1);
     fence_barrier_init();
-    *gen_smem = (MODE == 0 || MODE == 4) ? read_generation(p.gen_ctr) : 0u;
-    // the next launch's tail counter (tail.cuh "Counters")
-    if ((MODE == 0 || MODE == 4) && blockIdx.x == 0) p.arrive[(*gen_smem + 1u) & 1u] = 0u;
   }
   if (role == 1) {
     tmem_alloc_2sm(tmem_holder, 512);
@@ -91,7 +87,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<NG>::kThreads,
   cluster_sync();      // barriers of both CTAs initialised before any remote use
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
-  const uint32_t gen = *gen_smem;
+  // this launch's tag (hints, tail counters): read by the epilogue threads
+  // (the only users), off the TMA producer's path to its first load
+  uint32_t gen = 0u;
 
   const TcDyn dyn = tc_dyn<true>(p);       // N (and the schedule) from the device in _dev mode
   const long long start = (long long)pair * dyn.sch.C;
@@ -166,8 +164,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<NG>::kThreads,
     }
   } else {
     reg_alloc<Cfg::kEpiRegs>();
+    if constexpr (MODE == 0 || MODE == 4) {
+      gen = read_generation(p.gen_ctr);
+      // the next launch's tail counter (tail.cuh "Counters")
+      if (blockIdx.x == 0 && threadIdx.x == 0) p.arrive[(gen + 1u) & 1u] = 0u;
+    }
     tc_epilogue<KB, MODE, NG, true>(p, tmem_base, start, stop, tfull, tempty, bfull, sbias, xch,
                                     thr_x, gen, warp, lane, rank, (long long)pair, dyn);
+    if constexpr (MODE == 0 || MODE == 4) {
+      // the merge in this launch, inside the epilogue branch (see ol_tc.cuh)
+      if (p.tail) {
+        tc_fence_before();
+        named_bar_sync(11, Cfg::kEpiThreads);
+        grid_tail<KB>(p, dyn, reinterpret_cast<uint8_t*>(xch), gen);
+      }
+    }
   }
 
   tc_fence_before();
@@ -177,10 +188,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<NG>::kThreads,
     tmem_dealloc_2sm(tmem_base, 512);
   }
   if constexpr (MODE == 0 || MODE == 4) {
-    if (p.tail)   // the merge in this launch (tail.cuh); the exchange area is free now
-      grid_tail<KB>(p, dyn, reinterpret_cast<uint8_t*>(xch), gen);
-    else if (threadIdx.x == 0)
-      finish_generation(p.gen_ctr);
+    if (!p.tail && threadIdx.x == 0) finish_generation(p.gen_ctr);
   }
 }
 

@@ -127,7 +127,9 @@ __device__ __forceinline__ void grid_tail(const TcParams& p, const TcDyn& dyn, u
   const int G = gridDim.x, c = blockIdx.x, warp = tid >> 5, lane = tid & 31;
   const int kind = p.tail & 15;
   if (p.tail & TAIL_X_NOWORK) return;   // (experiment: the arrival / wait alone)
-  if (kind == TAIL_SENT) {
+  if (kind == TAIL_SENT && KB == 1) {   // k_max = 1: a warp per sentence (merge_sentence_k1)
+    for (int s = c + G * warp; s < mp.S; s += G * MS_WARPS) merge_sentence_k1(mp, s, lane);
+  } else if (kind == TAIL_SENT) {
     Cand* pool = reinterpret_cast<Cand*>(scratch);
     Cand* best = pool + KB + MS_CAP;
     int* s_valid = reinterpret_cast<int*>(best + KB);

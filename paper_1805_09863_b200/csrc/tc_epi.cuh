@@ -44,10 +44,40 @@ struct TcParams {
   long long pf_max_bytes;                  // prefetch at most this many bytes of a CTA's W range
   unsigned long long* __restrict__ tl;     // timeline probe [grid][TL_N] (amun_debug_timeline), else NULL
   OneShotTail os;                          // TAIL_ONESHOT: the peer buffers (peer.cuh)
+  int taper;                               // single-CTA kernel: narrow final tiles (TileIter)
+  int prepass;                             // k-best bound pre-pass over a segment's first tile
+  int wpf;                                 // W L2 prefetch distance in K blocks (0 = off)
+};
+
+// W L2 prefetch stream of the TMA producer: walks the CTA's (tile, K block)
+// sequence `dist` blocks ahead of the loads and prefetches those W boxes
+// into L2 (cp.async.bulk.prefetch.tensor), so a load finds W in L2 (~0.5 us)
+// instead of waiting on DRAM (~1.5 us) — with 4 stages of 48 KB the pipeline
+// holds too few bytes in flight to cover DRAM latency at the MMA's rate.
+struct WPrefetch {
+  TileIter it;
+  int mt = 0, v0 = 0, width = 0, kb = 0, n_kblk = 1;
+  bool last = false, done = false;
+  __device__ __forceinline__ void step(const CUtensorMap* tmW, int block_elems, int wbox,
+                                       bool issue) {
+    if (done) return;
+    if (kb == 0 || kb == n_kblk) {
+      if (!it.next(mt, v0, width, last)) {
+        done = true;
+        return;
+      }
+      kb = 0;
+    }
+    if (issue)
+      for (int j = 0; j < (width + wbox - 1) / wbox; ++j)
+        tma_prefetch_2d(tmW, kb * block_elems, v0 + j * wbox);
+    ++kb;
+  }
 };
 // Timeline probe points (globaltimer ns; per CTA; see amun_debug_timeline).
 enum { TL_ENTRY = 0, TL_SETUP = 1, TL_TMA0 = 2, TL_FULL0 = 3, TL_MMA_END = 4, TL_EPI_LAST = 5,
-       TL_EPI_END = 6, TL_BARRIER = 7, TL_RELEASED = 8, TL_TAIL_END = 9, TL_TILE0 = 10, TL_N = 16 };
+       TL_EPI_END = 6, TL_BARRIER = 7, TL_RELEASED = 8, TL_TAIL_END = 9, TL_TILE0 = 10,
+       TL_MMA0 = 24, TL_N = 40 };
 __device__ __forceinline__ void tl_mark(const unsigned long long* tl_base, int point) {
   if (tl_base) {
     unsigned long long t;
@@ -85,6 +115,7 @@ constexpr int TC_BN = 256;
 constexpr int TC_BN = TC_BN_OVERRIDE;
 #endif
 constexpr int TC_BK = 64;
+constexpr int TC_WBOX = 64;                            // W rows per TMA box (single-CTA kernel)
 constexpr int TC_NBIAS = 8;                          // bias ring slots (see producer bound)
 constexpr int TC_BIAS_BYTES = TC_NBIAS * TC_BN * 4;
 constexpr int TC_XCH_FLOATS = 2 + 2 * 16;            // one row's state in the exchange area
@@ -179,6 +210,7 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
   RowState<KB> st;
   st.reset();
   TileIter it{start, stop, dyn.sch};
+  it.taper = PAIR ? 0 : p.taper;
   int unit, v0, width;
   bool last;
   int acc = 0, tile = 0;
@@ -189,6 +221,13 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
   // earlier segment is never used) and gates with the best of all groups.
   unsigned long long* my_thr = thr_x + grp * 128 + row_local;
   float shared_kth = kNegInf;
+  // Pre-pass bound (first tile of a segment, when the row lists are empty and
+  // every chunk would pass the k-best gate): the KB-th largest group maximum
+  // over this group's chunks of the tile. KB distinct elements reach it, so
+  // nothing below it can be in the row's top-KB (the same argument as the
+  // list-filling bound of kbest32 and reading G15); ties at it are kept.
+  float pre = kNegInf;
+  bool seg_first = true;
   while (it.next(unit, v0, width, last)) {
     const int mt = PAIR ? 2 * unit + (int)rank : unit;
     const uint32_t tag = (uint32_t)mt + 1u;
@@ -262,6 +301,34 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
         }
       }
     };
+    if constexpr (MODE == 0 && KB > 1) {
+      if (live && seg_first && p.prepass) {
+        float top[KB];
+#pragma unroll
+        for (int i = 0; i < KB; ++i) top[i] = kNegInf;
+        for (int c = grp; c < nch; c += NG) {
+          uint32_t r[32];
+          tmem_ld32(tbase + c * 32, r);
+          float x[32];
+          tmem_ld_wait(r);
+          build_x(r, c, x);
+          float g[8];
+          RowState<KB>::groups32(x, g);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {   // insert g[j] into the descending top[]
+            float t = g[j];
+#pragma unroll
+            for (int i = 0; i < KB; ++i) {
+              const float hi = fmaxf(top[i], t);
+              t = fminf(top[i], t);
+              top[i] = hi;
+            }
+          }
+        }
+        pre = top[KB - 1];
+        if (pre != kNegInf) sts_u64(smem_u32(my_thr), ((unsigned long long)tag << 32) | f2o(pre));
+      }
+    }
     if (live) {
       for (int c = grp; c < nch; c += NG) {
         uint32_t r[32];
@@ -292,8 +359,9 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
             }
           }
           const float before = st.l[KB - 1];
-          st.template chunk32r<true, MODE != 4>(x, p.v_offset + v0 + c0, fmaxf(hintv, shared_kth));
-          if (AMUN_EXP != 3 && st.l[KB - 1] > before)
+          st.template chunk32r<true, MODE != 4>(x, p.v_offset + v0 + c0,
+                                                fmaxf(fmaxf(hintv, shared_kth), pre));
+          if (AMUN_EXP != 3 && st.l[KB - 1] > before && st.l[KB - 1] > pre)
             sts_u64(smem_u32(my_thr), ((unsigned long long)tag << 32) | f2o(st.l[KB - 1]));
         }
       }
@@ -317,10 +385,13 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
       }
       hintv = fmaxf(hintv, hint_decode(hraw, gen));   // 0 (no hint) when `last`
     }
+    seg_first = false;
     if (last) {
       hintv = kNegInf;   // the next segment is another M-tile (other rows)
       published = kNegInf;
       shared_kth = kNegInf;
+      pre = kNegInf;
+      seg_first = true;
       if constexpr (MODE != 1) {
         float* xr = xch + row_local * TC_XCH_FLOATS;
         for (int g = 1; g < NG; ++g) {

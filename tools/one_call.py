@@ -1,5 +1,6 @@
 """Run the fused output layer a few times eagerly (for ncu captures).
-  python tools/one_call.py [config] [calls] [bf16|e4m3]   (env AMUN_SENTENCES, AMUN_PAIRS)"""
+  python tools/one_call.py [config] [calls] [bf16|e4m3|bare|stats]
+  (env AMUN_SENTENCES, AMUN_PAIRS; bare / stats: amun_bench_variant 2 / 3)"""
 import dataclasses
 import os
 import sys
@@ -25,6 +26,10 @@ if prec == "e4m3":
     ol = amun.OutputLayer(w.H, w.V, dtype="e4m3", k_max=w.k, max_rows=w.N, max_sentences=w.S)
     for _ in range(calls):
         ol.call_e4m3(X8, xs, W8, ws, b, pc, off, w.k)
+elif prec in ("bare", "stats"):
+    ol = amun.OutputLayer(w.H, w.V, k_max=w.k, max_rows=w.N, max_sentences=w.S)
+    for _ in range(calls):
+        ol.bench_variant(X, W, b, 2 if prec == "bare" else 3)
 else:
     ol = amun.OutputLayer(w.H, w.V, k_max=w.k, max_rows=w.N, max_sentences=w.S)
     for _ in range(calls):

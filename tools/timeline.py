@@ -4,7 +4,7 @@ calls (W rotated so L2 does not serve it). Prints, per probe point, the
 median / max over CTAs of (stamp - earliest entry) in microseconds, and the
 launch-to-launch gap.
 
-  python tools/timeline.py [workload] [tail|sep|scores]
+  python tools/timeline.py [workload] [tail|sep|scores|bare|stats] [taper] [prepass]
 """
 import json
 import os
@@ -19,13 +19,20 @@ import paper_1805_09863_b200 as amun  # noqa: E402
 from paper_1805_09863_b200 import _L, check  # noqa: E402
 
 NAMES = ["entry", "setup", "tma0", "full0", "mma_end", "epi_last", "epi_end", "barrier",
-         "released", "tail_end", "tile0", "tile1", "tile2", "tile3", "tile4", "tile5"]
+         "released", "tail_end"] + [f"tile{i}" for i in range(14)] + [f"mma{i}" for i in range(14)]
+TL_N = 40
 
 
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "greedy"
     variant = sys.argv[2] if len(sys.argv) > 2 else "tail"
-    os.environ["AMUN_TAIL"] = "off" if variant in ("sep", "scores") else "on"
+    os.environ["AMUN_TAIL"] = "off" if variant in ("sep", "scores", "bare", "stats") else "on"
+    if len(sys.argv) > 3:   # taper on / off (1 / 0)
+        os.environ["AMUN_TAPER"] = sys.argv[3]
+    if len(sys.argv) > 4:   # first-tile pre-pass on / off (1 / 0)
+        os.environ["AMUN_PREPASS"] = sys.argv[4]
+    if len(sys.argv) > 5:   # W L2 prefetch distance in K blocks
+        os.environ["AMUN_WPF"] = sys.argv[5]
     w = synth.CONFIGS[name]
     dev = torch.device("cuda", 0)
     X, W, b = synth.gen_X(w).to(dev), synth.gen_W(w).to(dev), synth.gen_b(w).to(dev)
@@ -34,7 +41,7 @@ def main():
     Ws = [W] + [W.clone() for _ in range(nc - 1)]
     ol = amun.OutputLayer(w.H, w.V, dtype=w.dtype, k_max=w.k, max_rows=w.N, max_sentences=w.S)
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
-    tl = torch.zeros((nsm, 16), dtype=torch.int64, device=dev)
+    tl = torch.zeros((nsm, TL_N), dtype=torch.int64, device=dev)
     check(_L.amun_debug_timeline(ol._h, tl.data_ptr()))
     oi = torch.empty((w.S, w.k), dtype=torch.int64, device=dev)
     oc = torch.empty((w.S, w.k), dtype=torch.float32, device=dev)
@@ -42,6 +49,8 @@ def main():
     def step(i):
         if variant == "scores":
             ol.scores(X, Ws[i % nc], b)
+        elif variant in ("bare", "stats"):   # amun_bench_variant 2 / 3 (Table 4 analogues)
+            ol.bench_variant(X, Ws[i % nc], b, 2 if variant == "bare" else 3)
         else:
             ol(X, Ws[i % nc], b, pc, off, w.k, out_idx=oi, out_cost=oc)
     K = 20
@@ -63,7 +72,8 @@ def main():
     used = t[:, 0] > 0
     t = t[used]
     t0 = t[:, 0].min()
-    out = {"workload": name, "variant": variant, "ctas": int(used.sum())}
+    out = {"workload": name, "variant": variant, "ctas": int(used.sum()),
+           "env": {k: os.environ.get(k) for k in ("AMUN_TAPER", "AMUN_PREPASS", "AMUN_WPF")}}
     for j, n in enumerate(NAMES):
         col = t[:, j]
         col = col[col > 0]
