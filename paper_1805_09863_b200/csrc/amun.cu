@@ -83,6 +83,7 @@ struct MapEntry {
   const void* ptr = nullptr;
   long long rows = -1;
   int box_rows = 0;
+  int kbytes = 0;
   CUtensorMap map;
 };
 
@@ -125,8 +126,7 @@ struct amun_ol {
   int taper = 0;        // env AMUN_TAPER=1: narrow final tiles (experiments; measured slower:
                         // less W in flight per SM in the narrow tiles)
   int prepass = 1;      // env AMUN_PREPASS=0: no first-tile k-best bound pre-pass (experiments)
-  int wpf = 0;          // env AMUN_WPF: W L2 prefetch distance in K blocks (0 = off; 8 measured
-                        // 1.4x SLOWER at cfg beam in steady state)
+  int wbox = 256;       // env AMUN_WBOX: W rows per TMA box, 256 or 64 (64 for tapered tiles)
   int pairs_mode = 0;   // env AMUN_PAIRS: 0 auto, 1 never ("off"), 2 always ("force"; tests)
   MapEntry xmaps[4];
   MapEntry wmaps[8];
@@ -137,37 +137,41 @@ namespace {
 
 // Tensor map of a row-major [rows, H] bf16 matrix, box [box_rows, 64],
 // 128-byte swizzle (matches sdesc_k_sw128), OOB rows/columns read as zero.
-amun_status encode_map(amun_ol* pl, const void* ptr, long long rows, int box_rows,
+amun_status encode_map(amun_ol* pl, const void* ptr, long long rows, int box_rows, int kbytes,
                        CUtensorMap* out) {
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return fail(AMUN_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
-  // 128-byte box rows: 64 bf16, 128 e4m3 codes, or 32 fp32 of the 3H-wide tf32x3 rows
+  // box rows of `kbytes` bytes (128: 64 bf16, 128 e4m3 codes or 32 fp32 of the
+  // 3H-wide tf32x3 rows; 64: half of that), swizzled to match sdesc_k<kbytes>
   const bool f8 = pl->dtype == AMUN_E4M3, t3 = pl->dtype == AMUN_TF32X3;
   const cuuint64_t K = t3 ? 3ull * pl->H : (cuuint64_t)pl->H;
+  const cuuint32_t esz = f8 ? 1 : t3 ? 4 : 2;
   cuuint64_t dims[2] = {K, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {K * (f8 ? 1 : t3 ? 4 : 2)};
-  cuuint32_t box[2] = {f8 ? 128u : t3 ? 32u : 64u, (cuuint32_t)box_rows};
+  cuuint64_t strides[1] = {K * esz};
+  cuuint32_t box[2] = {(cuuint32_t)kbytes / esz, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(out,
                    f8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
                       : t3 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
                    2, const_cast<void*>(ptr), dims, strides,
-                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   kbytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(AMUN_ECUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return AMUN_OK;
 }
 
 amun_status get_map(amun_ol* pl, MapEntry* cache, int n, int& next, const void* ptr,
-                    long long rows, int box_rows, const CUtensorMap** out) {
+                    long long rows, int box_rows, int kbytes, const CUtensorMap** out) {
   for (int i = 0; i < n; ++i)
-    if (cache[i].ptr == ptr && cache[i].rows == rows && cache[i].box_rows == box_rows) {
+    if (cache[i].ptr == ptr && cache[i].rows == rows && cache[i].box_rows == box_rows &&
+        cache[i].kbytes == kbytes) {
       *out = &cache[i].map;
       return AMUN_OK;
     }
   MapEntry& e = cache[next];
   next = (next + 1) % n;
-  amun_status s = encode_map(pl, ptr, rows, box_rows, &e.map);
+  amun_status s = encode_map(pl, ptr, rows, box_rows, kbytes, &e.map);
   if (s != AMUN_OK) {
     e.ptr = nullptr;
     return s;
@@ -175,6 +179,7 @@ amun_status get_map(amun_ol* pl, MapEntry* cache, int n, int& next, const void* 
   e.ptr = ptr;
   e.rows = rows;
   e.box_rows = box_rows;
+  e.kbytes = kbytes;
   *out = &e.map;
   return AMUN_OK;
 }
@@ -252,21 +257,25 @@ amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b
     // (cfg beam at S = 1: 59 vs 53 us per call); the MMA still reads the full
     // 128-row A tile, whose extra rows only feed accumulator rows >= N.
     const int a_rows = (!pairs && !N_dev && N < TC_BM) ? (int)cdiv(N, 8) * 8 : TC_BM;
-    amun_status s = get_map(pl, pl->xmaps, 4, pl->xnext, X, N, a_rows, &mx);
+    // bytes of K per pipeline block: the pair kernel 128 (SW128), the
+    // single-CTA kernel TC_KBYTES (ol_tc.cuh)
+    const int kbytes = pairs ? 128 : TC_KBYTES;
+    amun_status s = get_map(pl, pl->xmaps, 4, pl->xnext, X, N, a_rows, kbytes, &mx);
     if (s != AMUN_OK) return s;
-    s = get_map(pl, pl->wmaps, 8, pl->wnext, W, pl->V_local, pairs ? TC_BN / 2 : TC_WBOX, &mw);
+    s = get_map(pl, pl->wmaps, 8, pl->wnext, W, pl->V_local, pairs ? TC_BN / 2 : pl->wbox, kbytes,
+                &mw);
     if (s != AMUN_OK) return s;
     TcParams tp;
     memset(&tp, 0, sizeof(tp));
     tp.N = N;
     tp.V_local = pl->V_local;
     tp.v_offset = pl->v_offset;
-    tp.n_kblk = (int)(pl->dtype == AMUN_E4M3 ? cdiv(pl->H, 2 * TC_BK)
-                      : pl->dtype == AMUN_TF32X3 ? cdiv(3LL * pl->H, TC_BK / 2)
-                                                 : cdiv(pl->H, TC_BK));
+    const long long kbytes_total = pl->dtype == AMUN_E4M3 ? pl->H
+                                 : pl->dtype == AMUN_TF32X3 ? 12LL * pl->H : 2LL * pl->H;
+    tp.n_kblk = (int)cdiv(kbytes_total, kbytes);
     tp.x_scale = x_scale;
     tp.w_scale = w_scale;
-    tp.a_box_bytes = a_rows * 128;   // 128 bytes of K per row (bf16 and e4m3 alike)
+    tp.a_box_bytes = a_rows * kbytes;   // kbytes of K per row (every dtype)
     tp.sch = sch;
     tp.bias = b;
     tp.part = static_cast<float*>(workspace);
@@ -301,7 +310,7 @@ amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b
     tp.tl = pl->tl;
     tp.taper = pairs ? 0 : pl->taper;
     tp.prepass = pl->prepass;
-    tp.wpf = pairs ? 0 : pl->wpf;
+    tp.wbox = pl->wbox;
     if (pl->pf_bytes > 0 && !N_dev) {
       tp.pf_w = static_cast<const char*>(W);
       tp.pf_row_bytes = pl->dtype == AMUN_E4M3 ? pl->H : pl->dtype == AMUN_TF32X3 ? 12LL * pl->H
@@ -521,12 +530,13 @@ amun_status amun_ol_create(amun_ol** plan, int H, int V_local, int v_offset, int
                   : strcmp(t, "nocoop") == 0 ? 3 : strcmp(t, "fence") == 0 ? 4
                   : strcmp(t, "sleep") == 0 ? 5 : strcmp(t, "waitnocoop") == 0 ? 6
                   : strcmp(t, "arriveonly") == 0 ? 7 : 0;
-    const char* wp = getenv("AMUN_WPF");
-    if (wp) pl->wpf = atoi(wp);
+    const char* wb = getenv("AMUN_WBOX");
+    if (wb) pl->wbox = atoi(wb) == 64 ? 64 : 256;
     const char* pp = getenv("AMUN_PREPASS");
     if (pp) pl->prepass = atoi(pp) != 0;
     const char* tp = getenv("AMUN_TAPER");
     if (tp) pl->taper = atoi(tp) != 0;
+    if (pl->taper) pl->wbox = 64;   // narrow tiles load only their own rows
     const char* f = getenv("AMUN_PF_BYTES");
     if (f) pl->pf_bytes = atoll(f);
   }

@@ -23,13 +23,20 @@
 
 namespace amun {
 
+// Pipeline geometry of the single-CTA kernel: stages of TC_KBYTES bytes of
+// K per row (128: SWIZZLE_128B, 4 stages of 16 KB A + 32 KB B; 64:
+// SWIZZLE_64B, 8 stages of 8 + 16 KB). The same 192 KB of stages; 64-byte
+// blocks keep 7 of 8 stages in flight instead of 3 of 4 but measured 1.3x
+// SLOWER per tile (9.2-9.9 vs 7.0 us at cfg beam, tools/timeline.py): twice
+// the barrier round trips and MMA issues per byte. An L2-resident W (V =
+// 45k, one copy) runs at the same 7.0 us per tile, so DRAM is not the bound.
 #ifdef TC_STAGES_OVERRIDE
 constexpr int TC_STAGES = TC_STAGES_OVERRIDE;
 #else
-constexpr int TC_STAGES = 4;
+constexpr int TC_STAGES = TC_KBYTES == 64 ? 8 : 4;
 #endif
-constexpr int TC_A_BYTES = TC_BM * TC_BK * 2;   // 16 KB
-constexpr int TC_B_BYTES = TC_BN * TC_BK * 2;   // 32 KB
+constexpr int TC_A_BYTES = TC_BM * TC_KBYTES;   // 8 KB (16 KB)
+constexpr int TC_B_BYTES = TC_BN * TC_KBYTES;   // 16 KB (32 KB)
 constexpr int TC_SMEM = TC_STAGES * (TC_A_BYTES + TC_B_BYTES) + TC_BIAS_BYTES + TC_XCH_BYTES +
                         TC_THRX_BYTES + 1024 /*align*/ + 512 /*barriers*/;
 constexpr int TC_SMEM_F8 = TC_SMEM + TC_SCALE_BYTES;   // + the e4m3 column-scale ring
@@ -55,7 +62,7 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
   float* sbias = reinterpret_cast<float*>(sB + TC_STAGES * TC_B_BYTES);
   float* xch = sbias + TC_NBIAS * TC_BN;
   unsigned long long* thr_x = reinterpret_cast<unsigned long long*>(xch + 128 * TC_XCH_FLOATS);
-  uint64_t* full = reinterpret_cast<uint64_t*>(thr_x + 4 * 128);
+  uint64_t* full = reinterpret_cast<uint64_t*>(thr_x + TC_THRX_BYTES / 8);
   uint64_t* empty = full + TC_STAGES;
   uint64_t* tfull = empty + TC_STAGES;
   uint64_t* tempty = tfull + 2;
@@ -79,7 +86,8 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
   if (role == 0 && lane == 0 && !p.N_dev)   // W to L2 before the prologue (tail.cuh)
     entry_prefetch_w(p, (long long)blockIdx.x * p.sch.C,
                      min((long long)(blockIdx.x + 1) * p.sch.C, p.sch.total), p.sch);
-  for (int i = threadIdx.x; i < 4 * 128; i += blockDim.x) sts_u64(smem_u32(thr_x + i), 0ull);   // no stale tags
+  for (int i = threadIdx.x; i < TC_THRX_BYTES / 8; i += blockDim.x)   // no stale tags
+    sts_u64(smem_u32(thr_x + i), 0ull);
   if (role == 0 && lane == 0) {
     prefetch_tmap(&tmX);
     prefetch_tmap(&tmW);
@@ -123,34 +131,25 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
       bool last;
       int stage = 0, tile = 0;
       uint32_t phase = 0;
-      constexpr int kBlockElems = ELT == 1 ? 2 * TC_BK : ELT == 2 ? TC_BK / 2 : TC_BK;
-      // W L2 prefetch (lane 0), p.wpf K blocks ahead of the loads; one CTA per
-      // W tile (aligned schedule: the M-tile-0 CTA of each vocab split)
-      WPrefetch wpf;
-      wpf.it = it;
-      wpf.n_kblk = p.n_kblk;
-      const bool wpf_on = p.wpf > 0 && (dyn.sch.band == dyn.sch.Vp || start < dyn.sch.band);
-      if (lane == 0 && wpf_on) {
-        for (int i = 0; i < p.wpf; ++i) wpf.step(&tmW, kBlockElems, TC_WBOX, i >= TC_STAGES);
-      }
+      // TC_KBYTES of K per block: bf16 / e4m3 / fp32 (tf32x3) elements
+      constexpr int kBlockElems = ELT == 1 ? TC_KBYTES : ELT == 2 ? TC_KBYTES / 4 : TC_KBYTES / 2;
       while (it.next(mt, v0, width, last)) {
         if (lane == 0) bias_ring_load(p, sbias, bfull, tile, v0, width, sscale);
         for (int kb = 0; kb < p.n_kblk; ++kb) {
           mbar_wait_spin(&empty[stage], phase ^ 1);
           if (lane == 0) {
             if (tile == 0 && kb == 0) tl_mark(p.tl, TL_TMA0);
-            if (wpf_on) wpf.step(&tmW, kBlockElems, TC_WBOX, true);
-            // W in boxes of TC_WBOX rows: only the tile's own rows (narrow
-            // tapered tiles do not drag 256 rows through L2 -> SMEM); the
-            // boxes land contiguously, i.e. the same SW128 K-major tile
-            const int nbox = (width + TC_WBOX - 1) / TC_WBOX;
-            mbar_arrive_expect_tx(&full[stage], p.a_box_bytes + nbox * TC_WBOX * 128);
-            // 128 bytes of K per block: 64 bf16, 128 e4m3 or 32 fp32 (tf32x3)
+            // W in boxes of p.wbox rows (256, or 64 so narrow tapered tiles
+            // do not drag 256 rows through L2 -> SMEM); the boxes land
+            // contiguously, i.e. the same SW128 K-major tile
+            const int wbox = p.wbox;
+            const int nbox = (width + wbox - 1) / wbox;
+            mbar_arrive_expect_tx(&full[stage], p.a_box_bytes + nbox * wbox * TC_KBYTES);
             tma_load_2d(&tmX, &full[stage], sA + stage * TC_A_BYTES, kb * kBlockElems, mt * TC_BM,
                         pol_x);
             for (int j = 0; j < nbox; ++j)
-              tma_load_2d(&tmW, &full[stage], sB + stage * TC_B_BYTES + j * TC_WBOX * 128,
-                          kb * kBlockElems, v0 + j * TC_WBOX, 0ull);
+              tma_load_2d(&tmW, &full[stage], sB + stage * TC_B_BYTES + j * wbox * TC_KBYTES,
+                          kb * kBlockElems, v0 + j * wbox, 0ull);
           }
           __syncwarp();
           if (++stage == TC_STAGES) {
@@ -187,10 +186,10 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
           tc_fence_after();
           if (lane == 0) {
             if (kb == 0 && mtile == 1) tl_mark(p.tl, TL_FULL0);
-            const uint64_t ad = sdesc_k_sw128(smem_u32(sA + stage * TC_A_BYTES));
-            const uint64_t bd = sdesc_k_sw128(smem_u32(sB + stage * TC_B_BYTES));
+            const uint64_t ad = sdesc_k<TC_KBYTES>(smem_u32(sA + stage * TC_A_BYTES));
+            const uint64_t bd = sdesc_k<TC_KBYTES>(smem_u32(sB + stage * TC_B_BYTES));
 #pragma unroll
-            for (int k = 0; k < TC_BK / 16; ++k) {   // +32 bytes of K per MMA (>>4 = 2)
+            for (int k = 0; k < TC_KBYTES / 32; ++k) {   // +32 bytes of K per MMA (>>4 = 2)
               if constexpr (ELT == 0)
                 mma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
               else if constexpr (ELT == 1)

@@ -43,7 +43,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<NG>::kThreads,
   float* sbias = reinterpret_cast<float*>(sB + TC2_STAGES * TC2_B_BYTES);
   float* xch = sbias + TC_NBIAS * TC_BN;
   unsigned long long* thr_x = reinterpret_cast<unsigned long long*>(xch + 128 * TC_XCH_FLOATS);
-  uint64_t* full = reinterpret_cast<uint64_t*>(thr_x + 4 * 128);
+  uint64_t* full = reinterpret_cast<uint64_t*>(thr_x + TC_THRX_BYTES / 8);
   uint64_t* empty = full + TC2_STAGES;
   uint64_t* tfull = empty + TC2_STAGES;
   uint64_t* tempty = tfull + 2;
@@ -64,7 +64,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<NG>::kThreads,
   if (role == 0 && lane == 0 && rank == 0 && !p.N_dev)   // W to L2 before the prologue (tail.cuh)
     entry_prefetch_w(p, (long long)pair * p.sch.C,
                      min((long long)(pair + 1) * p.sch.C, p.sch.total), p.sch);
-  for (int i = threadIdx.x; i < 4 * 128; i += blockDim.x) sts_u64(smem_u32(thr_x + i), 0ull);   // no stale tags
+  for (int i = threadIdx.x; i < TC_THRX_BYTES / 8; i += blockDim.x)   // no stale tags
+    sts_u64(smem_u32(thr_x + i), 0ull);
   if (role == 0 && lane == 0) {
     prefetch_tmap(&tmX);
     prefetch_tmap(&tmW);

@@ -103,12 +103,6 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* m, uint64_t* bar,
       "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "l"(cache_hint)
       : "memory");
 }
-// L2 prefetch of one tensor-map box (no shared memory, no completion).
-__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* m, int c0, int c1) {
-  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(
-                   reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1)
-               : "memory");
-}
 // 1-D bulk copy global -> shared (size % 16 == 0, 16-byte aligned), completion
 // on an mbarrier.
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes,
@@ -230,6 +224,25 @@ __device__ __forceinline__ uint64_t sdesc_k_sw128(uint32_t smem_addr) {
   d |= (uint64_t)1 << 46;                 // version = 1
   d |= (uint64_t)2 << 61;                 // SWIZZLE_128B
   return d;
+}
+
+// The same for SWIZZLE_64B K-major tiles: rows of 64 bytes, 8-row core
+// groups 512 B apart (SBO), layout type 4 (SWIZZLE_64B). Tiles 512-byte
+// aligned.
+__device__ __forceinline__ uint64_t sdesc_k_sw64(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;                 // LBO (ignored)
+  d |= (uint64_t)(512 >> 4) << 32;        // SBO
+  d |= (uint64_t)1 << 46;                 // version = 1
+  d |= (uint64_t)4 << 61;                 // SWIZZLE_64B
+  return d;
+}
+// K-major smem descriptor for rows of KBYTES (128: SW128, 64: SW64).
+template <int KBYTES>
+__device__ __forceinline__ uint64_t sdesc_k(uint32_t smem_addr) {
+  static_assert(KBYTES == 128 || KBYTES == 64, "K block of 64 or 128 bytes");
+  return KBYTES == 128 ? sdesc_k_sw128(smem_addr) : sdesc_k_sw64(smem_addr);
 }
 
 // Instruction descriptor, kind::f16: D f32, A/B bf16, both K-major, M x N.

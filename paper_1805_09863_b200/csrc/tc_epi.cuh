@@ -46,34 +46,9 @@ struct TcParams {
   OneShotTail os;                          // TAIL_ONESHOT: the peer buffers (peer.cuh)
   int taper;                               // single-CTA kernel: narrow final tiles (TileIter)
   int prepass;                             // k-best bound pre-pass over a segment's first tile
-  int wpf;                                 // W L2 prefetch distance in K blocks (0 = off)
+  int wbox;                                // W rows per TMA box (single-CTA kernel: 256 or 64)
 };
 
-// W L2 prefetch stream of the TMA producer: walks the CTA's (tile, K block)
-// sequence `dist` blocks ahead of the loads and prefetches those W boxes
-// into L2 (cp.async.bulk.prefetch.tensor), so a load finds W in L2 (~0.5 us)
-// instead of waiting on DRAM (~1.5 us) — with 4 stages of 48 KB the pipeline
-// holds too few bytes in flight to cover DRAM latency at the MMA's rate.
-struct WPrefetch {
-  TileIter it;
-  int mt = 0, v0 = 0, width = 0, kb = 0, n_kblk = 1;
-  bool last = false, done = false;
-  __device__ __forceinline__ void step(const CUtensorMap* tmW, int block_elems, int wbox,
-                                       bool issue) {
-    if (done) return;
-    if (kb == 0 || kb == n_kblk) {
-      if (!it.next(mt, v0, width, last)) {
-        done = true;
-        return;
-      }
-      kb = 0;
-    }
-    if (issue)
-      for (int j = 0; j < (width + wbox - 1) / wbox; ++j)
-        tma_prefetch_2d(tmW, kb * block_elems, v0 + j * wbox);
-    ++kb;
-  }
-};
 // Timeline probe points (globaltimer ns; per CTA; see amun_debug_timeline).
 enum { TL_ENTRY = 0, TL_SETUP = 1, TL_TMA0 = 2, TL_FULL0 = 3, TL_MMA_END = 4, TL_EPI_LAST = 5,
        TL_EPI_END = 6, TL_BARRIER = 7, TL_RELEASED = 8, TL_TAIL_END = 9, TL_TILE0 = 10,
@@ -114,13 +89,20 @@ constexpr int TC_BN = 256;
 #else
 constexpr int TC_BN = TC_BN_OVERRIDE;
 #endif
-constexpr int TC_BK = 64;
-constexpr int TC_WBOX = 64;                            // W rows per TMA box (single-CTA kernel)
-constexpr int TC_NBIAS = 8;                          // bias ring slots (see producer bound)
+constexpr int TC_BK = 64;                            // bf16 elements per K block (pair kernel)
+#ifndef TC1_KBYTES   // 64 (SW64, 8 stages) measured 1.3x slower per tile at cfg beam
+#define TC1_KBYTES 128
+#endif
+constexpr int TC_KBYTES = TC1_KBYTES;                 // bytes of K per block, single-CTA kernel
+constexpr int TC_NBIAS = 10;                         // bias ring slots (see producer bound)
 constexpr int TC_BIAS_BYTES = TC_NBIAS * TC_BN * 4;
 constexpr int TC_XCH_FLOATS = 2 + 2 * 16;            // one row's state in the exchange area
 constexpr int TC_XCH_BYTES = 128 * TC_XCH_FLOATS * 4;
+#if defined(AMUN_WITH_NG3) || defined(AMUN_WITH_NG4)
 constexpr int TC_THRX_BYTES = 4 * 128 * 8;           // per-(group, row) k-th-best words (NG <= 4)
+#else
+constexpr int TC_THRX_BYTES = 2 * 128 * 8;           // per-(group, row) k-th-best words (NG = 2)
+#endif
 // e4m3 column-scale ring. 4 slots suffice when a tile has more K blocks than
 // pipeline stages: the producer can only start tile t after the MMA started
 // tile t-1, which needed the epilogue of tile t-3 to have released its
@@ -135,6 +117,7 @@ constexpr int TC_SCALE_BYTES = TC_NSCALE * TC_BN * 4;
 // grow only into what the others released, else setmaxnreg.inc blocks).
 template <int NG>
 struct TcCfg {
+  static_assert(NG * 128 * 8 <= TC_THRX_BYTES, "thr_x area too small for NG epilogue groups");
   static constexpr int kEpiThreads = NG * 128;
   static constexpr int kThreads = 128 + kEpiThreads;
   static constexpr int kLaunchRegs = 65536 / kThreads / 8 * 8 > 248 ? 248 : 65536 / kThreads / 8 * 8;

@@ -37,13 +37,11 @@ VARIANTS["scores_t1"] = {"AMUN_TAIL": "off", "AMUN_PF_BYTES": "0", "AMUN_TAPER":
 VARIANTS["tail_pp0"] = {"AMUN_TAIL": "on", "AMUN_PF_BYTES": "0", "AMUN_PREPASS": "0"}
 VARIANTS["sep_pp0"] = {"AMUN_TAIL": "off", "AMUN_PF_BYTES": "0", "AMUN_PREPASS": "0"}
 VARIANTS["scores_pp0"] = {"AMUN_TAIL": "off", "AMUN_PF_BYTES": "0", "AMUN_PREPASS": "0"}
-# W L2 prefetch distance (default 8 K blocks)
-for _d in (0, 4, 16):
-    VARIANTS[f"sep_wpf{_d}"] = {"AMUN_TAIL": "off", "AMUN_WPF": str(_d)}
-    VARIANTS[f"scores_wpf{_d}"] = {"AMUN_TAIL": "off", "AMUN_WPF": str(_d)}
+for _b in (64, 256):
+    VARIANTS[f"sep_box{_b}"] = {"AMUN_TAIL": "off", "AMUN_WBOX": str(_b)}
+    VARIANTS[f"scores_box{_b}"] = {"AMUN_TAIL": "off", "AMUN_WBOX": str(_b)}
 for _v in VARIANTS.values():
     _v.setdefault("AMUN_PF_BYTES", "0")
-    _v.setdefault("AMUN_WPF", "8")
     _v.setdefault("AMUN_TAPER", "0")
     _v.setdefault("AMUN_PREPASS", "1")
 NOCHECK = {v for v in VARIANTS if v.startswith("scores")} | {"tailwait", "waitnocoop", "arriveonly"}

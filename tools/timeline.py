@@ -31,13 +31,16 @@ def main():
         os.environ["AMUN_TAPER"] = sys.argv[3]
     if len(sys.argv) > 4:   # first-tile pre-pass on / off (1 / 0)
         os.environ["AMUN_PREPASS"] = sys.argv[4]
-    if len(sys.argv) > 5:   # W L2 prefetch distance in K blocks
-        os.environ["AMUN_WPF"] = sys.argv[5]
     w = synth.CONFIGS[name]
+    if os.environ.get("AMUN_TL_V"):   # (experiment: another vocabulary size)
+        import dataclasses
+        w = dataclasses.replace(w, V=int(os.environ["AMUN_TL_V"]))
     dev = torch.device("cuda", 0)
     X, W, b = synth.gen_X(w).to(dev), synth.gen_W(w).to(dev), synth.gen_b(w).to(dev)
     pc, off = synth.gen_prev_cost(w).to(dev), synth.gen_offsets(w).to(dev)
     nc = max(2, -(-2 * 126 * 2 ** 20 // (W.numel() * W.element_size())))
+    if os.environ.get("AMUN_TL_COPIES"):   # (experiment: 1 = W may stay in L2)
+        nc = int(os.environ["AMUN_TL_COPIES"])
     Ws = [W] + [W.clone() for _ in range(nc - 1)]
     ol = amun.OutputLayer(w.H, w.V, dtype=w.dtype, k_max=w.k, max_rows=w.N, max_sentences=w.S)
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
@@ -72,8 +75,8 @@ def main():
     used = t[:, 0] > 0
     t = t[used]
     t0 = t[:, 0].min()
-    out = {"workload": name, "variant": variant, "ctas": int(used.sum()),
-           "env": {k: os.environ.get(k) for k in ("AMUN_TAPER", "AMUN_PREPASS", "AMUN_WPF")}}
+    out = {"workload": name, "variant": variant, "ctas": int(used.sum()), "V": w.V, "copies": nc,
+           "env": {k: os.environ.get(k) for k in ("AMUN_TAPER", "AMUN_PREPASS")}}
     for j, n in enumerate(NAMES):
         col = t[:, j]
         col = col[col > 0]
