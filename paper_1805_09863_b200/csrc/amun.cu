@@ -267,6 +267,7 @@ amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b
     if (s != AMUN_OK) return s;
     TcParams tp;
     memset(&tp, 0, sizeof(tp));
+    tp.mp.part_floats = (long long)(pl->slots_bytes / 4);   // (checked builds' bound)
     tp.N = N;
     tp.V_local = pl->V_local;
     tp.v_offset = pl->v_offset;
@@ -400,6 +401,7 @@ MergeParams base_merge(const amun_ol* pl) {
   MergeParams mp;
   memset(&mp, 0, sizeof(mp));
   mp.stride = pl->stride;
+  mp.part_floats = (long long)(pl->slots_bytes / 4);   // the workspace's record slots
   mp.k_max = pl->k_max;
   mp.V_total = pl->V_total;
   return mp;
@@ -710,6 +712,7 @@ amun_status amun_merge_partials(amun_ol* plan, const float* partials, int G,
   mp.layout = 1;
   mp.G = G;
   mp.N = N;
+  mp.part_floats = (long long)G * N * plan->stride;
   mp.S = S;
   mp.prev_cost = prev_cost;
   mp.offsets = beam_offsets;

@@ -20,6 +20,8 @@
 #pragma once
 #include <cstdint>
 
+#include "ptx.cuh"   // AMUN_DCHECK
+
 
 namespace amun {
 
@@ -266,6 +268,7 @@ __global__ void __launch_bounds__(CP_THREADS, CP_CTAS_PER_SM) compact_kernel(con
     excl += v;
   }
   if (tid == 0) cntb[nblk] = total;
+  AMUN_DCHECK(nblk <= CP_MAXBLK && total >= 0 && total <= N);
   __syncthreads();
   dbg(1);
   if (p.exp >= 3 && p.exp < 9) {
@@ -378,6 +381,7 @@ __global__ void __launch_bounds__(CP_THREADS, CP_CTAS_PER_SM) compact_kernel(con
   if (nrows <= 0) return;
   if (tid < nrows) {
     const int v = map[tid];
+    AMUN_DCHECK(nrows <= CP_MAXR && v >= 0 && v < N && d0 + tid < total && total <= N);
     const int src = p.parent ? p.parent[v] : v;
     gsrc[tid] = src;
     p.src_row[d0 + tid] = src;

@@ -34,6 +34,7 @@ struct MergeParams {
   long long* __restrict__ out_idx;
   float* __restrict__ out_cost;
   float* __restrict__ out_part;  // ROW mode: [N][stride]
+  long long part_floats;          // capacity of part (checked builds; 0 = unchecked)
   const int* __restrict__ N_dev; // amun_output_layer_dev: N on the device (layout 0), else NULL
   int num_sms;
 };
@@ -71,6 +72,10 @@ __device__ __forceinline__ void row_splits(const MergeParams& p, int r, const fl
     jstride = (long long)p.N * p.stride;
     n = p.G;
   }
+  // every record of the row inside the partial buffer
+  AMUN_DCHECK(r >= 0 && r < p.N && n >= 1 && base >= p.part &&
+              (p.part_floats == 0 ||
+               (base - p.part) + (n - 1) * jstride + p.stride <= p.part_floats));
 }
 
 struct Cand {
@@ -471,6 +476,7 @@ __device__ __forceinline__ void merge_sentence(const MergeParams& p, int s, Cand
   }
   if (threadIdx.x < p.k) {
     const int i = threadIdx.x;
+    AMUN_DCHECK(s >= 0 && s < p.S && r0 >= 0 && r0 <= r1 && r1 <= p.N);
     const bool ok = i < keep && i < ks;
     p.out_idx[(long long)s * p.k + i] = ok ? (long long)pool[i].r * p.V_total + pool[i].v : -1LL;
     p.out_cost[(long long)s * p.k + i] = ok ? pool[i].cost : kNegInf;
@@ -497,6 +503,7 @@ __device__ __forceinline__ void merge_sentence_k1(const MergeParams& p, int s, i
     }
   }
   if (lane == 0 && p.k >= 1) {
+    AMUN_DCHECK(s >= 0 && s < p.S && r0 >= 0 && r0 <= r1 && r1 <= p.N);
     const bool ok = best.v != 0x7fffffff && ks >= 1;
     p.out_idx[(long long)s * p.k] = ok ? (long long)best.r * p.V_total + best.v : -1LL;
     p.out_cost[(long long)s * p.k] = ok ? best.cost : kNegInf;

@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(MS_WARPS * 32) oneshot_kernel(const OneShotPar
   MergeParams dp = q.dst;
   dp.part = reinterpret_cast<const float*>(q.buf[me] + OS_CTRL_BYTES) +
             (long long)(epoch & 1u) * q.recv_elems;
+  dp.part_floats = q.recv_elems;
   dp.out_idx = q.out_idx[q.emulate ? me : 0];
   dp.out_cost = q.out_cost[q.emulate ? me : 0];
   for (int s = b; s < dp.S; s += q.nb) {

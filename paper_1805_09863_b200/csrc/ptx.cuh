@@ -38,6 +38,27 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                : "memory");
 }
 // Blocks until the phase with parity `parity` has completed.
+// Checked builds (-DAMUN_CHECKS, the sanitizer substitute; tools/run_checked.sh):
+// every mbarrier wait traps with its barrier after ~2 s instead of hanging,
+// and AMUN_DCHECK bounds / invariant assertions trap with a message.
+#if defined(AMUN_CHECKS) && !defined(AMUN_HANG_CHECK)
+#define AMUN_HANG_CHECK
+#endif
+#ifdef AMUN_CHECKS
+#define AMUN_DCHECK(cond, ...)                                                   \
+  do {                                                                           \
+    if (!(cond)) {                                                               \
+      printf("AMUN_DCHECK %s:%d block %d thread %d: %s\n", __FILE__, __LINE__,  \
+             (int)blockIdx.x, (int)threadIdx.x, #cond);                         \
+      __trap();                                                                  \
+    }                                                                            \
+  } while (0)
+#else
+#define AMUN_DCHECK(cond, ...) \
+  do {                         \
+  } while (0)
+#endif
+
 #ifdef AMUN_HANG_CHECK
 // Debug builds (-DAMUN_HANG_CHECK): report and trap instead of hanging.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -76,7 +97,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // issuer): no suspend-time hint, so the next copy / MMA issues as soon as
 // the phase completes.
 __device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
-#ifdef AMUN_NO_SPIN
+#if defined(AMUN_NO_SPIN) || defined(AMUN_HANG_CHECK)
   mbar_wait(bar, parity);
 #else
   uint32_t addr = smem_u32(bar);

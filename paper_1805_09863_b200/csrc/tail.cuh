@@ -171,6 +171,7 @@ __device__ __forceinline__ void grid_tail(const TcParams& p, const TcDyn& dyn, u
     MergeParams dp = mp;              // sentence phase over [G][N][stride]
     dp.layout = 1;
     dp.G = os.G;
+    dp.part_floats = os.recv_elems;
     dp.part = reinterpret_cast<const float*>(os.buf[os.rank] + OS_CTRL_BYTES) +
               (long long)(epoch & 1u) * os.recv_elems;
     for (int s = c; s < dp.S; s += G) {

@@ -402,6 +402,8 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
         }
         if (grp == 0 && row < dyn.N) {
           const long long slot = PAIR ? (slot_base + unit) * 2 + rank : slot_base + unit;
+          AMUN_DCHECK(p.mp.part_floats == 0 ||
+                      (slot * TC_BM + row_local + 1) * p.stride <= p.mp.part_floats);
           st.emit(p.part + (slot * TC_BM + row_local) * p.stride, p.k_max);
         }
       }

@@ -145,13 +145,16 @@ class DecodeTrace:
         st.total_ms = t_all0.elapsed_time(t_all1)
         return st
 
-    def run_graph(self, X0, W, b, prev0, finish) -> TraceStats:
+    def run_graph(self, X0, W, b, prev0, finish, log_steps=()) -> TraceStats:
         """Alg. 2 (dynamic) with every step on the device: N stays in device
         memory (amun_output_layer_dev reads it; amun_compact writes it), the
         bookkeeping glue uses fixed shapes over the N0-row buffers, and all
         T_max steps are captured in ONE CUDA graph, timed as one replay.
         Rows per step are logged on the device (they must equal the eager
-        dynamic mode's: the finish schedule alone decides them)."""
+        dynamic mode's: the finish schedule alone decides them). For the
+        steps in log_steps, the step's inputs (X, prev_cost, offsets, k_s, N)
+        and outputs (idx, cost) are copied on the device into st.logs (for
+        oracle checks of the graph-mode winners; copies are graph nodes)."""
         dev, S, B, N0 = self.dev, self.S, self.B, self.N0
         st = TraceStats("dynamic_graph")
         fin = finish.to(dev).reshape(-1).contiguous()
@@ -176,6 +179,13 @@ class DecodeTrace:
         alive = torch.empty(N0, dtype=torch.uint8, device=dev)
         src_row = torch.empty(N0, dtype=torch.int32, device=dev)
         rows_log = torch.zeros(T, dtype=torch.int32, device=dev)
+        logs = {t: {"X": torch.empty_like(X0, device=dev), "prev": torch.empty(N0, device=dev),
+                    "off": torch.empty(S + 1, dtype=torch.int32, device=dev),
+                    "k_s": torch.empty(S, dtype=torch.int32, device=dev),
+                    "N": torch.empty(1, dtype=torch.int32, device=dev),
+                    "idx": torch.empty((S, B), dtype=torch.int64, device=dev),
+                    "cost": torch.empty((S, B), dtype=torch.float32, device=dev)}
+                for t in log_steps if t < T}
 
         def steps(state):
             for t in range(T):
@@ -183,7 +193,14 @@ class DecodeTrace:
                 X, prev, ids = state["cols"][a][0], state["cols"][a][2], state["cols"][a][3]
                 off, cnt = state["off"][a], state["cnt"][a]
                 torch.sub(off[1:], off[:-1], out=k_s)                       # live beam per sentence
+                if t in logs:   # the step's inputs, before the bookkeeping overwrites prev
+                    for key, src in (("X", X), ("prev", prev), ("off", off), ("k_s", k_s),
+                                     ("N", cnt[:1])):
+                        logs[t][key].copy_(src)
                 self.ol.call_dev(X, W, b, prev, off, cnt[:1], B, k_s, out_idx=idx, out_cost=cost)
+                if t in logs:
+                    logs[t]["idx"].copy_(idx)
+                    logs[t]["cost"].copy_(cost)
                 # synthetic beam bookkeeping (driver glue), fixed shapes over N0 rows
                 sent = torch.searchsorted(off[1:], ar32, right=True).clamp_(max=S - 1)
                 slot = (ar - off.to(torch.int64)[sent]).clamp_(0, B - 1)
@@ -210,5 +227,6 @@ class DecodeTrace:
         st.total_ms = e0.elapsed_time(e1)
         st.rows = [int(n) for n in rows_log.cpu().tolist()]
         st.steps = T
+        st.logs = {t: {k: v.cpu() for k, v in d.items()} for t, d in logs.items()}
         self._graph_state = state              # (tests read the final state)
         return st

@@ -74,3 +74,33 @@ def compare_kbest(g_idx, g_cost, oracle_cost_of, o_cost64, k_s, dtype: str, V_to
 def exact_index_match_rate(g_idx, o_idx):
     g, o = np.asarray(g_idx), np.asarray(o_idx)
     return float(np.mean([np.array_equal(a, b) for a, b in zip(g, o)]))
+
+
+def compare_row_topk(g_l, g_v, L, k, band, v_offset=0, l_tol=1e-4):
+    """Per-row top-k of a partial record (reading G15/G3) against the oracle
+    logits L [N, V] (fp64): tie-band exact. With c_k the row's k-th oracle
+    logit, every oracle entry above c_k + band must be returned, every
+    returned token's oracle logit must be >= c_k - band, ids are unique, and
+    each returned logit is within l_tol of the oracle's for that token.
+    band covers the GPU's fp32 rounding (outside near-ties: exact sets).
+    Returns the number of rows with a near-tie inside the band."""
+    g_l = np.asarray(g_l, np.float64)
+    g_v = np.asarray(g_v, np.int64)
+    N, V = L.shape
+    ties = 0
+    for r in range(N):
+        order = np.lexsort((np.arange(V), -L[r]))
+        kk = min(k, V)
+        ck = L[r, order[kk - 1]]
+        nxt = L[r, order[kk]] if kk < V else -np.inf
+        gv = g_v[r, :kk] - v_offset
+        assert (gv >= 0).all() and (gv < V).all(), f"row {r}: ids out of range {gv}"
+        assert len(set(gv.tolist())) == kk, f"row {r}: duplicate ids {gv}"
+        ol = L[r, gv]
+        assert (ol >= ck - band).all(), f"row {r}: returned entry below the top-{kk} band"
+        must = set(order[:kk][L[r, order[:kk]] > ck + band].tolist())
+        assert must <= set(gv.tolist()), f"row {r}: missing entries above the band {must - set(gv.tolist())}"
+        assert np.abs(g_l[r, :kk] - ol).max() <= l_tol * max(1.0, np.abs(ol).max()), f"row {r}: logits"
+        if ck - nxt < band or np.any(np.abs(np.diff(L[r, order[:kk]])) < band):
+            ties += 1
+    return ties

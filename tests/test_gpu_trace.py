@@ -133,8 +133,19 @@ def test_trace_graph_mode_same_rows_as_dynamic():
     tr = DecodeTrace(H, V, S, B, device=dev)
     Wd, bd = W.to(dev), b.to(dev)
     dyn = tr.run(X, Wd, bd, pc, f, mode="dynamic")
-    gr = tr.run_graph(X, Wd, bd, pc, f)
+    gr = tr.run_graph(X, Wd, bd, pc, f, log_steps=(0, 2, 4, 6))
     assert gr.rows[:len(dyn.rows)] == dyn.rows
+    # the graph-mode winners against the oracle on the step's own inputs
+    Wo, bo = O.as_f64(W), O.as_f64(b)
+    for t, lg in gr.logs.items():
+        n = int(lg["N"][0])
+        assert n == gr.rows[t]
+        logp = O.log_softmax(O.add_bias(O.gemm(O.as_f64(lg["X"][:n]), Wo), bo))
+        prevd = O.as_f64(lg["prev"][:n])
+        offn, ksn = lg["off"].numpy(), lg["k_s"].numpy()
+        _, _, oc64, nxt = O.kbest_sentences(logp, prevd, offn, B, ksn)
+        compare_kbest(lg["idx"].numpy(), lg["cost"].numpy(), lambda s, r, v: prevd[r] + logp[r, v],
+                      oc64, ksn, "bf16", V, o_next=nxt)
     assert all(n == 0 for n in gr.rows[len(dyn.rows):])
     assert sum(gr.rows) == int(f.sum())
     # the surviving ids after the last step: none (everything finished)

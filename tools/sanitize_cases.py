@@ -46,15 +46,22 @@ def inputs(w):
             synth.gen_prev_cost(w).to(DEV), synth.gen_offsets(w).to(DEV))
 
 
-def case_beam(pairs):
+def case_beam(pairs, tail="on"):
     os.environ["AMUN_PAIRS"] = pairs
+    os.environ["AMUN_TAIL"] = tail
     w = synth.Workload("san", H=256, V=3001, S=52, B=5, k=5, seed=synth.BASE_SEED + 900)
     X, W, b, pc, off = inputs(w)
     ol = amun().OutputLayer(w.H, w.V, k_max=w.k, max_rows=w.N, max_sentences=w.S)
     idx, cost = ol(X, W, b, pc, off, w.k)
     torch.cuda.synchronize()
     check_beam(w, idx, cost)
+    # determinism (a race would show as run-to-run differences): bit-equal again
+    for _ in range(3):
+        i2, c2 = ol(X, W, b, pc, off, w.k)
+        torch.cuda.synchronize()
+        assert torch.equal(i2, idx) and torch.equal(c2, cost), "nondeterministic output"
     os.environ.pop("AMUN_PAIRS")
+    os.environ.pop("AMUN_TAIL")
 
 
 def case_beam_single():
@@ -63,6 +70,28 @@ def case_beam_single():
 
 def case_beam_pairs():
     case_beam("force")
+
+
+def case_beam_sep():
+    """The two-kernel form (fused kernel, then the separate merge kernel)."""
+    case_beam("off", tail="off")
+
+
+def case_oneshot_real():
+    """The one-shot exchange in the fused kernel's tail, real mode at world 1
+    (IPC-exported buffer, self-signal), equal to the single-GPU path."""
+    from paper_1805_09863_b200.sharded import ShardedOutputLayer
+    w = synth.Workload("san", H=256, V=3001, S=30, B=5, k=5, seed=synth.BASE_SEED + 908)
+    X, W, b, pc, off = inputs(w)
+    sh = ShardedOutputLayer(w.H, w.V, 1, 0, k_max=w.k, max_rows=w.N, max_sentences=w.S,
+                            exchange="oneshot")
+    ref = sh.ol(X, W, b, pc, off, w.k)
+    for _ in range(3):
+        i2, c2 = sh(X, W, b, pc, off, w.k)
+        torch.cuda.synchronize()
+        assert torch.equal(i2, ref[0]) and torch.equal(c2, ref[1])
+    assert not sh.oneshot.error()
+    sh.oneshot.close()
 
 
 def case_greedy():
