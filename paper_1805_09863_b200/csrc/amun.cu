@@ -127,6 +127,8 @@ struct amun_ol {
                         // less W in flight per SM in the narrow tiles)
   int prepass = 1;      // env AMUN_PREPASS=0: no first-tile k-best bound pre-pass (experiments)
   int wbox = 256;       // env AMUN_WBOX: W rows per TMA box, 256 or 64 (64 for tapered tiles)
+  int pdl = 1;          // env AMUN_PDL=0: no programmatic dependent launch of the fused kernel
+                        // (single-CTA kernel; greedy path 20.7 -> 19.7 us)
   int pairs_mode = 0;   // env AMUN_PAIRS: 0 auto, 1 never ("off"), 2 always ("force"; tests)
   MapEntry xmaps[4];
   MapEntry wmaps[8];
@@ -312,6 +314,7 @@ amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b
     tp.taper = pairs ? 0 : pl->taper;
     tp.prepass = pl->prepass;
     tp.wbox = pl->wbox;
+    tp.pdl = pairs ? 0 : pl->pdl;
     if (pl->pf_bytes > 0 && !N_dev) {
       tp.pf_w = static_cast<const char*>(W);
       tp.pf_row_bytes = pl->dtype == AMUN_E4M3 ? pl->H : pl->dtype == AMUN_TF32X3 ? 12LL * pl->H
@@ -532,6 +535,8 @@ amun_status amun_ol_create(amun_ol** plan, int H, int V_local, int v_offset, int
                   : strcmp(t, "nocoop") == 0 ? 3 : strcmp(t, "fence") == 0 ? 4
                   : strcmp(t, "sleep") == 0 ? 5 : strcmp(t, "waitnocoop") == 0 ? 6
                   : strcmp(t, "arriveonly") == 0 ? 7 : 0;
+    const char* pd = getenv("AMUN_PDL");
+    if (pd) pl->pdl = atoi(pd) != 0;
     const char* wb = getenv("AMUN_WBOX");
     if (wb) pl->wbox = atoi(wb) == 64 ? 64 : 256;
     const char* pp = getenv("AMUN_PREPASS");

@@ -47,24 +47,35 @@ amun_status launch_kernel(void (*kern)(const CUtensorMap, const CUtensorMap, con
     return launch_fail("fused kernel compiled with %d registers/thread, needs %d for its "
                 "setmaxnreg budget", fa.numRegs, TcCfg<NG>::kLaunchRegs);
   LT_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
-  if (!tp.tail || (tp.tail & TAIL_X_NOCOOP)) {
+  const bool coop = tp.tail && !(tp.tail & TAIL_X_NOCOOP);
+  if (!coop && !tp.pdl) {
     kern<<<grid, TcCfg<NG>::kThreads, smem_bytes, st>>>(*mx, *mw, tp);
     LT_TRY(cudaGetLastError());
     return AMUN_OK;
   }
   // The fused tail waits on every CTA of the grid (tail.cuh): a cooperative
   // launch guarantees they are co-resident (grid <= #SMs, one CTA per SM).
+  // tp.pdl: programmatic dependent launch (the kernel's prologue may overlap
+  // the previous kernel's end; it waits in griddepcontrol.wait before any
+  // global memory access, ol_tc.cuh).
   cudaLaunchConfig_t cfg;
   memset(&cfg, 0, sizeof(cfg));
   cfg.gridDim = dim3((unsigned)grid, 1, 1);
   cfg.blockDim = dim3(TcCfg<NG>::kThreads, 1, 1);
   cfg.dynamicSmemBytes = (size_t)smem_bytes;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (coop) {
+    attr[na].id = cudaLaunchAttributeCooperative;
+    attr[na++].val.cooperative = 1;
+  }
+  if (tp.pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na++].val.programmaticStreamSerializationAllowed = 1;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = na;
   LT_TRY(cudaLaunchKernelEx(&cfg, kern, *mx, *mw, tp));
   return AMUN_OK;
 }

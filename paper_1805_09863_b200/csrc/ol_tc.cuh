@@ -82,8 +82,11 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
   constexpr int kCtrl = 4 * NG;                    // first control warp
   const int role = warp - kCtrl;                   // 0 = TMA, 1 = MMA, 2-3 idle, < 0 epilogue
 
-  if (threadIdx.x == 0) tl_mark(p.tl, TL_ENTRY);
-  if (role == 0 && lane == 0 && !p.N_dev)   // W to L2 before the prologue (tail.cuh)
+  // Programmatic dependent launch: the next launch in the stream may be
+  // scheduled now (its CTAs still need this kernel's SMs to free up).
+  if (p.pdl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  if (threadIdx.x == 0 && !p.pdl) tl_mark(p.tl, TL_ENTRY);
+  if (role == 0 && lane == 0 && !p.N_dev && !p.pdl)   // W to L2 before the prologue (tail.cuh)
     entry_prefetch_w(p, (long long)blockIdx.x * p.sch.C,
                      min((long long)(blockIdx.x + 1) * p.sch.C, p.sch.total), p.sch);
   for (int i = threadIdx.x; i < TC_THRX_BYTES / 8; i += blockDim.x)   // no stale tags
@@ -109,6 +112,13 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  // (PDL) everything above touched only shared memory / TMEM / the kernel
+  // parameters; wait for the previous grid in the stream (completion and
+  // memory visibility) before any global memory access
+  if (p.pdl) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (threadIdx.x == 0) tl_mark(p.tl, TL_ENTRY);
+  }
   const uint32_t tmem_base = *tmem_holder;
   // this launch's tag (hints, tail counters): read by the epilogue threads
   // (the only users), off the TMA producer's path to its first load

@@ -47,6 +47,7 @@ struct TcParams {
   int taper;                               // single-CTA kernel: narrow final tiles (TileIter)
   int prepass;                             // k-best bound pre-pass over a segment's first tile
   int wbox;                                // W rows per TMA box (single-CTA kernel: 256 or 64)
+  int pdl;                                 // launched with programmatic stream serialization
 };
 
 // Timeline probe points (globaltimer ns; per CTA; see amun_debug_timeline).

@@ -37,6 +37,10 @@ VARIANTS["scores_t1"] = {"AMUN_TAIL": "off", "AMUN_PF_BYTES": "0", "AMUN_TAPER":
 VARIANTS["tail_pp0"] = {"AMUN_TAIL": "on", "AMUN_PF_BYTES": "0", "AMUN_PREPASS": "0"}
 VARIANTS["sep_pp0"] = {"AMUN_TAIL": "off", "AMUN_PF_BYTES": "0", "AMUN_PREPASS": "0"}
 VARIANTS["scores_pp0"] = {"AMUN_TAIL": "off", "AMUN_PF_BYTES": "0", "AMUN_PREPASS": "0"}
+for _p in (0, 1):
+    VARIANTS[f"tail_pdl{_p}"] = {"AMUN_TAIL": "on", "AMUN_PDL": str(_p)}
+    VARIANTS[f"sep_pdl{_p}"] = {"AMUN_TAIL": "off", "AMUN_PDL": str(_p)}
+    VARIANTS[f"scores_pdl{_p}"] = {"AMUN_TAIL": "off", "AMUN_PDL": str(_p)}
 for _b in (64, 256):
     VARIANTS[f"sep_box{_b}"] = {"AMUN_TAIL": "off", "AMUN_WBOX": str(_b)}
     VARIANTS[f"scores_box{_b}"] = {"AMUN_TAIL": "off", "AMUN_WBOX": str(_b)}
@@ -101,6 +105,9 @@ def main():
                         ol.scores(X, Ws[i % ncopy], b)
                     else:
                         ol(X, Ws[i % ncopy], b, pc, off, w.k, out_idx=oi, out_cost=oc)
+                if os.environ.get("AB_SLEEP"):   # cool down between measurements (burst clocks)
+                    import time
+                    time.sleep(float(os.environ["AB_SLEEP"]))
                 res[v] += graph_us(fn, K)
                 if v in NOCHECK:
                     pass
