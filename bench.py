@@ -726,6 +726,17 @@ def main():
             cpu = {"value": parity["rows"] / dt, "unit": UNIT, "cores": blas_threads(),
                    "kind": "oracle", "sample": f"first {n_sent} sentences ({parity['rows']} rows)"
                                                f" x full V={w.V}, one pass, {dt:.1f} s"}
+            # the same oracle on ONE host thread (BLAS limited to 1), a smaller sample
+            try:
+                from threadpoolctl import threadpool_limits
+                n1 = min(8, n_sent)
+                with threadpool_limits(limits=1):
+                    dt1, rows1, *_ = oracle_sample(w, p.X_h, p.W_h, p.b_h, p.pc_h, n1)
+                cpu["one_thread"] = {"value": rows1 / dt1, "unit": UNIT, "cores": 1,
+                                     "sample": f"first {n1} sentences ({rows1} rows) x full "
+                                               f"V={w.V}, {dt1:.1f} s"}
+            except ImportError:
+                pass
         elif not args.no_cpu_baseline:
             parity, _ = parity_sample(w, p.idx, p.cost, p.X_h, p.full_W(), p.full_b(), p.pc_h,
                                       int(os.environ.get("AMUN_PARITY_SENTENCES", "16")))

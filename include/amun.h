@@ -286,7 +286,10 @@ amun_status amun_debug_logits(amun_ol* plan, const void* X, const void* W, const
  * the same fused kernel with part of the epilogue compiled out.
  *   variant 2: bare GEMM, the epilogue only drains the TMEM accumulators;
  *   variant 3: GEMM + bias + online max/sum-of-exp, no k-best;
- *   variant 4: the first kernel of amun_argmax alone (k = 1, no exp).
+ *   variant 4: the first kernel of amun_argmax alone (k = 1, no exp);
+ *   variant 5: variant 2 whose MMAs re-read the first pipeline stages after
+ *              they are loaded once (the MMA issue rate without TMA traffic);
+ *   variant 6 / 7: the same, but X / W is still copied for every block.
  * Results are meaningless scratch in `workspace`; bf16 plans only. */
 amun_status amun_bench_variant(amun_ol* plan, const void* X, const void* W, const float* b,
                                int N, int variant, void* workspace, void* stream);

@@ -127,6 +127,8 @@ struct amun_ol {
                         // less W in flight per SM in the narrow tiles)
   int prepass = 1;      // env AMUN_PREPASS=0: no first-tile k-best bound pre-pass (experiments)
   int wbox = 256;       // env AMUN_WBOX: W rows per TMA box, 256 or 64 (64 for tapered tiles)
+  int mma_only = 0;     // (amun_bench_variant 5: the MMA issue rate alone)
+  int mc = 0;           // env AMUN_MC: W multicast cluster size (experiment; ol_tc.cuh)
   int pdl = 1;          // env AMUN_PDL=0: no programmatic dependent launch of the fused kernel
                         // (single-CTA kernel; greedy path 20.7 -> 19.7 us)
   int pairs_mode = 0;   // env AMUN_PAIRS: 0 auto, 1 never ("off"), 2 always ("force"; tests)
@@ -262,9 +264,17 @@ amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b
     // bytes of K per pipeline block: the pair kernel 128 (SW128), the
     // single-CTA kernel TC_KBYTES (ol_tc.cuh)
     const int kbytes = pairs ? 128 : TC_KBYTES;
+    // W multicast clusters (env AMUN_MC = cluster size, experiment): when the
+    // aligned schedule has exactly mc M-tiles, the mc CTAs of one vocab split
+    // form a cluster and share each W K-block (one multicast per 64-row box)
+    int mc = 0;
+    if (pl->mc > 1 && !pairs && !N_dev && mode != 1 && sch.band != sch.Vp &&
+        cdiv(N, TC_BM) == pl->mc && grid % pl->mc == 0)
+      mc = pl->mc;
+    const int wbox = mc > 1 ? 64 : pl->wbox;
     amun_status s = get_map(pl, pl->xmaps, 4, pl->xnext, X, N, a_rows, kbytes, &mx);
     if (s != AMUN_OK) return s;
-    s = get_map(pl, pl->wmaps, 8, pl->wnext, W, pl->V_local, pairs ? TC_BN / 2 : pl->wbox, kbytes,
+    s = get_map(pl, pl->wmaps, 8, pl->wnext, W, pl->V_local, pairs ? TC_BN / 2 : wbox, kbytes,
                 &mw);
     if (s != AMUN_OK) return s;
     TcParams tp;
@@ -313,8 +323,10 @@ amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b
     tp.tl = pl->tl;
     tp.taper = pairs ? 0 : pl->taper;
     tp.prepass = pl->prepass;
-    tp.wbox = pl->wbox;
+    tp.wbox = wbox;
+    tp.mc = mc;
     tp.pdl = pairs ? 0 : pl->pdl;
+    tp.mma_only = pl->mma_only;
     if (pl->pf_bytes > 0 && !N_dev) {
       tp.pf_w = static_cast<const char*>(W);
       tp.pf_row_bytes = pl->dtype == AMUN_E4M3 ? pl->H : pl->dtype == AMUN_TF32X3 ? 12LL * pl->H
@@ -535,6 +547,8 @@ amun_status amun_ol_create(amun_ol** plan, int H, int V_local, int v_offset, int
                   : strcmp(t, "nocoop") == 0 ? 3 : strcmp(t, "fence") == 0 ? 4
                   : strcmp(t, "sleep") == 0 ? 5 : strcmp(t, "waitnocoop") == 0 ? 6
                   : strcmp(t, "arriveonly") == 0 ? 7 : 0;
+    const char* mcv = getenv("AMUN_MC");
+    if (mcv) pl->mc = atoi(mcv);
     const char* pd = getenv("AMUN_PDL");
     if (pd) pl->pdl = atoi(pd) != 0;
     const char* wb = getenv("AMUN_WBOX");
@@ -855,10 +869,15 @@ amun_status amun_bench_variant(amun_ol* plan, const void* X, const void* W, cons
                                int N, int variant, void* workspace, void* stream) {
   amun_status s = check_score_args(plan, X, W, b, N, workspace);
   if (s != AMUN_OK) return s;
-  if (variant < 2 || variant > 4) return fail(AMUN_EINVAL, "variant %d not in {2, 3, 4}", variant);
+  if (variant < 2 || variant > 7) return fail(AMUN_EINVAL, "variant %d not in [2, 7]", variant);
   if (plan->dtype != AMUN_BF16) return fail(AMUN_EUNSUPPORTED, "variants exist for bf16 only");
-  return run_scores(plan, X, W, b, N, workspace, nullptr, static_cast<cudaStream_t>(stream),
-                    variant);
+  // 5 = bare GEMM whose MMAs re-read the first stages; 6 / 7 = only X / only W
+  // copied again after the first stages
+  plan->mma_only = variant >= 5 ? variant - 4 : 0;
+  const amun_status s2 = run_scores(plan, X, W, b, N, workspace, nullptr,
+                                    static_cast<cudaStream_t>(stream), variant >= 5 ? 2 : variant);
+  plan->mma_only = 0;
+  return s2;
 }
 
 }  // extern "C"

@@ -48,7 +48,7 @@ amun_status launch_kernel(void (*kern)(const CUtensorMap, const CUtensorMap, con
                 "setmaxnreg budget", fa.numRegs, TcCfg<NG>::kLaunchRegs);
   LT_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
   const bool coop = tp.tail && !(tp.tail & TAIL_X_NOCOOP);
-  if (!coop && !tp.pdl) {
+  if (!coop && !tp.pdl && tp.mc <= 1) {
     kern<<<grid, TcCfg<NG>::kThreads, smem_bytes, st>>>(*mx, *mw, tp);
     LT_TRY(cudaGetLastError());
     return AMUN_OK;
@@ -64,8 +64,14 @@ amun_status launch_kernel(void (*kern)(const CUtensorMap, const CUtensorMap, con
   cfg.blockDim = dim3(TcCfg<NG>::kThreads, 1, 1);
   cfg.dynamicSmemBytes = (size_t)smem_bytes;
   cfg.stream = st;
-  cudaLaunchAttribute attr[2];
+  cudaLaunchAttribute attr[3];
   int na = 0;
+  if (tp.mc > 1) {   // W multicast clusters (ol_tc.cuh)
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = (unsigned)tp.mc;
+    attr[na].val.clusterDim.y = 1;
+    attr[na++].val.clusterDim.z = 1;
+  }
   if (coop) {
     attr[na].id = cudaLaunchAttributeCooperative;
     attr[na++].val.cooperative = 1;

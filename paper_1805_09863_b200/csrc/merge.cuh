@@ -488,12 +488,20 @@ __device__ __forceinline__ void merge_sentence(const MergeParams& p, int s, Cand
 // its rows' single candidates pc + (l - lse) — exactly what merge_sentence
 // selects for k = 1 (the same expression, so the same bits), so warps can
 // take sentences independently.
-__device__ __forceinline__ void merge_sentence_k1(const MergeParams& p, int s, int lane) {
-  const int r0 = p.offsets[s], r1 = p.offsets[s + 1];
+// r0 / r1 / pc0: the sentence's row range and its first row's prev_cost when
+// the caller loaded them already (the fused tail does, before its grid-wide
+// wait: they are inputs, not other CTAs' results); r0 < 0: load them here.
+__device__ __forceinline__ void merge_sentence_k1(const MergeParams& p, int s, int lane, int r0 = -1,
+                                                  int r1 = 0, float pc0 = 0.f) {
+  if (r0 < 0) {
+    r0 = p.offsets[s];
+    r1 = p.offsets[s + 1];
+    pc0 = r1 > r0 ? p.prev_cost[r0] : 0.f;
+  }
   const int ks = p.k_s ? min(p.k_s[s], p.k) : p.k;
   Cand best{kNegInf, kNegInf, 0x7fffffff, 0x7fffffff};
   for (int r = r0; r < r1; ++r) {
-    const float pc = p.prev_cost[r];
+    const float pc = r == r0 ? pc0 : p.prev_cost[r];
     float lse, M, Z, l;
     int v;
     row_topk<1>(p, r, lane, lse, M, Z, l, v);   // lane 0 holds the row's best

@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
   // scheduled now (its CTAs still need this kernel's SMs to free up).
   if (p.pdl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (threadIdx.x == 0 && !p.pdl) tl_mark(p.tl, TL_ENTRY);
-  if (role == 0 && lane == 0 && !p.N_dev && !p.pdl)   // W to L2 before the prologue (tail.cuh)
+  if (role == 0 && lane == 0 && !p.N_dev && !p.pdl && p.mc <= 1)   // W to L2 before the prologue (tail.cuh)
     entry_prefetch_w(p, (long long)blockIdx.x * p.sch.C,
                      min((long long)(blockIdx.x + 1) * p.sch.C, p.sch.total), p.sch);
   for (int i = threadIdx.x; i < TC_THRX_BYTES / 8; i += blockDim.x)   // no stale tags
@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
     prefetch_tmap(&tmW);
     for (int i = 0; i < TC_STAGES; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+      mbar_init(&empty[i], p.mc > 1 ? p.mc : 1);   // W multicast: every cluster CTA's MMAs
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
+  if (p.mc > 1) cluster_sync();   // peers' barriers initialised before any multicast
   tc_fence_after();
   // (PDL) everything above touched only shared memory / TMEM / the kernel
   // parameters; wait for the previous grid in the stream (completion and
@@ -126,7 +127,14 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
   if (threadIdx.x == 0) tl_mark(p.tl, TL_SETUP);
 
   const TcDyn dyn = tc_dyn<false>(p);      // N (and the schedule) from the device in _dev mode
-  const long long start = (long long)blockIdx.x * dyn.sch.C;
+  // W multicast clusters (p.mc > 1): the mc CTAs of a cluster are the mc
+  // M-tiles of ONE vocab split (aligned schedule), so they stream the same W
+  // tiles in lockstep; the logical CTA index (ranges, record slots) is
+  // M-tile * splits + split
+  const uint32_t mc_rank = p.mc > 1 ? cluster_ctarank() : 0u;
+  const long long cta = p.mc > 1 ? (long long)mc_rank * (dyn.sch.band / dyn.sch.C) + blockIdx.x / p.mc
+                                 : (long long)blockIdx.x;
+  const long long start = cta * dyn.sch.C;
   const long long stop = min(start + dyn.sch.C, dyn.sch.total);
 
   if (role >= 0) {
@@ -143,10 +151,26 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
       uint32_t phase = 0;
       // TC_KBYTES of K per block: bf16 / e4m3 / fp32 (tf32x3) elements
       constexpr int kBlockElems = ELT == 1 ? TC_KBYTES : ELT == 2 ? TC_KBYTES / 4 : TC_KBYTES / 2;
+      int loads = 0;
       while (it.next(mt, v0, width, last)) {
         if (lane == 0) bias_ring_load(p, sbias, bfull, tile, v0, width, sscale);
         for (int kb = 0; kb < p.n_kblk; ++kb) {
           mbar_wait_spin(&empty[stage], phase ^ 1);
+          // (experiment p.mma_only, MODE 2: only the first TC_STAGES blocks are
+          // loaded; later stages are marked full without a copy, so the MMAs
+          // re-read stale data: the pipeline without TMA traffic)
+          // (mma_only 2: only X is copied again, 3: only W; stale otherwise)
+          const bool warm = MODE == 2 && p.mma_only && loads++ >= TC_STAGES;
+          if (warm && p.mma_only == 1) {
+            if (lane == 0) mbar_arrive(&full[stage]);
+            __syncwarp();
+            if (++stage == TC_STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
+          }
+          const bool load_x = !warm || p.mma_only == 2, load_w = !warm || p.mma_only == 3;
           if (lane == 0) {
             if (tile == 0 && kb == 0) tl_mark(p.tl, TL_TMA0);
             // W in boxes of p.wbox rows (256, or 64 so narrow tapered tiles
@@ -154,12 +178,22 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
             // contiguously, i.e. the same SW128 K-major tile
             const int wbox = p.wbox;
             const int nbox = (width + wbox - 1) / wbox;
-            mbar_arrive_expect_tx(&full[stage], p.a_box_bytes + nbox * wbox * TC_KBYTES);
-            tma_load_2d(&tmX, &full[stage], sA + stage * TC_A_BYTES, kb * kBlockElems, mt * TC_BM,
-                        pol_x);
-            for (int j = 0; j < nbox; ++j)
+            mbar_arrive_expect_tx(&full[stage], (load_x ? p.a_box_bytes : 0) +
+                                                    (load_w ? nbox * wbox * TC_KBYTES : 0));
+            if (load_x)
+              tma_load_2d(&tmX, &full[stage], sA + stage * TC_A_BYTES, kb * kBlockElems, mt * TC_BM,
+                          pol_x);
+            if (p.mc > 1) {
+              // this CTA's box of the W tile, multicast to the whole cluster
+              for (int j = (int)mc_rank; load_w && j < nbox; j += p.mc)
+                tma_load_2d_mc(&tmW, &full[stage], sB + stage * TC_B_BYTES + j * wbox * TC_KBYTES,
+                               kb * kBlockElems, v0 + j * wbox, (uint16_t)((1u << p.mc) - 1u));
+            }
+            for (int j = 0; load_w && p.mc <= 1 && j < nbox; ++j) {
+              // (the L2 hint measured the same as evict_first / evict_normal / none)
               tma_load_2d(&tmW, &full[stage], sB + stage * TC_B_BYTES + j * wbox * TC_KBYTES,
                           kb * kBlockElems, v0 + j * wbox, 0ull);
+            }
           }
           __syncwarp();
           if (++stage == TC_STAGES) {
@@ -207,7 +241,10 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
               else
                 mma_tf32(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
             }
-            mma_commit(&empty[stage]);              // smem slot free once these MMAs finish
+            if (p.mc > 1)   // the slot is free in every cluster CTA once all their MMAs finish
+              mma_commit_mc(&empty[stage], (uint16_t)((1u << p.mc) - 1u));
+            else
+              mma_commit(&empty[stage]);            // smem slot free once these MMAs finish
           }
           __syncwarp();
           if (++stage == TC_STAGES) {
@@ -230,8 +267,7 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
       if (blockIdx.x == 0 && threadIdx.x == 0) p.arrive[(gen + 1u) & 1u] = 0u;
     }
     tc_epilogue<KB, MODE, NG, false, ELT>(p, tmem_base, start, stop, tfull, tempty, bfull, sbias, xch,
-                                     thr_x, gen, warp, lane, 0u, (long long)blockIdx.x, dyn,
-                                     sscale);
+                                     thr_x, gen, warp, lane, 0u, cta, dyn, sscale);
     if (threadIdx.x == 0) tl_mark(p.tl, TL_EPI_END);
     if constexpr (MODE == 0 || MODE == 4) {
       // The merge in this launch (tail.cuh), run by the epilogue warps INSIDE
@@ -250,6 +286,7 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
 
   tc_fence_before();
   __syncthreads();
+  if (p.mc > 1) cluster_sync();   // no CTA leaves while peers may still signal into it
   if (threadIdx.x == 0 && !p.tail) tl_mark(p.tl, TL_BARRIER);
   if (role == 1) {
     tc_fence_after();

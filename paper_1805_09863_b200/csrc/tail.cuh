@@ -93,6 +93,19 @@ __device__ __forceinline__ void grid_tail(const TcParams& p, const TcDyn& dyn, u
                                           uint32_t tag) {
   const int tid = threadIdx.x;
   if (tid >= MS_WARPS * 32) return;
+  // k_max = 1 sentences: their row range and prev_cost are inputs (not other
+  // CTAs' results), so each warp requests its first sentence's now and the
+  // loads overlap the grid-wide wait below
+  int pre_r0 = -1, pre_r1 = 0;
+  float pre_pc = 0.f;
+  if (KB == 1 && (p.tail & 15) == TAIL_SENT && !(p.tail & TAIL_X_NOWORK)) {
+    const int s = blockIdx.x + gridDim.x * (tid >> 5);
+    if (s < p.mp.S) {
+      pre_r0 = p.mp.offsets[s];
+      pre_r1 = p.mp.offsets[s + 1];
+      pre_pc = pre_r1 > pre_r0 ? p.mp.prev_cost[pre_r0] : 0.f;
+    }
+  }
   if (tid == 0) {
     // arrival: acq_rel RMW on this launch's counter (release: the CTA's
     // records, ordered before it by the barrier; acquire: every earlier
@@ -128,7 +141,10 @@ __device__ __forceinline__ void grid_tail(const TcParams& p, const TcDyn& dyn, u
   const int kind = p.tail & 15;
   if (p.tail & TAIL_X_NOWORK) return;   // (experiment: the arrival / wait alone)
   if (kind == TAIL_SENT && KB == 1) {   // k_max = 1: a warp per sentence (merge_sentence_k1)
-    for (int s = c + G * warp; s < mp.S; s += G * MS_WARPS) merge_sentence_k1(mp, s, lane);
+    for (int s = c + G * warp; s < mp.S; s += G * MS_WARPS) {
+      merge_sentence_k1(mp, s, lane, pre_r0, pre_r1, pre_pc);
+      pre_r0 = -1;   // later sentences load their own
+    }
   } else if (kind == TAIL_SENT) {
     Cand* pool = reinterpret_cast<Cand*>(scratch);
     Cand* best = pool + KB + MS_CAP;

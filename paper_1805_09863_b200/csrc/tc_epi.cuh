@@ -48,6 +48,8 @@ struct TcParams {
   int prepass;                             // k-best bound pre-pass over a segment's first tile
   int wbox;                                // W rows per TMA box (single-CTA kernel: 256 or 64)
   int pdl;                                 // launched with programmatic stream serialization
+  int mma_only;                            // (experiment, MODE 2) MMAs re-read the first stages
+  int mc;                                  // > 1: clusters of mc M-tile CTAs share W (multicast)
 };
 
 // Timeline probe points (globaltimer ns; per CTA; see amun_debug_timeline).

@@ -26,7 +26,7 @@ TL_N = 40
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "greedy"
     variant = sys.argv[2] if len(sys.argv) > 2 else "tail"
-    os.environ["AMUN_TAIL"] = "off" if variant in ("sep", "scores", "bare", "stats") else "on"
+    os.environ["AMUN_TAIL"] = "off" if variant in ("sep", "scores", "bare", "stats", "mmaonly") else "on"
     if len(sys.argv) > 3:   # taper on / off (1 / 0)
         os.environ["AMUN_TAPER"] = sys.argv[3]
     if len(sys.argv) > 4:   # first-tile pre-pass on / off (1 / 0)
@@ -52,8 +52,8 @@ def main():
     def step(i):
         if variant == "scores":
             ol.scores(X, Ws[i % nc], b)
-        elif variant in ("bare", "stats"):   # amun_bench_variant 2 / 3 (Table 4 analogues)
-            ol.bench_variant(X, Ws[i % nc], b, 2 if variant == "bare" else 3)
+        elif variant in ("bare", "stats", "mmaonly"):   # amun_bench_variant 2 / 3 / 5
+            ol.bench_variant(X, Ws[i % nc], b, {"bare": 2, "stats": 3, "mmaonly": 5}[variant])
         else:
             ol(X, Ws[i % nc], b, pc, off, w.k, out_idx=oi, out_cost=oc)
     K = 20
