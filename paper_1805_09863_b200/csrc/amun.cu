@@ -125,7 +125,8 @@ struct amun_ol {
   int ng_override = 0;  // env AMUN_NG: 2 or 4 epilogue warpgroups (experiments)
   int taper = 0;        // env AMUN_TAPER=1: narrow final tiles (experiments; measured slower:
                         // less W in flight per SM in the narrow tiles)
-  int prepass = 1;      // env AMUN_PREPASS=0: no first-tile k-best bound pre-pass (experiments)
+  int prepass = 1;      // env AMUN_PREPASS=n: the k-best bound pre-pass on a segment's first n
+                        // tiles (0 = off; experiments)
   int wbox = 256;       // env AMUN_WBOX: W rows per TMA box, 256 or 64 (64 for tapered tiles)
   int mma_only = 0;     // (amun_bench_variant 5: the MMA issue rate alone)
   int mc = 0;           // env AMUN_MC: W multicast cluster size (experiment; ol_tc.cuh)
@@ -532,6 +533,11 @@ amun_status amun_ol_create(amun_ol** plan, int H, int V_local, int v_offset, int
   pl->max_sentences = max_sentences;
   pl->device = device;
   pl->num_sms = prop.multiProcessorCount;
+  {   // (experiment AMUN_SMS: the plan schedules over fewer SMs, e.g. to share
+      // the GPU with a concurrent kernel on another stream)
+    const char* e = getenv("AMUN_SMS");
+    if (e && atoi(e) > 0 && atoi(e) < pl->num_sms) pl->num_sms = atoi(e);
+  }
   pl->stride = 2 + 2 * k_max;
   {
     const char* g = getenv("AMUN_NG");
@@ -554,7 +560,7 @@ amun_status amun_ol_create(amun_ol** plan, int H, int V_local, int v_offset, int
     const char* wb = getenv("AMUN_WBOX");
     if (wb) pl->wbox = atoi(wb) == 64 ? 64 : 256;
     const char* pp = getenv("AMUN_PREPASS");
-    if (pp) pl->prepass = atoi(pp) != 0;
+    if (pp) pl->prepass = atoi(pp);
     const char* tp = getenv("AMUN_TAPER");
     if (tp) pl->taper = atoi(tp) != 0;
     if (pl->taper) pl->wbox = 64;   // narrow tiles load only their own rows

@@ -45,7 +45,7 @@ struct TcParams {
   unsigned long long* __restrict__ tl;     // timeline probe [grid][TL_N] (amun_debug_timeline), else NULL
   OneShotTail os;                          // TAIL_ONESHOT: the peer buffers (peer.cuh)
   int taper;                               // single-CTA kernel: narrow final tiles (TileIter)
-  int prepass;                             // k-best bound pre-pass over a segment's first tile
+  int prepass;                             // k-best bound pre-pass over a segment's first n tiles
   int wbox;                                // W rows per TMA box (single-CTA kernel: 256 or 64)
   int pdl;                                 // launched with programmatic stream serialization
   int mma_only;                            // (experiment, MODE 2) MMAs re-read the first stages
@@ -213,7 +213,7 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
   // nothing below it can be in the row's top-KB (the same argument as the
   // list-filling bound of kbest32 and reading G15); ties at it are kept.
   float pre = kNegInf;
-  bool seg_first = true;
+  int seg_tile = 0;   // tiles of the current segment processed so far
   while (it.next(unit, v0, width, last)) {
     const int mt = PAIR ? 2 * unit + (int)rank : unit;
     const uint32_t tag = (uint32_t)mt + 1u;
@@ -288,7 +288,7 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
       }
     };
     if constexpr (MODE == 0 && KB > 1) {
-      if (live && seg_first && p.prepass) {
+      if (live && seg_tile < p.prepass) {
         float top[KB];
 #pragma unroll
         for (int i = 0; i < KB; ++i) top[i] = kNegInf;
@@ -311,8 +311,10 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
             }
           }
         }
-        pre = top[KB - 1];
-        if (pre != kNegInf) sts_u64(smem_u32(my_thr), ((unsigned long long)tag << 32) | f2o(pre));
+        if (top[KB - 1] > pre) {   // bounds only rise within a segment
+          pre = top[KB - 1];
+          sts_u64(smem_u32(my_thr), ((unsigned long long)tag << 32) | f2o(fmaxf(pre, st.l[KB - 1])));
+        }
       }
     }
     if (live) {
@@ -371,13 +373,13 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
       }
       hintv = fmaxf(hintv, hint_decode(hraw, gen));   // 0 (no hint) when `last`
     }
-    seg_first = false;
+    ++seg_tile;
     if (last) {
       hintv = kNegInf;   // the next segment is another M-tile (other rows)
       published = kNegInf;
       shared_kth = kNegInf;
       pre = kNegInf;
-      seg_first = true;
+      seg_tile = 0;
       if constexpr (MODE != 1) {
         float* xr = xch + row_local * TC_XCH_FLOATS;
         for (int g = 1; g < NG; ++g) {
