@@ -40,7 +40,7 @@ __all__ = [
     "find_best", "kbest_sentences", "output_layer", "shard_partial", "beam_advance",
     "combine_partials", "online_stats", "argmax_1best", "argmax_1best_parallel",
     "compact", "decode_work", "beam_advance", "e4m3_decode", "quantize_rows_e4m3",
-    "dequant_rows_e4m3",
+    "dequant_rows_e4m3", "e2m1_decode", "quantize_rows_mxfp4", "dequant_rows_mxfp4",
 ]
 
 
@@ -332,6 +332,76 @@ def quantize_rows_e4m3(x):
 def dequant_rows_e4m3(codes, scale):
     """Exact fp64 value of code * scale (<= 4 + 24 significant bits)."""
     return e4m3_decode(codes) * np.asarray(scale, np.float64)[:, None]
+
+
+# ---------------------------------------------------------------- MXFP4 (f4)
+# OCP Microscaling (MX) formats, v1.0: MXFP4 = blocks of 32 E2M1 elements
+# sharing one E8M0 (power-of-two) scale. The block-scaled 4-bit analogue of
+# the paper's reduced-precision storage (section 2.3, P:264-268; SURVEY
+# section 8(f) f4, reading G20 in DESIGN.md).
+MX_BLOCK = 32
+E2M1_EMAX = 2          # largest E2M1 exponent (max magnitude 6 = 1.5 * 2^2)
+
+
+def e2m1_decode(codes):
+    """OCP FP4 E2M1 code (low 4 bits) -> exact value, from the format
+    definition: sign = bit 3, exponent e = bits 1-2 (bias 1), mantissa m =
+    bit 0; e = 0: (-1)^s m/2 (zero or the subnormal 0.5); otherwise
+    (-1)^s (1 + m/2) 2^(e-1). No infinities or NaN; max magnitude 6."""
+    c = np.asarray(codes, np.uint8).astype(np.int64) & 0xF
+    sgn = np.where(c & 0x8, -1.0, 1.0)
+    e = (c >> 1) & 0x3
+    m = (c & 0x1).astype(np.float64)
+    val = np.where(e == 0, m / 2.0, (1.0 + m / 2.0) * np.exp2(e.astype(np.float64) - 1))
+    return sgn * val
+
+
+def quantize_rows_mxfp4(x):
+    """MXFP4 quantisation of each row of x (fp32 values, H % 32 == 0), block
+    by block as the MX spec defines the conversion: for the 32 elements of a
+    block, the shared exponent is e = floor(log2(max |x|)) - E2M1_EMAX (an
+    all-zero block takes e = 0), stored as the E8M0 code e + 127 (clamped to
+    [0, 254]); each element becomes the E2M1 code nearest to x / 2^e (ties:
+    even code, i.e. even mantissa; magnitudes above 6 saturate to 6; the sign
+    is kept, so a negative value that rounds to zero gives -0 = code 8).
+    Plain loops; the nearest search is over the 8 magnitudes.
+    Returns (codes uint8 [R, H], one code per element, unpacked;
+             sexp uint8 [R, H / 32], the E8M0 codes)."""
+    x32 = np.asarray(x, np.float32)
+    R, H = x32.shape
+    assert H % MX_BLOCK == 0
+    mags = e2m1_decode(np.arange(8, dtype=np.uint8))          # 0, .5, 1, 1.5, 2, 3, 4, 6
+    codes = np.zeros((R, H), np.uint8)
+    sexp = np.zeros((R, H // MX_BLOCK), np.uint8)
+    for r in range(R):
+        for blk in range(H // MX_BLOCK):
+            v = x32[r, blk * MX_BLOCK:(blk + 1) * MX_BLOCK].astype(np.float64)
+            amax = float(np.abs(v).max())
+            if amax > 0:
+                _, E = np.frexp(amax)                          # amax = f 2^E, f in [0.5, 1)
+                e = int(E) - 1 - E2M1_EMAX
+            else:
+                e = 0
+            code_e = min(max(e + 127, 0), 254)
+            e = code_e - 127
+            sexp[r, blk] = code_e
+            for j in range(MX_BLOCK):
+                q = v[j] / 2.0 ** e                              # exact (power of two)
+                a = min(abs(q), 6.0)
+                d = np.abs(mags - a)
+                best = np.flatnonzero(d == d.min())
+                c = int(best[0]) if len(best) == 1 else int(best[best % 2 == 0][0])
+                if np.signbit(q):
+                    c |= 0x8
+                codes[r, blk * MX_BLOCK + j] = c
+    return codes, sexp
+
+
+def dequant_rows_mxfp4(codes, sexp):
+    """Exact fp64 value of code * 2^(sexp - 127), the scale repeated over its
+    block of 32 elements."""
+    scale = np.exp2(np.asarray(sexp, np.float64) - 127.0)
+    return e2m1_decode(codes) * np.repeat(scale, MX_BLOCK, axis=1)
 
 
 def decode_work(finish_steps, beam: int, mode: str) -> int:

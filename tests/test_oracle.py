@@ -423,3 +423,77 @@ def test_quantize_rows_e4m3_is_nearest_by_brute_force():
     rep = O.e4m3_decode(np.array([[0x38, 0x30, 0x7E, 0x01]], np.uint8)).astype(np.float32)
     c2, s2 = O.quantize_rows_e4m3(rep)
     assert np.array_equal(O.dequant_rows_e4m3(c2, s2), rep.astype(np.float64))
+
+
+# ---------------------------------------------------------------- MXFP4 (f4)
+def test_e2m1_decode_is_the_ocp_table():
+    """The OCP MX v1.0 E2M1 table: codes 0-7 = 0, 0.5, 1, 1.5, 2, 3, 4, 6;
+    codes 8-15 the same negated (8 = -0)."""
+    d = O.e2m1_decode(np.arange(16, dtype=np.uint8))
+    table = [0.0, 0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 6.0]
+    assert d[:8].tolist() == table
+    assert d[8:].tolist() == [-t for t in table]
+    assert np.signbit(d[8])
+    # only the low nibble is a code
+    assert O.e2m1_decode(np.array([0x37, 0xF9], np.uint8)).tolist() == [6.0, -0.5]
+
+
+def test_quantize_rows_mxfp4_is_nearest_by_brute_force():
+    """Per block: the scale puts the block max in [4, 8) x 2^e (the MX rule
+    e = floor(log2 amax) - 2); every code is the nearest of the 15 distinct
+    E2M1 values times 2^e to x (magnitudes above 6 x 2^e clamp to 6 x 2^e),
+    ties to the even code; an all-zero block has scale code 127."""
+    rng = np.random.default_rng(21)
+    x = (rng.normal(size=(5, 128)) * np.exp(rng.normal(size=(5, 1)) * 2)).astype(np.float32)
+    x[4, :32] = 0.0
+    x[3, 32:64] = np.float32(-1e-3)          # small negatives beside a large value round to -0
+    x[3, 40] = np.float32(5.0)
+    codes, sexp = O.quantize_rows_mxfp4(x)
+    assert codes.shape == x.shape and sexp.shape == (5, 4)
+    assert sexp[4, 0] == 127 and (codes[4, :32] & 0x7 == 0).all()
+    assert (np.delete(codes[3, 32:64], 8) == 0x8).all()
+    mags = np.array([0.0, 0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 6.0])
+    for r in range(5):
+        for blk in range(4):
+            v = x[r, 32 * blk:32 * blk + 32].astype(np.float64)
+            amax = np.abs(v).max()
+            if amax == 0:
+                continue
+            X = 2.0 ** (int(sexp[r, blk]) - 127)
+            assert 4.0 <= amax / X < 8.0
+            for j in range(32):
+                a = min(abs(v[j]) / X, 6.0)
+                c = int(codes[r, 32 * blk + j])
+                dist = np.abs(mags - a)
+                assert abs(mags[c & 7] - a) == dist.min()
+                if (dist == dist.min()).sum() > 1:   # a true tie: even code
+                    assert (c & 7) % 2 == 0
+                assert bool(c & 8) == bool(np.signbit(v[j]))
+    deq = O.dequant_rows_mxfp4(codes, sexp)
+    # error bound: half the E2M1 spacing at the value (0.25 below 2, 0.5 below
+    # 4, 1 up to 6) times 2^e; above 6 x 2^e the clamp
+    X = np.repeat(2.0 ** (sexp.astype(np.float64) - 127), 32, axis=1)
+    q = np.abs(x.astype(np.float64)) / X
+    half = np.where(q < 2, 0.25, np.where(q < 4, 0.5, 1.0))
+    err = np.abs(deq - x) / X
+    assert (err <= np.maximum(half, q - 6.0) + 1e-12).all()
+
+
+def test_quantize_rows_mxfp4_round_trip_and_special_blocks():
+    """Values on the E2M1 grid whose block max is 4 or 6 x 2^e round-trip
+    exactly; a constant block maps its value to code 6 (4 x 2^e) or 7."""
+    grid = np.array([0.0, 0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 6.0])
+    rng = np.random.default_rng(3)
+    rows = []
+    for e in (-9, -1, 0, 3):
+        v = rng.choice(grid, size=32) * rng.choice([-1.0, 1.0], size=32)
+        v[5] = 6.0
+        rows.append(v * 2.0 ** e)
+    x = np.concatenate([np.array(rows)], axis=1).astype(np.float32)
+    codes, sexp = O.quantize_rows_mxfp4(x)
+    assert np.array_equal(O.dequant_rows_mxfp4(codes, sexp), x.astype(np.float64))
+    assert sexp[:, 0].tolist() == [127 - 9, 127 - 1, 127, 127 + 3]
+    c1, s1 = O.quantize_rows_mxfp4(np.full((1, 32), 5.0, np.float32))   # 5 = 1.25 * 4: X = 1
+    assert s1[0, 0] == 127 and (c1 == 6).all()                          # 5 -> tie(4, 6) -> 4 (even)
+    c2, s2 = O.quantize_rows_mxfp4(np.full((1, 32), -7.0, np.float32))  # 7 / 1 -> clamp 6
+    assert s2[0, 0] == 127 and (c2 == 0xF).all()
