@@ -17,7 +17,8 @@
  *   + mini-batching (Alg. 2): remove finished hypotheses
  *     ("Remove h from b") by stable compaction, or fused with the
  *     beam reorder (amun_beam_advance); greedy argmax without the softmax
- *     (Alg. 5, amun_argmax); 8-bit storage (amun_*_e4m3).
+ *     (Alg. 5, amun_argmax); 8-bit storage (amun_*_e4m3) and
+ *     block-scaled 4-bit W (amun_*_mxfp4).
  *
  * Conventions (all entry points):
  *   - Every pointer argument that names device memory is a CUDA device
@@ -31,7 +32,9 @@
  *   - Layouts are row-major, C order. dtype AMUN_BF16 means IEEE bfloat16
  *     storage (fp32 accumulation); AMUN_F32 means fp32 storage and true fp32
  *     products (SIMT kernel); AMUN_E4M3 means OCP FP8 E4M3 codes with fp32
- *     per-row scales (fp32 accumulation; the *_e4m3 entry points).
+ *     per-row scales (fp32 accumulation; the *_e4m3 entry points);
+ *     AMUN_MXFP4 means E4M3 X with per-row scales and OCP MXFP4 W (E2M1
+ *     codes + one E8M0 scale per 32 elements; the *_mxfp4 entry points).
  *   - Errors: every call returns amun_status; no exception crosses the ABI.
  *     The message of the last failure on the calling thread is returned by
  *     amun_last_error(). Host-side validation happens before anything is
@@ -67,8 +70,10 @@ typedef enum amun_dtype {
   AMUN_F32 = 0,     /* fp32 X, W: SIMT kernel, true fp32 products */
   AMUN_BF16 = 1,    /* bf16 X, W: tcgen05 kind::f16 */
   AMUN_E4M3 = 2,    /* E4M3 codes + per-row fp32 scales: tcgen05 kind::f8f6f4 (*_e4m3 calls) */
-  AMUN_TF32X3 = 3   /* fp32 as 3xTF32 on tcgen05 kind::tf32: X, W passed pre-split by
+  AMUN_TF32X3 = 3,  /* fp32 as 3xTF32 on tcgen05 kind::tf32: X, W passed pre-split by
                        amun_split_tf32x3 as [N, 3H] / [V_local, 3H] fp32 rows */
+  AMUN_MXFP4 = 4    /* E4M3 X (per-row scales) x MXFP4 W (E2M1 + E8M0 per 32 K):
+                       tcgen05 kind::mxf8f6f4.block_scale (*_mxfp4 calls), H % 128 == 0 */
 } amun_dtype;
 
 /* Opaque plan: shapes, kernel choice, persistent-grid schedule and cached TMA
@@ -275,6 +280,63 @@ amun_status amun_split_tf32x3(const float* src, int R, int H, int role, float* d
  * device; dst [R, H] uint8, scale [R] fp32, device. One launch. */
 amun_status amun_quantize_e4m3(const void* src, amun_dtype src_dtype, int R, int H, uint8_t* dst,
                                float* scale, void* stream);
+
+/* Block-scaled 4-bit W (the 4-bit analogue of the paper's
+ * reduced-precision storage, section 2.3; reading G20 in
+ * DESIGN.md): W in the OCP Microscaling format MXFP4 (v1.0): each row's H
+ * values in blocks of 32 sharing one E8M0 scale 2^(c - 127), each element an
+ * E2M1 code (values 0, 0.5, 1, 1.5, 2, 3, 4, 6 and their negatives). X stays
+ * E4M3 with per-row fp32 scales (amun_quantize_e4m3). The logits are
+ *   L[r][v] = (sum_h x8[r][h] * e2m1(w4[v][h]) * 2^(sf[v][h/32] - 127)) * x_scale[r] + b[v]
+ * computed by tcgen05.mma kind::mxf8f6f4.block_scale (the block scales are
+ * applied inside the tensor core; fp32 accumulation), then the same
+ * softmax / k-best / merge as amun_output_layer. Plan: amun_ol_create(...,
+ * AMUN_MXFP4, ...), H % 128 == 0; single-CTA kernel, 128-column tiles.
+ *
+ * Layouts (device):
+ *   W4   [V_local, H/2] uint8: two codes per byte, element 2j in the low
+ *        nibble of byte j; 32-byte aligned (TMA 16U4_ALIGN16B).
+ *   w_sf amun_mxfp4_sf_bytes(V_local, H) bytes, 16-byte aligned, in the
+ *        scale-atom order the kernel copies to tensor memory unchanged: for
+ *        W row v and element h, the E8M0 code of block h/32 is at byte
+ *          ((v/128) * (H/128) + h/128) * 512 + 16 * (v%32) + 4 * ((v%128)/32) + (h%128)/32.
+ *        Rows beyond V_local in the last 128-row atom: any code (their W
+ *        rows read as zero and their columns are masked).
+ * Parity: the oracle computes on the exactly dequantised values
+ * (oracle.dequant_rows_mxfp4 / dequant_rows_e4m3). */
+size_t amun_mxfp4_sf_bytes(int R, int H);   /* 0 if H % 128 != 0 or R < 0 */
+/* Quantise R rows of H values (fp32 or bf16, device) to MXFP4 in the layouts
+ * above: shared exponent e = floor(log2(max |x| of the block)) - 2 (E8M0
+ * code e + 127 clamped to [0, 254]; 127 for an all-zero block), code =
+ * round-to-nearest-even E2M1 of x * 2^-e, saturating at +-6, sign kept (-0
+ * possible); equals oracle.quantize_rows_mxfp4 bit for bit. H % 128 == 0;
+ * codes [R, H/2] (2-byte aligned), sf amun_mxfp4_sf_bytes(R, H) bytes. One
+ * launch. */
+amun_status amun_quantize_mxfp4(const void* src, amun_dtype src_dtype, int R, int H,
+                                uint8_t* codes, uint8_t* sf, void* stream);
+/* Steps 1-4 for AMUN_MXFP4 plans: arguments as amun_output_layer_e4m3 with
+ * W4 / w_sf for W8 / w_scale. One launch (the merge in the fused kernel's
+ * tail), two with AMUN_TAIL=off. */
+amun_status amun_output_layer_mxfp4(amun_ol* plan, const uint8_t* X8, const float* x_scale,
+                                    const uint8_t* W4, const uint8_t* w_sf, const float* b,
+                                    const float* prev_cost, const int32_t* beam_offsets, int N,
+                                    int S, const int32_t* k_per_sentence, int k, int64_t* out_idx,
+                                    float* out_cost, void* workspace, void* stream);
+/* Stage 1 alone (variant 0; then amun_ol_select), or the bare-GEMM (2) /
+ * no-k-best (3) benchmark builds. */
+amun_status amun_ol_scores_mxfp4(amun_ol* plan, const uint8_t* X8, const float* x_scale,
+                                 const uint8_t* W4, const uint8_t* w_sf, const float* b, int N,
+                                 int variant, void* workspace, void* stream);
+/* Greedy argmax (Alg. 5) for AMUN_MXFP4 plans: as amun_argmax, out_logit =
+ * L[r][token] as defined above. One launch. */
+amun_status amun_argmax_mxfp4(amun_ol* plan, const uint8_t* X8, const float* x_scale,
+                              const uint8_t* W4, const uint8_t* w_sf, const float* b, int N,
+                              int64_t* out_token, float* out_logit, void* workspace,
+                              void* stream);
+/* Test hook (as amun_debug_logits): L [N, V_local] fp32 of an AMUN_MXFP4 plan. */
+amun_status amun_debug_logits_mxfp4(amun_ol* plan, const uint8_t* X8, const float* x_scale,
+                                    const uint8_t* W4, const uint8_t* w_sf, const float* b, int N,
+                                    float* logits, void* workspace, void* stream);
 
 /* Test hook: steps 1-2 only. Writes the biased logits of the same tcgen05
  * (bf16) or SIMT (f32) GEMM to logits [N, V_local] fp32 (these never reach

@@ -20,7 +20,8 @@ from ._lib import AMUN_MAX_COLUMNS, AMUN_MAX_K, AmunError, check
 
 _L = _lib.load()
 
-__all__ = ["OutputLayer", "compact", "compact_sentences", "beam_advance", "quantize_e4m3", "split_tf32x3", "AmunError", "AMUN_MAX_K",
+__all__ = ["OutputLayer", "compact", "compact_sentences", "beam_advance", "quantize_e4m3",
+           "quantize_mxfp4", "mxfp4_sf_bytes", "split_tf32x3", "AmunError", "AMUN_MAX_K",
            "AMUN_MAX_COLUMNS", "lib_path"]
 
 lib_path = _lib.LIB_PATH
@@ -65,13 +66,14 @@ class OutputLayer:
         self.V_total = V_local if V_total is None else V_total
         self.dtype = dtype
         self.tdtype = {"bf16": torch.bfloat16, "f32": torch.float32, "e4m3": torch.uint8,
-                       "tf32x3": torch.float32}[dtype]
+                       "tf32x3": torch.float32, "mxfp4": torch.uint8}[dtype]
         self.K = 3 * H if dtype == "tf32x3" else H   # columns of X / W rows as passed
         self.k_max, self.max_rows, self.max_sentences = k_max, max_rows, max_sentences
         h = ctypes.c_void_p()
         check(_L.amun_ol_create(ctypes.byref(h), H, V_local, v_offset, self.V_total,
                                 {"bf16": _lib.AMUN_BF16, "f32": _lib.AMUN_F32,
-                                 "e4m3": _lib.AMUN_E4M3, "tf32x3": _lib.AMUN_TF32X3}[dtype],
+                                 "e4m3": _lib.AMUN_E4M3, "tf32x3": _lib.AMUN_TF32X3,
+                                 "mxfp4": _lib.AMUN_MXFP4}[dtype],
                                 k_max, max_rows, max_sentences, dev.index or 0))
         self._h = h
         self.stride = _L.amun_ol_partial_stride(h)
@@ -210,6 +212,57 @@ class OutputLayer:
                                   _ptr(b), N, _ptr(out_token), _ptr(out_logit),
                                   _ptr(self.workspace), _stream(self.device)))
         return out_token, out_logit
+
+    # ------------------------------------------------ MXFP4 W (amun_*_mxfp4)
+    def _check_mxfp4(self, X8, xs, W4, w_sf, b):
+        N = X8.shape[0]
+        _need(X8, "X8", torch.uint8, self.device, (N, self.H))
+        _need(W4, "W4", torch.uint8, self.device, (self.V_local, self.H // 2))
+        _need(w_sf, "w_sf", torch.uint8, self.device, (_L.amun_mxfp4_sf_bytes(self.V_local, self.H),))
+        _need(xs, "x_scale", torch.float32, self.device, (N,))
+        _need(b, "b", torch.float32, self.device, (self.V_local,))
+        return N
+
+    def call_mxfp4(self, X8, x_scale, W4, w_sf, b, prev_cost, beam_offsets, k: int,
+                   k_per_sentence=None, out_idx=None, out_cost=None):
+        """Steps 1-4 for plan dtype "mxfp4": X8 E4M3 codes + per-row scales
+        (quantize_e4m3), W4 / w_sf from quantize_mxfp4. Returns (idx, cost)."""
+        N = self._check_mxfp4(X8, x_scale, W4, w_sf, b)
+        S = self._check_select(prev_cost, beam_offsets, N, k_per_sentence)
+        out_idx, out_cost = self._outputs(S, k, out_idx, out_cost)
+        check(_L.amun_output_layer_mxfp4(self._h, _ptr(X8), _ptr(x_scale), _ptr(W4), _ptr(w_sf),
+                                         _ptr(b), _ptr(prev_cost), _ptr(beam_offsets), N, S,
+                                         _ptr(k_per_sentence), k, _ptr(out_idx), _ptr(out_cost),
+                                         _ptr(self.workspace), _stream(self.device)))
+        return out_idx, out_cost
+
+    def scores_mxfp4(self, X8, x_scale, W4, w_sf, b, variant: int = 0):
+        """MXFP4 stage 1 (variant 0), or the bare-GEMM (2) / no-k-best (3) builds."""
+        N = self._check_mxfp4(X8, x_scale, W4, w_sf, b)
+        check(_L.amun_ol_scores_mxfp4(self._h, _ptr(X8), _ptr(x_scale), _ptr(W4), _ptr(w_sf),
+                                      _ptr(b), N, variant, _ptr(self.workspace),
+                                      _stream(self.device)))
+
+    def argmax_mxfp4(self, X8, x_scale, W4, w_sf, b, out_token=None, out_logit=None):
+        """MXFP4 greedy argmax (Alg. 5): (token [N] int64, logit [N] fp32)."""
+        N = self._check_mxfp4(X8, x_scale, W4, w_sf, b)
+        if out_token is None:
+            out_token = torch.empty(N, dtype=torch.int64, device=self.device)
+        if out_logit is None:
+            out_logit = torch.empty(N, dtype=torch.float32, device=self.device)
+        check(_L.amun_argmax_mxfp4(self._h, _ptr(X8), _ptr(x_scale), _ptr(W4), _ptr(w_sf),
+                                   _ptr(b), N, _ptr(out_token), _ptr(out_logit),
+                                   _ptr(self.workspace), _stream(self.device)))
+        return out_token, out_logit
+
+    def debug_logits_mxfp4(self, X8, x_scale, W4, w_sf, b):
+        """Test hook: the biased logits [N, V_local] fp32 of the MXFP4 GEMM."""
+        N = self._check_mxfp4(X8, x_scale, W4, w_sf, b)
+        out = torch.empty((N, self.V_local), dtype=torch.float32, device=self.device)
+        check(_L.amun_debug_logits_mxfp4(self._h, _ptr(X8), _ptr(x_scale), _ptr(W4), _ptr(w_sf),
+                                         _ptr(b), N, _ptr(out), _ptr(self.workspace),
+                                         _stream(self.device)))
+        return out
 
     def scores(self, X, W, b):
         """Stage 1 only (fused GEMM + bias + online softmax stats + row k-best)."""
@@ -402,6 +455,31 @@ def quantize_e4m3(src, out=None, scale=None):
     check(_L.amun_quantize_e4m3(_ptr(src), _lib.AMUN_BF16 if src.dtype == torch.bfloat16 else _lib.AMUN_F32,
                                 R, H, _ptr(out), _ptr(scale), _stream(dev)))
     return out, scale
+
+
+def mxfp4_sf_bytes(R: int, H: int) -> int:
+    """Bytes of the MXFP4 scale-atom array of R rows of H values (amun.h)."""
+    return int(_L.amun_mxfp4_sf_bytes(R, H))
+
+
+def quantize_mxfp4(src, codes=None, sf=None):
+    """OCP MXFP4 quantisation on the GPU (amun_quantize_mxfp4): src [R, H]
+    fp32 or bf16, H % 128 == 0 -> (codes [R, H/2] uint8, two E2M1 codes per
+    byte, low nibble first; sf [mxfp4_sf_bytes(R, H)] uint8 E8M0 scales in the
+    kernel's atom layout)."""
+    if src.dim() != 2 or not src.is_contiguous() or src.dtype not in (torch.float32, torch.bfloat16):
+        raise ValueError("src must be a contiguous 2-D fp32 or bf16 tensor")
+    R, H = src.shape
+    dev = src.device
+    if codes is None:
+        codes = torch.empty((R, H // 2), dtype=torch.uint8, device=dev)
+    if sf is None:
+        sf = torch.empty(mxfp4_sf_bytes(R, H), dtype=torch.uint8, device=dev)
+    _need(codes, "codes", torch.uint8, dev, (R, H // 2))
+    _need(sf, "sf", torch.uint8, dev, (mxfp4_sf_bytes(R, H),))
+    check(_L.amun_quantize_mxfp4(_ptr(src), _lib.AMUN_BF16 if src.dtype == torch.bfloat16 else _lib.AMUN_F32,
+                                 R, H, _ptr(codes), _ptr(sf), _stream(dev)))
+    return codes, sf
 
 
 def split_tf32x3(src, role: str, out=None):

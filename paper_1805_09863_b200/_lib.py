@@ -13,7 +13,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("AMUN_LIB", os.path.join(_HERE, "libamun.so"))
 
 AMUN_OK, AMUN_EINVAL, AMUN_EUNSUPPORTED, AMUN_ECUDA = 0, 1, 2, 3
-AMUN_F32, AMUN_BF16, AMUN_E4M3, AMUN_TF32X3 = 0, 1, 2, 3
+AMUN_F32, AMUN_BF16, AMUN_E4M3, AMUN_TF32X3, AMUN_MXFP4 = 0, 1, 2, 3, 4
 AMUN_MAX_K = 16
 AMUN_MAX_COLUMNS = 16
 
@@ -28,6 +28,8 @@ EXPORTS = [
     "amun_oneshot_free", "amun_oneshot_open", "amun_oneshot_close", "amun_output_layer_oneshot",
     "amun_output_layer_oneshot_emulated", "amun_sentence_alive", "amun_ol_workspace_init",
     "amun_debug_timeline", "amun_ol_launches_per_call", "amun_oneshot_error",
+    "amun_mxfp4_sf_bytes", "amun_quantize_mxfp4", "amun_output_layer_mxfp4", "amun_ol_scores_mxfp4",
+    "amun_argmax_mxfp4", "amun_debug_logits_mxfp4",
 ]
 AMUN_ONESHOT_MAX_G = 8
 
@@ -86,6 +88,13 @@ def load() -> ctypes.CDLL:
         "amun_output_layer_partial_e4m3": (st, [vp, vp, vp, vp, vp, vp, i32, vp, vp, vp]),
         "amun_argmax_e4m3": (st, [vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, vp]),
         "amun_split_tf32x3": (st, [vp, i32, i32, i32, vp, vp]),
+        "amun_mxfp4_sf_bytes": (sz, [i32, i32]),
+        "amun_quantize_mxfp4": (st, [vp, i32, i32, i32, vp, vp, vp]),
+        "amun_output_layer_mxfp4": (st, [vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, vp, i32, vp, vp,
+                                         vp, vp]),
+        "amun_ol_scores_mxfp4": (st, [vp, vp, vp, vp, vp, vp, i32, i32, vp, vp]),
+        "amun_argmax_mxfp4": (st, [vp, vp, vp, vp, vp, vp, i32, vp, vp, vp, vp]),
+        "amun_debug_logits_mxfp4": (st, [vp, vp, vp, vp, vp, vp, i32, vp, vp, vp]),
         "amun_oneshot_buffer_bytes": (sz, [vp, i32]),
         "amun_sentence_alive": (st, [vp, i32, vp, vp, vp]),
         "amun_oneshot_alloc": (st, [vp, i32, ctypes.POINTER(vp), vp]),

@@ -119,8 +119,6 @@ struct amun_ol {
   size_t flags_bytes;              // (reserved after the counters; 0)
   const void* hint_ws = nullptr;   // workspace whose hint / counter / flag region is initialised
   int tail_mode = 0;    // env AMUN_TAIL: 0 fused tail (one launch per call), 1 "off" (separate merge kernel)
-  long long pf_bytes = 0;   // env AMUN_PF_BYTES: entry L2 prefetch of W per CTA (0 = off;
-                            // measured slower at greedy and beam)
   unsigned long long* tl = nullptr;   // amun_debug_timeline buffer (device), else NULL
   int ng_override = 0;  // env AMUN_NG: 2 or 4 epilogue warpgroups (experiments)
   int taper = 0;        // env AMUN_TAPER=1: narrow final tiles (experiments; measured slower:
@@ -143,20 +141,26 @@ namespace {
 // Tensor map of a row-major [rows, H] bf16 matrix, box [box_rows, 64],
 // 128-byte swizzle (matches sdesc_k_sw128), OOB rows/columns read as zero.
 amun_status encode_map(amun_ol* pl, const void* ptr, long long rows, int box_rows, int kbytes,
-                       CUtensorMap* out) {
+                       bool is_w, CUtensorMap* out) {
   EncodeTiledFn enc = get_encode_fn();
   if (!enc) return fail(AMUN_ECUDA, "cuTensorMapEncodeTiled entry point unavailable");
   // box rows of `kbytes` bytes (128: 64 bf16, 128 e4m3 codes or 32 fp32 of the
-  // 3H-wide tf32x3 rows; 64: half of that), swizzled to match sdesc_k<kbytes>
-  const bool f8 = pl->dtype == AMUN_E4M3, t3 = pl->dtype == AMUN_TF32X3;
+  // 3H-wide tf32x3 rows; 64: half of that), swizzled to match sdesc_k<kbytes>.
+  // MXFP4 W: packed E2M1 pairs in HBM (H/2 bytes per row); the 16U4_ALIGN16B
+  // type spreads each 8 bytes (16 codes) over 16 bytes of shared memory, the
+  // layout kind::mxf8f6f4 reads, so a box of 128 codes fills 128 bytes.
+  const bool f4 = pl->dtype == AMUN_MXFP4 && is_w;
+  const bool f8 = pl->dtype == AMUN_E4M3 || (pl->dtype == AMUN_MXFP4 && !is_w);
+  const bool t3 = pl->dtype == AMUN_TF32X3;
   const cuuint64_t K = t3 ? 3ull * pl->H : (cuuint64_t)pl->H;
-  const cuuint32_t esz = f8 ? 1 : t3 ? 4 : 2;
+  const cuuint32_t esz = f8 || f4 ? 1 : t3 ? 4 : 2;   // smem bytes per element
   cuuint64_t dims[2] = {K, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {K * esz};
+  cuuint64_t strides[1] = {f4 ? K / 2 : K * esz};
   cuuint32_t box[2] = {(cuuint32_t)kbytes / esz, (cuuint32_t)box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = enc(out,
-                   f8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                   f4 ? CU_TENSOR_MAP_DATA_TYPE_16U4_ALIGN16B
+                   : f8 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
                       : t3 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
                    2, const_cast<void*>(ptr), dims, strides,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -168,6 +172,7 @@ amun_status encode_map(amun_ol* pl, const void* ptr, long long rows, int box_row
 
 amun_status get_map(amun_ol* pl, MapEntry* cache, int n, int& next, const void* ptr,
                     long long rows, int box_rows, int kbytes, const CUtensorMap** out) {
+  const bool is_w = cache == pl->wmaps;
   for (int i = 0; i < n; ++i)
     if (cache[i].ptr == ptr && cache[i].rows == rows && cache[i].box_rows == box_rows &&
         cache[i].kbytes == kbytes) {
@@ -176,7 +181,7 @@ amun_status get_map(amun_ol* pl, MapEntry* cache, int n, int& next, const void* 
     }
   MapEntry& e = cache[next];
   next = (next + 1) % n;
-  amun_status s = encode_map(pl, ptr, rows, box_rows, kbytes, &e.map);
+  amun_status s = encode_map(pl, ptr, rows, box_rows, kbytes, is_w, &e.map);
   if (s != AMUN_OK) {
     e.ptr = nullptr;
     return s;
@@ -208,7 +213,8 @@ Schedule make_schedule(const amun_ol* pl, int N, int* grid) {
   const bool pairs = use_pairs(pl, N);
   const long long G = pairs ? pl->num_sms / 2 : pl->num_sms;
   const long long n_mt = cdiv(N > 0 ? N : 1, pairs ? 256 : 128);
-  Schedule s = schedule_for(n_mt, cdiv(pl->V_local, 16) * 16, G);
+  const long long align = pl->dtype == AMUN_MXFP4 ? TC_BN_F4 : 16;   // scale atoms: 128 W rows
+  Schedule s = schedule_for(n_mt, cdiv(pl->V_local, align) * align, G, align);
   const int units = (int)cdiv((n_mt - 1) * s.band + s.Vp, s.C);
   *grid = pairs ? 2 * units : units;
   return s;
@@ -272,7 +278,7 @@ amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b
     if (pl->mc > 1 && !pairs && !N_dev && mode != 1 && sch.band != sch.Vp &&
         cdiv(N, TC_BM) == pl->mc && grid % pl->mc == 0)
       mc = pl->mc;
-    const int wbox = mc > 1 ? 64 : pl->wbox;
+    const int wbox = pl->dtype == AMUN_MXFP4 ? TC_BN_F4 : mc > 1 ? 64 : pl->wbox;
     amun_status s = get_map(pl, pl->xmaps, 4, pl->xnext, X, N, a_rows, kbytes, &mx);
     if (s != AMUN_OK) return s;
     s = get_map(pl, pl->wmaps, 8, pl->wnext, W, pl->V_local, pairs ? TC_BN / 2 : wbox, kbytes,
@@ -284,11 +290,15 @@ amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b
     tp.N = N;
     tp.V_local = pl->V_local;
     tp.v_offset = pl->v_offset;
-    const long long kbytes_total = pl->dtype == AMUN_E4M3 ? pl->H
+    // smem bytes of K per row (mxfp4 W: one byte per code once unpacked)
+    const long long kbytes_total = pl->dtype == AMUN_E4M3 || pl->dtype == AMUN_MXFP4 ? pl->H
                                  : pl->dtype == AMUN_TF32X3 ? 12LL * pl->H : 2LL * pl->H;
     tp.n_kblk = (int)cdiv(kbytes_total, kbytes);
     tp.x_scale = x_scale;
-    tp.w_scale = w_scale;
+    if (pl->dtype == AMUN_MXFP4)   // (the mxfp4 entry points pass W's block scales here)
+      tp.w_sf = reinterpret_cast<const uint8_t*>(w_scale);
+    else
+      tp.w_scale = w_scale;
     tp.a_box_bytes = a_rows * kbytes;   // kbytes of K per row (every dtype)
     tp.sch = sch;
     tp.bias = b;
@@ -328,12 +338,6 @@ amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b
     tp.mc = mc;
     tp.pdl = pairs ? 0 : pl->pdl;
     tp.mma_only = pl->mma_only;
-    if (pl->pf_bytes > 0 && !N_dev) {
-      tp.pf_w = static_cast<const char*>(W);
-      tp.pf_row_bytes = pl->dtype == AMUN_E4M3 ? pl->H : pl->dtype == AMUN_TF32X3 ? 12LL * pl->H
-                                                                                  : 2LL * pl->H;
-      tp.pf_max_bytes = pl->pf_bytes;
-    }
     if ((mode == 0 || mode == 4) && pl->hint_ws != workspace) {
       // hint words carry the launch generation (advanced on the device by the
       // kernel itself); zero words + counters + tail flags once per workspace
@@ -445,6 +449,9 @@ bool use_tail(const amun_ol* pl, int N) {
   return pl->tail_mode != 1 && pl->dtype != AMUN_F32 && N > 0;
 }
 
+// Plans whose entry points carry scales (*_e4m3, *_mxfp4).
+bool scaled_plan(const amun_ol* pl) { return pl->dtype == AMUN_E4M3 || pl->dtype == AMUN_MXFP4; }
+
 }  // namespace
 
 namespace {
@@ -499,13 +506,16 @@ amun_status amun_ol_create(amun_ol** plan, int H, int V_local, int v_offset, int
                            int device) {
   if (!plan) return fail(AMUN_EINVAL, "NULL plan pointer");
   *plan = nullptr;
-  if (dtype != AMUN_F32 && dtype != AMUN_BF16 && dtype != AMUN_E4M3 && dtype != AMUN_TF32X3)
+  if (dtype != AMUN_F32 && dtype != AMUN_BF16 && dtype != AMUN_E4M3 && dtype != AMUN_TF32X3 &&
+      dtype != AMUN_MXFP4)
     return fail(AMUN_EINVAL, "unknown dtype %d", (int)dtype);
   if (H < 1) return fail(AMUN_EINVAL, "H=%d must be >= 1", H);
   if (dtype == AMUN_BF16 && H % 8 != 0) return fail(AMUN_EINVAL, "bf16 needs H %% 8 == 0 (H=%d)", H);
   if ((dtype == AMUN_F32 || dtype == AMUN_TF32X3) && H % 4 != 0)
     return fail(AMUN_EINVAL, "f32 / tf32x3 need H %% 4 == 0 (H=%d)", H);
   if (dtype == AMUN_E4M3 && H % 16 != 0) return fail(AMUN_EINVAL, "e4m3 needs H %% 16 == 0 (H=%d)", H);
+  if (dtype == AMUN_MXFP4 && H % 128 != 0)
+    return fail(AMUN_EINVAL, "mxfp4 needs H %% 128 == 0 (H=%d)", H);
   if (V_local < 1) return fail(AMUN_EINVAL, "V_local=%d must be >= 1", V_local);
   if (v_offset < 0 || V_total < 1 || (long long)v_offset + V_local > V_total)
     return fail(AMUN_EINVAL, "need 0 <= v_offset and v_offset + V_local <= V_total");
@@ -564,8 +574,6 @@ amun_status amun_ol_create(amun_ol** plan, int H, int V_local, int v_offset, int
     const char* tp = getenv("AMUN_TAPER");
     if (tp) pl->taper = atoi(tp) != 0;
     if (pl->taper) pl->wbox = 64;   // narrow tiles load only their own rows
-    const char* f = getenv("AMUN_PF_BYTES");
-    if (f) pl->pf_bytes = atoll(f);
   }
   const long long slots = pl->num_sms + cdiv(max_rows > 0 ? max_rows : 1, 128) + 1;
   pl->slots_bytes = (size_t)cdiv(slots * 128LL * pl->stride * 4, 256) * 256;
@@ -605,8 +613,8 @@ int amun_ol_launches_per_call(const amun_ol* plan, int call) {
 
 amun_status amun_ol_scores(amun_ol* plan, const void* X, const void* W, const float* b, int N,
                            void* workspace, void* stream) {
-  if (plan && plan->dtype == AMUN_E4M3)
-    return fail(AMUN_EINVAL, "e4m3 plans take the *_e4m3 entry points (they carry the scales)");
+  if (plan && scaled_plan(plan))
+    return fail(AMUN_EINVAL, "e4m3 / mxfp4 plans take their own entry points (they carry the scales)");
   amun_status s = check_score_args(plan, X, W, b, N, workspace);
   if (s != AMUN_OK) return s;
   return run_scores(plan, X, W, b, N, workspace, nullptr, static_cast<cudaStream_t>(stream), 0);
@@ -646,7 +654,7 @@ amun_status amun_output_layer(amun_ol* plan, const void* X, const void* W, const
   if (s != AMUN_OK) return s;
   s = check_select_args(plan, prev_cost, beam_offsets, N, S, k, out_idx, out_cost);
   if (s != AMUN_OK) return s;
-  if (plan->dtype != AMUN_E4M3 && use_tail(plan, N)) {
+  if (!scaled_plan(plan) && use_tail(plan, N)) {
     const MergeParams mp = sent_merge(plan, prev_cost, beam_offsets, N, S, k_per_sentence, k,
                                       out_idx, out_cost);
     return run_scores(plan, X, W, b, N, workspace, nullptr, static_cast<cudaStream_t>(stream), 0,
@@ -704,8 +712,8 @@ amun_status amun_output_layer_dev(amun_ol* plan, const void* X, const void* W, c
 amun_status amun_output_layer_partial(amun_ol* plan, const void* X, const void* W,
                                       const float* b, int N, float* partial, void* workspace,
                                       void* stream) {
-  if (plan && plan->dtype == AMUN_E4M3)
-    return fail(AMUN_EINVAL, "e4m3 plans take the *_e4m3 entry points (they carry the scales)");
+  if (plan && scaled_plan(plan))
+    return fail(AMUN_EINVAL, "e4m3 / mxfp4 plans take their own entry points (they carry the scales)");
   return partial_impl(plan, X, W, b, N, partial, workspace, stream, nullptr, nullptr);
 }
 
@@ -750,8 +758,8 @@ amun_status amun_merge_partials(amun_ol* plan, const float* partials, int G,
 
 amun_status amun_debug_logits(amun_ol* plan, const void* X, const void* W, const float* b, int N,
                               float* logits, void* workspace, void* stream) {
-  if (plan && plan->dtype == AMUN_E4M3)
-    return fail(AMUN_EINVAL, "e4m3 plans take the *_e4m3 entry points (they carry the scales)");
+  if (plan && scaled_plan(plan))
+    return fail(AMUN_EINVAL, "e4m3 / mxfp4 plans take their own entry points (they carry the scales)");
   amun_status s = check_score_args(plan, X, W, b, N, workspace);
   if (s != AMUN_OK) return s;
   if (N > 0 && !logits) return fail(AMUN_EINVAL, "NULL logits");
@@ -793,8 +801,8 @@ amun_status argmax_impl(amun_ol* plan, const void* X, const void* W, const float
 
 amun_status amun_argmax(amun_ol* plan, const void* X, const void* W, const float* b, int N,
                         int64_t* out_token, float* out_logit, void* workspace, void* stream) {
-  if (plan && plan->dtype == AMUN_E4M3)
-    return fail(AMUN_EINVAL, "e4m3 plans take the *_e4m3 entry points (they carry the scales)");
+  if (plan && scaled_plan(plan))
+    return fail(AMUN_EINVAL, "e4m3 / mxfp4 plans take their own entry points (they carry the scales)");
   return argmax_impl(plan, X, W, b, N, out_token, out_logit, workspace, stream, nullptr, nullptr);
 }
 
@@ -845,6 +853,105 @@ amun_status amun_output_layer_e4m3(amun_ol* plan, const uint8_t* X8, const float
   if (s != AMUN_OK) return s;
   return amun_ol_select(plan, workspace, prev_cost, beam_offsets, N, S, k_per_sentence, k,
                         out_idx, out_cost, stream);
+}
+
+// ------------------------------------------------------------ MXFP4 W (f4)
+namespace {
+amun_status check_mxfp4(const amun_ol* plan, const float* x_scale, const void* W4,
+                        const uint8_t* w_sf, int N) {
+  if (!plan) return fail(AMUN_EINVAL, "NULL plan");
+  if (plan->dtype != AMUN_MXFP4) return fail(AMUN_EINVAL, "plan dtype is not AMUN_MXFP4");
+  if (N > 0 && (!x_scale || !w_sf)) return fail(AMUN_EINVAL, "NULL x_scale / w_sf");
+  if (N > 0 && (reinterpret_cast<uintptr_t>(W4) & 31) != 0)
+    return fail(AMUN_EINVAL, "W4 must be 32-byte aligned (TMA 16U4_ALIGN16B)");
+  if (N > 0 && !aligned16(w_sf)) return fail(AMUN_EINVAL, "w_sf must be 16-byte aligned");
+  return AMUN_OK;
+}
+// the SF pointer travels in run_scores' w_scale slot (run_scores: tp.w_sf)
+inline const float* sf_arg(const uint8_t* w_sf) { return reinterpret_cast<const float*>(w_sf); }
+}  // namespace
+
+size_t amun_mxfp4_sf_bytes(int R, int H) {
+  if (R < 0 || H < 128 || H % 128 != 0) return 0;
+  return (size_t)cdiv(R, 128) * (size_t)(H / 128) * 512;
+}
+
+amun_status amun_quantize_mxfp4(const void* src, amun_dtype src_dtype, int R, int H,
+                                uint8_t* codes, uint8_t* sf, void* stream) {
+  if (src_dtype != AMUN_F32 && src_dtype != AMUN_BF16)
+    return fail(AMUN_EINVAL, "src_dtype must be AMUN_F32 or AMUN_BF16");
+  if (R < 0 || H < 128 || H % 128 != 0) return fail(AMUN_EINVAL, "need R >= 0, H %% 128 == 0");
+  if (R == 0) return AMUN_OK;
+  if (!src || !codes || !sf) return fail(AMUN_EINVAL, "NULL src / codes / sf");
+  if ((reinterpret_cast<uintptr_t>(codes) & 1) != 0) return fail(AMUN_EINVAL, "codes must be 2-byte aligned");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const long long tasks = cdiv(R, 128) * 128 * (H / 128);
+  const unsigned grid = (unsigned)std::min<long long>(cdiv(tasks, QZ_THREADS / 32), 4096);
+  if (src_dtype == AMUN_BF16)
+    quantize_mxfp4_kernel<true><<<grid, QZ_THREADS, 0, st>>>(src, R, H, codes, sf);
+  else
+    quantize_mxfp4_kernel<false><<<grid, QZ_THREADS, 0, st>>>(src, R, H, codes, sf);
+  CUDA_TRY(cudaGetLastError());
+  return AMUN_OK;
+}
+
+amun_status amun_ol_scores_mxfp4(amun_ol* plan, const uint8_t* X8, const float* x_scale,
+                                 const uint8_t* W4, const uint8_t* w_sf, const float* b, int N,
+                                 int variant, void* workspace, void* stream) {
+  amun_status s = check_score_args(plan, X8, W4, b, N, workspace);
+  if (s != AMUN_OK) return s;
+  s = check_mxfp4(plan, x_scale, W4, w_sf, N);
+  if (s != AMUN_OK) return s;
+  if (variant != 0 && variant != 2 && variant != 3)
+    return fail(AMUN_EINVAL, "variant %d not in {0, 2, 3}", variant);
+  return run_scores(plan, X8, W4, b, N, workspace, nullptr, static_cast<cudaStream_t>(stream),
+                    variant, nullptr, x_scale, sf_arg(w_sf));
+}
+
+amun_status amun_output_layer_mxfp4(amun_ol* plan, const uint8_t* X8, const float* x_scale,
+                                    const uint8_t* W4, const uint8_t* w_sf, const float* b,
+                                    const float* prev_cost, const int32_t* beam_offsets, int N,
+                                    int S, const int32_t* k_per_sentence, int k, int64_t* out_idx,
+                                    float* out_cost, void* workspace, void* stream) {
+  if (!plan) return fail(AMUN_EINVAL, "NULL plan");
+  amun_status s = check_select_args(plan, prev_cost, beam_offsets, N, S, k, out_idx, out_cost);
+  if (s != AMUN_OK) return s;
+  if (use_tail(plan, N)) {
+    s = check_score_args(plan, X8, W4, b, N, workspace);
+    if (s != AMUN_OK) return s;
+    s = check_mxfp4(plan, x_scale, W4, w_sf, N);
+    if (s != AMUN_OK) return s;
+    const MergeParams mp = sent_merge(plan, prev_cost, beam_offsets, N, S, k_per_sentence, k,
+                                      out_idx, out_cost);
+    return run_scores(plan, X8, W4, b, N, workspace, nullptr, static_cast<cudaStream_t>(stream), 0,
+                      nullptr, x_scale, sf_arg(w_sf), TAIL_SENT, &mp);
+  }
+  s = amun_ol_scores_mxfp4(plan, X8, x_scale, W4, w_sf, b, N, 0, workspace, stream);
+  if (s != AMUN_OK) return s;
+  return amun_ol_select(plan, workspace, prev_cost, beam_offsets, N, S, k_per_sentence, k,
+                        out_idx, out_cost, stream);
+}
+
+amun_status amun_argmax_mxfp4(amun_ol* plan, const uint8_t* X8, const float* x_scale,
+                              const uint8_t* W4, const uint8_t* w_sf, const float* b, int N,
+                              int64_t* out_token, float* out_logit, void* workspace,
+                              void* stream) {
+  amun_status s = check_mxfp4(plan, x_scale, W4, w_sf, N);
+  if (s != AMUN_OK) return s;
+  return argmax_impl(plan, X8, W4, b, N, out_token, out_logit, workspace, stream, x_scale,
+                     sf_arg(w_sf));
+}
+
+amun_status amun_debug_logits_mxfp4(amun_ol* plan, const uint8_t* X8, const float* x_scale,
+                                    const uint8_t* W4, const uint8_t* w_sf, const float* b, int N,
+                                    float* logits, void* workspace, void* stream) {
+  amun_status s = check_score_args(plan, X8, W4, b, N, workspace);
+  if (s != AMUN_OK) return s;
+  s = check_mxfp4(plan, x_scale, W4, w_sf, N);
+  if (s != AMUN_OK) return s;
+  if (N > 0 && !logits) return fail(AMUN_EINVAL, "NULL logits");
+  return run_scores(plan, X8, W4, b, N, workspace, logits, static_cast<cudaStream_t>(stream), 1,
+                    nullptr, x_scale, sf_arg(w_sf));
 }
 
 amun_status amun_quantize_e4m3(const void* src, amun_dtype src_dtype, int R, int H, uint8_t* dst,

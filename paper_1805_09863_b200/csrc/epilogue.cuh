@@ -415,15 +415,19 @@ struct Schedule {
 // boundaries, so concurrent CTAs share W tiles in L2) when they fill >= 90%
 // of G, else an equal flattened split. Shared by the host (plan) and the
 // device (amun_output_layer_dev, where N is only known on the device).
-__host__ __device__ inline Schedule schedule_for(long long n_mt, long long Vp, long long G) {
+// `align` (16, or 128 for MXFP4 plans, whose scale atoms cover 128 W rows):
+// Vp and every CTA range start are multiples of it, so every tile starts on
+// an aligned column.
+__host__ __device__ inline Schedule schedule_for(long long n_mt, long long Vp, long long G,
+                                                 long long align = 16) {
   Schedule s;
   s.Vp = Vp;
   const long long splits = G / n_mt;
   if (splits >= 1 && n_mt * splits * 10 >= G * 9) {
-    s.C = ((Vp + splits - 1) / splits + 15) / 16 * 16;
+    s.C = ((Vp + splits - 1) / splits + align - 1) / align * align;
     s.band = (Vp + s.C - 1) / s.C * s.C;
   } else {
-    s.C = ((n_mt * Vp + G - 1) / G + 15) / 16 * 16;
+    s.C = ((n_mt * Vp + G - 1) / G + align - 1) / align * align;
     s.band = Vp;
   }
   s.total = n_mt * s.band;
@@ -446,6 +450,7 @@ struct TileIter {
   long long pos, end;
   Schedule sch;
   int taper = 0;
+  int wmax = 256;   // widest tile (128 for MXFP4: TMEM columns for the scale factors)
   __device__ __forceinline__ bool next(int& mt, int& v0, int& width, bool& last) {
     for (;;) {
       if (pos >= end) return false;
@@ -461,7 +466,7 @@ struct TileIter {
       width = (int)min((long long)TC_BN_OVERRIDE, seg_end - v0);
 #else
       width = (taper && base + sch.Vp >= end) ? taper_width(seg_end - v0)
-                                              : (int)min(256LL, seg_end - v0);
+                                              : (int)min((long long)wmax, seg_end - v0);
 #endif
       last = (v0 + width == seg_end);
       pos += width;

@@ -123,6 +123,21 @@ amun_status launch_tc_f8(const CUtensorMap* mx, const CUtensorMap* mw, const TcP
   return launch_kernel<NG>(kern, mx, mw, tp, grid, st, TC_SMEM_F8);
 }
 
+// mxfp4 plans: single CTAs; every mode (the fused path, the test/bench
+// builds and the argmax kernel).
+template <int KB, int NG>
+amun_status launch_tc_f4(const CUtensorMap* mx, const CUtensorMap* mw, const TcParams& tp,
+                         int grid, cudaStream_t st, int mode) {
+  void (*kern)(const CUtensorMap, const CUtensorMap, const TcParams) =
+      mode == 2 ? ol_tc_kernel<KB, 2, NG, 3> : mode == 3 ? ol_tc_kernel<KB, 3, NG, 3>
+                                             : ol_tc_kernel<KB, 0, NG, 3>;
+  if constexpr (KB == 1) {
+    if (mode == 1) kern = ol_tc_kernel<1, 1, NG, 3>;
+    if (mode == 4) kern = ol_tc_kernel<1, 4, NG, 3>;
+  }
+  return launch_kernel<NG>(kern, mx, mw, tp, grid, st, TC_SMEM_F4);
+}
+
 // tf32x3 plans: single CTAs; every mode (the fused path, the test/bench
 // builds and the argmax kernel).
 template <int KB, int NG>
@@ -147,6 +162,7 @@ template <int KB>
 amun_status launch_tc(int dtype, int ng_override, const CUtensorMap* mx, const CUtensorMap* mw,
                       const TcParams& tp, int grid, cudaStream_t st, int mode, bool pairs) {
   if (dtype == AMUN_TF32X3) return launch_tc_t3<KB, 2>(mx, mw, tp, grid, st, mode);
+  if (dtype == AMUN_MXFP4) return launch_tc_f4<KB, 2>(mx, mw, tp, grid, st, mode);
   if (dtype == AMUN_E4M3) {
 #ifdef AMUN_WITH_NG4
     if (ng_override == 4) return launch_tc_f8<KB, 4>(mx, mw, tp, grid, st, mode);

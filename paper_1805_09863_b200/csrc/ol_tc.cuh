@@ -40,7 +40,8 @@ constexpr int TC_B_BYTES = TC_BN * TC_KBYTES;   // 16 KB (32 KB)
 constexpr int TC_SMEM = TC_STAGES * (TC_A_BYTES + TC_B_BYTES) + TC_BIAS_BYTES + TC_XCH_BYTES +
                         TC_THRX_BYTES + 1024 /*align*/ + 512 /*barriers*/;
 constexpr int TC_SMEM_F8 = TC_SMEM + TC_SCALE_BYTES;   // + the e4m3 column-scale ring
-static_assert(TC_SMEM_F8 <= 227 * 1024, "shared memory budget");
+constexpr int TC_SMEM_F4 = TC_SMEM + (TC_STAGES + 1) * TC_SF_ATOM;   // + the mxfp4 scale atoms
+static_assert(TC_SMEM_F8 <= 227 * 1024 && TC_SMEM_F4 <= 227 * 1024, "shared memory budget");
 static_assert(TC_NBIAS >= 2 + TC_STAGES, "bias ring too small for the producer's lead");
 
 // ELT = 0: bf16 X, W (kind::f16, 64 elements per 128-byte K block);
@@ -49,6 +50,11 @@ static_assert(TC_NBIAS >= 2 + TC_STAGES, "bias ring too small for the producer's
 // ELT = 2: fp32 as 3xTF32 (kind::tf32, 32 elements per block): rows stored
 // as [X_hi | X_hi | X_lo] and [W_hi | W_lo | W_hi], so the K = 3H product is
 // X_hi W_hi + X_hi W_lo + X_lo W_hi (NEXT f2).
+// ELT = 3: e4m3 X with per-row scales, MXFP4 W (E2M1 codes + one E8M0 scale
+// per 32 K elements) on kind::mxf8f6f4.block_scale; 128-column tiles (the
+// TMEM columns between the accumulators hold the scales, tc_epi.cuh); each
+// stage also carries W's 512-byte scale atom, copied to TMEM by the MMA
+// thread (tcgen05.cp) before that stage's MMAs (NEXT f4).
 template <int KB, int MODE, int NG, int ELT = 0>
 __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
     ol_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
@@ -72,6 +78,9 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
   float* sscale = (ELT == 1 && scale_ring_ok(p, TC_STAGES))
                       ? reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 512)
                       : nullptr;
+  // mxfp4: W scale atoms [TC_STAGES][512] then A's constant atom (TC_SMEM_F4)
+  uint8_t* ssf = reinterpret_cast<uint8_t*>(full) + 512;
+  uint8_t* ssfa = ssf + TC_STAGES * TC_SF_ATOM;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -86,11 +95,16 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
   // scheduled now (its CTAs still need this kernel's SMs to free up).
   if (p.pdl) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (threadIdx.x == 0 && !p.pdl) tl_mark(p.tl, TL_ENTRY);
-  if (role == 0 && lane == 0 && !p.N_dev && !p.pdl && p.mc <= 1)   // W to L2 before the prologue (tail.cuh)
-    entry_prefetch_w(p, (long long)blockIdx.x * p.sch.C,
-                     min((long long)(blockIdx.x + 1) * p.sch.C, p.sch.total), p.sch);
   for (int i = threadIdx.x; i < TC_THRX_BYTES / 8; i += blockDim.x)   // no stale tags
     sts_u64(smem_u32(thr_x + i), 0ull);
+  if constexpr (ELT == 3) {
+    // A's scales: 2^0 (E8M0 code 127) for every row and K block; X keeps its
+    // per-row fp32 scale, applied in the epilogue. Written by the generic
+    // proxy, read by tcgen05.cp (async proxy): fence before the barrier.
+    for (int i = threadIdx.x; i < TC_SF_ATOM / 4; i += blockDim.x)
+      reinterpret_cast<uint32_t*>(ssfa)[i] = 0x7F7F7F7Fu;
+    fence_proxy_async_smem();
+  }
   if (role == 0 && lane == 0) {
     prefetch_tmap(&tmX);
     prefetch_tmap(&tmW);
@@ -121,6 +135,9 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
     if (threadIdx.x == 0) tl_mark(p.tl, TL_ENTRY);
   }
   const uint32_t tmem_base = *tmem_holder;
+  if constexpr (ELT == 3) {
+    if (role == 1 && lane == 0) tmem_cp_sf(tmem_base + TC_SFA_COL, sdesc_rows16(smem_u32(ssfa)));
+  }
   // this launch's tag (hints, tail counters): read by the epilogue threads
   // (the only users), off the TMA producer's path to its first load
   uint32_t gen = 0u;
@@ -145,12 +162,14 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
       const uint64_t pol_x = policy_evict_last();     // X is re-read by every CTA
       TileIter it{start, stop, dyn.sch};
       it.taper = p.taper;
+      if constexpr (ELT == 3) it.wmax = TC_BN_F4;
       int mt, v0, width;
       bool last;
       int stage = 0, tile = 0;
       uint32_t phase = 0;
       // TC_KBYTES of K per block: bf16 / e4m3 / fp32 (tf32x3) elements
-      constexpr int kBlockElems = ELT == 1 ? TC_KBYTES : ELT == 2 ? TC_KBYTES / 4 : TC_KBYTES / 2;
+      constexpr int kBlockElems = ELT == 1 || ELT == 3 ? TC_KBYTES : ELT == 2 ? TC_KBYTES / 4
+                                                                               : TC_KBYTES / 2;
       int loads = 0;
       while (it.next(mt, v0, width, last)) {
         if (lane == 0) bias_ring_load(p, sbias, bfull, tile, v0, width, sscale);
@@ -178,8 +197,21 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
             // contiguously, i.e. the same SW128 K-major tile
             const int wbox = p.wbox;
             const int nbox = (width + wbox - 1) / wbox;
+            // (mxfp4 W: the transaction counts the packed global bytes, half
+            // the unpacked shared-memory box)
+            constexpr int kWDiv = ELT == 3 ? 2 : 1;
             mbar_arrive_expect_tx(&full[stage], (load_x ? p.a_box_bytes : 0) +
-                                                    (load_w ? nbox * wbox * TC_KBYTES : 0));
+                                                    (load_w ? nbox * wbox * TC_KBYTES / kWDiv : 0) +
+                                                    (ELT == 3 && load_w ? TC_SF_ATOM : 0));
+            if constexpr (ELT == 3) {
+              // the tile's scale atom for this K block (v0 is 128-aligned:
+              // schedule_for align 128)
+              AMUN_DCHECK(v0 % TC_BN_F4 == 0);
+              if (load_w)
+                bulk_load(ssf + stage * TC_SF_ATOM,
+                          p.w_sf + ((long long)(v0 / TC_BN_F4) * p.n_kblk + kb) * TC_SF_ATOM,
+                          TC_SF_ATOM, &full[stage]);
+            }
             if (load_x)
               tma_load_2d(&tmX, &full[stage], sA + stage * TC_A_BYTES, kb * kBlockElems, mt * TC_BM,
                           pol_x);
@@ -209,6 +241,7 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
       // commit tracks the MMAs issued by the same thread).
       TileIter it{start, stop, dyn.sch};
       it.taper = p.taper;
+      if constexpr (ELT == 3) it.wmax = TC_BN_F4;
       int mt, v0, width;
       bool last;
       int stage = 0;
@@ -232,12 +265,21 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
             if (kb == 0 && mtile == 1) tl_mark(p.tl, TL_FULL0);
             const uint64_t ad = sdesc_k<TC_KBYTES>(smem_u32(sA + stage * TC_A_BYTES));
             const uint64_t bd = sdesc_k<TC_KBYTES>(smem_u32(sB + stage * TC_B_BYTES));
+            uint32_t sfb = 0;
+            if constexpr (ELT == 3) {   // this stage's W scales -> TMEM (ordered before the MMAs)
+              sfb = tmem_base + TC_SFB_COL + 4 * stage;
+              tmem_cp_sf(sfb, sdesc_rows16(smem_u32(ssf + stage * TC_SF_ATOM)));
+            }
 #pragma unroll
             for (int k = 0; k < TC_KBYTES / 32; ++k) {   // +32 bytes of K per MMA (>>4 = 2)
               if constexpr (ELT == 0)
                 mma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
               else if constexpr (ELT == 1)
                 mma_e4m3(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+              else if constexpr (ELT == 3)   // K step k uses byte k of each scale word
+                mma_mxf4(d, ad + 2 * k, bd + 2 * k, idesc_mxf4_f32(TC_BM, width, k, k),
+                         (tmem_base + TC_SFA_COL) | ((uint32_t)k << 30), sfb | ((uint32_t)k << 30),
+                         (kb | k) != 0);
               else
                 mma_tf32(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
             }

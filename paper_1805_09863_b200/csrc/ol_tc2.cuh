@@ -61,9 +61,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<NG>::kThreads,
   const uint32_t rank = cluster_ctarank();          // 0 = leader, 1 = peer
   const int pair = blockIdx.x >> 1;
 
-  if (role == 0 && lane == 0 && rank == 0 && !p.N_dev)   // W to L2 before the prologue (tail.cuh)
-    entry_prefetch_w(p, (long long)pair * p.sch.C,
-                     min((long long)(pair + 1) * p.sch.C, p.sch.total), p.sch);
   for (int i = threadIdx.x; i < TC_THRX_BYTES / 8; i += blockDim.x)   // no stale tags
     sts_u64(smem_u32(thr_x + i), 0ull);
   if (role == 0 && lane == 0) {

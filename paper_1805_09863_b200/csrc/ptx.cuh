@@ -315,6 +315,60 @@ __device__ __forceinline__ uint32_t idesc_e4m3_f32(int M, int N) {
   return d;
 }
 
+// Block-scaled MXFP4 W: kind::mxf8f6f4.block_scale with
+// A = E4M3 (format 0), B = E2M1 (format 5, "unpacked" in shared memory: the
+// 16U4_ALIGN16B TMA type leaves 16 codes in 16 bytes, so K advances 32 bytes
+// per instruction like e4m3), one E8M0 scale per 32 K elements for each
+// operand row (scale_format bit 23 = 1), read from TMEM. sf ids (bits 29-30
+// for A, 4-5 for B) pick the byte of the 32-bit TMEM scale word: the K = 32
+// step within a 128-element K block. D is always F32 (no c_format field).
+__device__ __forceinline__ uint32_t idesc_mxf4_f32(int M, int N, int a_sf_id, int b_sf_id) {
+  uint32_t d = 0;
+  d |= (uint32_t)b_sf_id << 4;            // B scale-factor id
+  d |= 0u << 7;                           // a_format = E4M3
+  d |= 5u << 10;                          // b_format = E2M1
+  d |= (uint32_t)(N >> 3) << 17;          // n_dim
+  d |= 1u << 23;                          // scale format E8M0
+  d |= (uint32_t)(M >> 4) << 24;          // m_dim
+  d |= (uint32_t)a_sf_id << 29;           // A scale-factor id
+  return d;
+}
+// D(fp32) += (A * sfA) (B * sfB)^T, K = 32 per instruction; sfa / sfb are the
+// TMEM addresses of the scale words (byte id also in bits 30-31).
+__device__ __forceinline__ void mma_mxf4(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t sfa, uint32_t sfb,
+                                         uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::mxf8f6f4.block_scale [%0], %1, %2, %3, [%5], [%6], p;\n\t}"
+      ::"r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(sfa), "r"(sfb)
+      : "memory");
+}
+// Shared memory -> TMEM copy of a scale-factor atom: 32 rows x 128 bits
+// (512 contiguous bytes: row m0 = 16 bytes = the 4 K-block scales of rows
+// m0, m0+32, m0+64, m0+96), broadcast to the 4 lane quarters; 4 columns.
+// Issued by the MMA thread: ordered with its later tcgen05.mma, tracked by
+// its tcgen05.commit.
+__device__ __forceinline__ void tmem_cp_sf(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::1.32x128b.warpx4 [%0], %1;" ::"r"(taddr), "l"(sdesc)
+               : "memory");
+}
+// Descriptor of a no-swizzle K-major tile of 16-byte rows: 8-row core
+// matrices of 128 contiguous bytes, SBO = 128 (next 8 rows), one core matrix
+// along K (LBO unused), layout type 0.
+__device__ __forceinline__ uint64_t sdesc_rows16(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;                 // LBO (unused)
+  d |= (uint64_t)(128 >> 4) << 32;        // SBO
+  d |= (uint64_t)1 << 46;                 // version = 1
+  return d;
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

@@ -49,6 +49,66 @@ __global__ void __launch_bounds__(QZ_THREADS) quantize_e4m3_kernel(const void* _
   }
 }
 
+// MXFP4 quantisation (amun_quantize_mxfp4; OCP MX v1.0, oracle
+// quantize_rows_mxfp4): one warp per (row, 128-element K block), lane l
+// converts elements 4l..4l+3; the 8 lanes of a 32-element MX block reduce
+// its max |x|. Shared exponent e = floor(log2 amax) - 2 (the biased fp32
+// exponent of amax minus 2 is the E8M0 code; 127 for an all-zero block;
+// clamped to [0, 254]); codes = RNE-to-E2M1(x * 2^-e), saturating, two per
+// byte, the lower element in the low nibble. Scales go to the atom layout
+// the fused kernel copies to TMEM (amun.h). Rows R..R_pad-1 of the last
+// 128-row atom get code 127 (their W rows read as zero).
+template <bool BF16>
+__global__ void __launch_bounds__(QZ_THREADS) quantize_mxfp4_kernel(const void* __restrict__ src,
+                                                                    int R, int H,
+                                                                    uint8_t* __restrict__ codes,
+                                                                    uint8_t* __restrict__ sf) {
+  const int lane = threadIdx.x & 31;
+  const int KT = H / 128;
+  const long long Rp = (R + 127LL) / 128 * 128;
+  const long long tasks = Rp * KT;
+  const long long nwarps = (long long)gridDim.x * (QZ_THREADS / 32);
+  for (long long t = blockIdx.x * (long long)(QZ_THREADS / 32) + (threadIdx.x >> 5); t < tasks;
+       t += nwarps) {
+    const long long r = t / KT;
+    const int kt = (int)(t - r * KT);
+    const int kb = lane >> 3;
+    float q[4] = {0.f, 0.f, 0.f, 0.f};
+    float amax = 0.f;
+    if (r < R) {
+      const long long base = r * H + kt * 128 + 4 * lane;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if constexpr (BF16)
+          q[j] = __bfloat162float(static_cast<const __nv_bfloat16*>(src)[base + j]);
+        else
+          q[j] = static_cast<const float*>(src)[base + j];
+        amax = fmaxf(amax, fabsf(q[j]));
+      }
+    }
+#pragma unroll
+    for (int o = 4; o >= 1; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    int code = 127;
+    if (amax > 0.f) code = min(max((int)((__float_as_uint(amax) >> 23) & 0xffu) - 2, 0), 254);
+    if (r < R) {
+      uint16_t out;
+      const int sh = 127 - code;   // x * 2^-e, exact (a power of two)
+      asm("{\n\t.reg .b8 b0, b1;\n\t"
+          "cvt.rn.satfinite.e2m1x2.f32 b0, %2, %1;\n\t"
+          "cvt.rn.satfinite.e2m1x2.f32 b1, %4, %3;\n\t"
+          "mov.b16 %0, {b0, b1};\n\t}"
+          : "=h"(out)
+          : "f"(ldexpf(q[0], sh)), "f"(ldexpf(q[1], sh)), "f"(ldexpf(q[2], sh)),
+            "f"(ldexpf(q[3], sh)));
+      reinterpret_cast<uint16_t*>(codes + r * (H / 2) + kt * 64)[lane] = out;
+    }
+    if ((lane & 7) == 0) {
+      const long long m = r & 127;
+      sf[((r >> 7) * KT + kt) * 512 + 16 * (m & 31) + 4 * (m >> 5) + kb] = (uint8_t)code;
+    }
+  }
+}
+
 // 3xTF32 split (amun_split_tf32x3): hi = tf32(x), lo = tf32(x - hi); row r
 // of dst = role 0: [hi | hi | lo], role 1: [hi | lo | hi].
 __global__ void split_tf32x3_kernel(const float* __restrict__ src, long long n, int H, int role,

@@ -1,5 +1,5 @@
 // tail.cuh — the fused kernels' grid-wide tail: the merge (a6) inside the
-// same launch as steps 1-4, and the entry L2 prefetch of W.
+// same launch as steps 1-4.
 //
 // Tail. Every CTA's partial records {m, s, top-k} (Alg. 6's per-shard state,
 // P:232-242) must be complete before any row can be merged (the reduce step
@@ -60,29 +60,6 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
-}
-
-// Entry prefetch (one thread, before barrier setup / TMEM allocation): the
-// first bytes of this CTA's W range go to L2 with bulk prefetches, so HBM
-// streams from the first microsecond instead of after the prologue and the
-// first TMA round trip (the HBM-bound greedy config is mostly that latency).
-// In aligned schedules only the M-tile-0 CTA of a vocab range prefetches (the
-// other M-tiles' CTAs read the same W tiles at the same time).
-__device__ __forceinline__ void entry_prefetch_w(const TcParams& p, long long start, long long stop,
-                                                 const Schedule& sch) {
-  if (!p.pf_w || start >= stop) return;
-  const long long mt = start / sch.band;
-  if (sch.band != sch.Vp && mt != 0) return;          // aligned: M-tile 0's CTA only
-  const long long v0 = start - mt * sch.band;
-  if (v0 >= p.V_local) return;
-  const long long v1 = min(min((long long)p.V_local, stop - mt * sch.band), sch.Vp);
-  long long bytes = (v1 - v0) * p.pf_row_bytes;
-  if (bytes > p.pf_max_bytes) bytes = p.pf_max_bytes;
-  const char* a = p.pf_w + v0 * p.pf_row_bytes;
-  for (long long o = 0; o < bytes; o += 65536) {
-    const uint32_t n = (uint32_t)min(65536LL, (bytes - o + 15) & ~15LL);
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a + o), "r"(n) : "memory");
-  }
 }
 
 // Called by every thread of the CTA after the kernel's final barrier (all

@@ -30,6 +30,8 @@ struct TcParams {
   const int* __restrict__ N_dev;           // amun_output_layer_dev: N on the device (else NULL)
   const float* __restrict__ x_scale;       // e4m3 plans: [N] per-row scales of X (else NULL)
   const float* __restrict__ w_scale;       // e4m3 plans: [V_local] per-row scales of W
+  const uint8_t* __restrict__ w_sf;        // mxfp4 plans: W's E8M0 block scales, atom layout
+                                           // [V_local/128][n_kblk][512] (amun.h)
   int a_box_bytes;                         // bytes of one X box (rows x 128; single-CTA kernel)
   int num_sms;                             // the device schedule's CTA count
   // Fused tail (tail.cuh): after every CTA of the grid has emitted its
@@ -39,9 +41,6 @@ struct TcParams {
   int tail;                                // TAIL_NONE / TAIL_SENT / TAIL_ROWS / TAIL_ARGMAX
   MergeParams mp;                          // the merge's parameters (outputs, offsets, ...)
   unsigned int* __restrict__ arrive;       // [2] tail arrival counters, by tag parity (tail.cuh)
-  const char* __restrict__ pf_w;           // W base for the entry L2 prefetch (else NULL)
-  long long pf_row_bytes;                  // bytes of one W row (K elements)
-  long long pf_max_bytes;                  // prefetch at most this many bytes of a CTA's W range
   unsigned long long* __restrict__ tl;     // timeline probe [grid][TL_N] (amun_debug_timeline), else NULL
   OneShotTail os;                          // TAIL_ONESHOT: the peer buffers (peer.cuh)
   int taper;                               // single-CTA kernel: narrow final tiles (TileIter)
@@ -113,6 +112,14 @@ constexpr int TC_THRX_BYTES = 2 * 128 * 8;           // per-(group, row) k-th-be
 // epilogue reads the scales from global memory.
 constexpr int TC_NSCALE = 4;
 constexpr int TC_SCALE_BYTES = TC_NSCALE * TC_BN * 4;
+// MXFP4 plans (ELT 3): tiles of TC_BN_F4 = 128 columns, so the two
+// accumulators use TMEM columns [0, 128) and [256, 384) and the block
+// scales live in the gap: A's (constant 1.0, written once) at TC_SFA_COL,
+// B's per pipeline stage at TC_SFB_COL + 4 * stage. Shared memory: one
+// 512-byte scale atom per stage + A's, after the barrier area.
+constexpr int TC_BN_F4 = 128;
+constexpr int TC_SF_ATOM = 512;
+constexpr uint32_t TC_SFA_COL = 128, TC_SFB_COL = 160;
 
 // Launch configuration of NG epilogue warpgroups (warps 0 .. 4NG-1) + the
 // control warpgroup (TMA producer warp, MMA warp, 2 idle warps), and the setmaxnreg budget,
@@ -197,6 +204,7 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
   st.reset();
   TileIter it{start, stop, dyn.sch};
   it.taper = PAIR ? 0 : p.taper;
+  if constexpr (ELT == 3) it.wmax = TC_BN_F4;
   int unit, v0, width;
   bool last;
   int acc = 0, tile = 0;
@@ -224,7 +232,8 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
     const int limit = min(width, p.V_local - v0);
     const int nch = (width + 31) >> 5;
     const float* bsl = sbias + (tile % TC_NBIAS) * TC_BN;
-    const float xs = (ELT == 1 && row < dyn.N) ? __ldg(p.x_scale + row) : 1.f;   // e4m3 row scale
+    const float xs = ((ELT == 1 || ELT == 3) && row < dyn.N) ? __ldg(p.x_scale + row)
+                                                              : 1.f;   // e4m3 row scale
     // request the newest cross-CTA hint now (L2, not L1: other SMs update it);
     // it is folded in after this tile's chunks, for the next tile of the segment
     // (per-chunk exchange halves the insertions but its loads and atomics cost
@@ -245,7 +254,16 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
       const int nv = limit - c0;
       if (nv >= 32) {   // full chunk: bias from the ring (same address in all lanes)
         const uint32_t b4 = smem_u32(bsl + c0);
-        if constexpr (ELT != 1) {   // bf16 / tf32x3: + bias
+        if constexpr (ELT == 3) {   // mxfp4 W (block scales inside the MMA): acc * x_scale + b
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float4 bq = lds128(b4 + 16 * j);
+            ffma2(x[4 * j + 0], x[4 * j + 1], __uint_as_float(r[4 * j + 0]),
+                  __uint_as_float(r[4 * j + 1]), xs, xs, bq.x, bq.y);
+            ffma2(x[4 * j + 2], x[4 * j + 3], __uint_as_float(r[4 * j + 2]),
+                  __uint_as_float(r[4 * j + 3]), xs, xs, bq.z, bq.w);
+          }
+        } else if constexpr (ELT != 1) {   // bf16 / tf32x3: + bias
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const float4 bq = lds128(b4 + 16 * j);
@@ -278,7 +296,9 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           const float bj = (j < nv4) ? bsl[c0 + j] : ((j < nv) ? __ldg(p.bias + v0 + c0 + j) : 0.f);
-          if constexpr (ELT != 1) {
+          if constexpr (ELT == 3) {
+            x[j] = (j < nv) ? fmaf(__uint_as_float(r[j]), xs, bj) : kNegInf;
+          } else if constexpr (ELT != 1) {
             x[j] = (j < nv) ? __uint_as_float(r[j]) + bj : kNegInf;
           } else {
             const float sj = (j < nv) ? xs * __ldg(p.w_scale + v0 + c0 + j) : 0.f;

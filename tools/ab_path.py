@@ -1,7 +1,8 @@
 """A/B device times of the whole output-layer path (amun_output_layer) under
 plan-creation switches (env read by amun_ol_create): the fused tail
-(AMUN_TAIL=off: separate merge kernel) and the entry L2 prefetch of W
-(AMUN_PF_BYTES). CUDA graph of K calls, W rotated over enough copies that
+(AMUN_TAIL=off: separate merge kernel), the tail experiments, taper,
+pre-pass, PDL and W box size. (The entry L2 prefetch of W that "+pf" once
+measured was removed after it measured slower.) CUDA graph of K calls, W rotated over enough copies that
 L2 never serves W across calls (as bench.py). Interleaved repetitions.
 
   python tools/ab_path.py [workload ...]     (JSON lines)
@@ -17,26 +18,24 @@ import synth  # noqa: E402
 import paper_1805_09863_b200 as amun  # noqa: E402
 
 VARIANTS = {
-    "tail+pf": {"AMUN_TAIL": "on", "AMUN_PF_BYTES": str(1 << 20)},
-    "tail": {"AMUN_TAIL": "on", "AMUN_PF_BYTES": "0"},
-    "sep+pf": {"AMUN_TAIL": "off", "AMUN_PF_BYTES": str(1 << 20)},
-    "sep": {"AMUN_TAIL": "off", "AMUN_PF_BYTES": "0"},
-    "tailwait": {"AMUN_TAIL": "wait", "AMUN_PF_BYTES": "0"},     # tail without merge work
-    "tailnocoop": {"AMUN_TAIL": "nocoop", "AMUN_PF_BYTES": "0"},
+    "tail": {"AMUN_TAIL": "on"},
+    "sep": {"AMUN_TAIL": "off"},
+    "tailwait": {"AMUN_TAIL": "wait"},     # tail without merge work
+    "tailnocoop": {"AMUN_TAIL": "nocoop"},
 }
-VARIANTS["tailfence"] = {"AMUN_TAIL": "fence", "AMUN_PF_BYTES": "0"}
-VARIANTS["tailsleep"] = {"AMUN_TAIL": "sleep", "AMUN_PF_BYTES": "0"}
-VARIANTS["waitnocoop"] = {"AMUN_TAIL": "waitnocoop", "AMUN_PF_BYTES": "0"}
-VARIANTS["arriveonly"] = {"AMUN_TAIL": "arriveonly", "AMUN_PF_BYTES": "0"}
-VARIANTS["scores"] = {"AMUN_TAIL": "off", "AMUN_PF_BYTES": "0"}   # the fused kernel alone
+VARIANTS["tailfence"] = {"AMUN_TAIL": "fence"}
+VARIANTS["tailsleep"] = {"AMUN_TAIL": "sleep"}
+VARIANTS["waitnocoop"] = {"AMUN_TAIL": "waitnocoop"}
+VARIANTS["arriveonly"] = {"AMUN_TAIL": "arriveonly"}
+VARIANTS["scores"] = {"AMUN_TAIL": "off"}   # the fused kernel alone
 # final-tile taper (TileIter) on (default off), the first-tile k-best bound
 # pre-pass off (default on)
-VARIANTS["tail_t1"] = {"AMUN_TAIL": "on", "AMUN_PF_BYTES": "0", "AMUN_TAPER": "1"}
-VARIANTS["sep_t1"] = {"AMUN_TAIL": "off", "AMUN_PF_BYTES": "0", "AMUN_TAPER": "1"}
-VARIANTS["scores_t1"] = {"AMUN_TAIL": "off", "AMUN_PF_BYTES": "0", "AMUN_TAPER": "1"}
-VARIANTS["tail_pp0"] = {"AMUN_TAIL": "on", "AMUN_PF_BYTES": "0", "AMUN_PREPASS": "0"}
-VARIANTS["sep_pp0"] = {"AMUN_TAIL": "off", "AMUN_PF_BYTES": "0", "AMUN_PREPASS": "0"}
-VARIANTS["scores_pp0"] = {"AMUN_TAIL": "off", "AMUN_PF_BYTES": "0", "AMUN_PREPASS": "0"}
+VARIANTS["tail_t1"] = {"AMUN_TAIL": "on", "AMUN_TAPER": "1"}
+VARIANTS["sep_t1"] = {"AMUN_TAIL": "off", "AMUN_TAPER": "1"}
+VARIANTS["scores_t1"] = {"AMUN_TAIL": "off", "AMUN_TAPER": "1"}
+VARIANTS["tail_pp0"] = {"AMUN_TAIL": "on", "AMUN_PREPASS": "0"}
+VARIANTS["sep_pp0"] = {"AMUN_TAIL": "off", "AMUN_PREPASS": "0"}
+VARIANTS["scores_pp0"] = {"AMUN_TAIL": "off", "AMUN_PREPASS": "0"}
 for _p in (0, 1):
     VARIANTS[f"tail_pdl{_p}"] = {"AMUN_TAIL": "on", "AMUN_PDL": str(_p)}
     VARIANTS[f"sep_pdl{_p}"] = {"AMUN_TAIL": "off", "AMUN_PDL": str(_p)}
@@ -45,7 +44,6 @@ for _b in (64, 256):
     VARIANTS[f"sep_box{_b}"] = {"AMUN_TAIL": "off", "AMUN_WBOX": str(_b)}
     VARIANTS[f"scores_box{_b}"] = {"AMUN_TAIL": "off", "AMUN_WBOX": str(_b)}
 for _v in VARIANTS.values():
-    _v.setdefault("AMUN_PF_BYTES", "0")
     _v.setdefault("AMUN_TAPER", "0")
     _v.setdefault("AMUN_PREPASS", "1")
 NOCHECK = {v for v in VARIANTS if v.startswith("scores")} | {"tailwait", "waitnocoop", "arriveonly"}
