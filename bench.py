@@ -403,10 +403,14 @@ def roofline(w, V_local, kern_ms, peaks, label, traffic=None, plan_dtype=None):
     """Algorithmic work of ONE fused-kernel launch over its time: FLOP =
     2*N*H*V_local; bytes = W + X + b once (the logits never reach HBM)."""
     dt = plan_dtype or w.dtype
-    esz = {"bf16": 2, "f32": 4, "e4m3": 1, "tf32x3": 12}[dt]
     flops = 2.0 * w.N * w.H * V_local
-    alg_bytes = V_local * w.H * esz + w.N * w.H * esz + V_local * 4
-    tc_peak = peaks["bf16_tflops"] * {"bf16": 1.0, "e4m3": 2.0, "tf32x3": 1.0 / 6.0}.get(dt, 1.0)
+    if dt == "mxfp4":   # W: 4-bit codes + one E8M0 byte per 32; X: e4m3
+        alg_bytes = V_local * w.H * (0.5 + 1 / 32) + w.N * w.H + V_local * 4
+    else:
+        esz = {"bf16": 2, "f32": 4, "e4m3": 1, "tf32x3": 12}[dt]
+        alg_bytes = V_local * w.H * esz + w.N * w.H * esz + V_local * 4
+    tc_peak = peaks["bf16_tflops"] * {"bf16": 1.0, "e4m3": 2.0, "mxfp4": 2.0,
+                                      "tf32x3": 1.0 / 6.0}.get(dt, 1.0)
     t_tc = flops / (tc_peak * 1e12)
     t_hbm = alg_bytes / (peaks["hbm_gbs"] * 1e9)
     common = {"traffic": traffic, "kernel": label, "kernel_ms_mean": kern_ms,
@@ -648,6 +652,79 @@ def e4m3_object(p: Problem, ctx, K):
                     "parity vs the oracle on the dequantised values in tests/test_gpu_e4m3.py"}
 
 
+def mxfp4_object(name, ctx, K, warmup, peaks, n_sent):
+    """Block-scaled 4-bit W (MXFP4 on tcgen05 kind::mxf8f6f4.block_scale) on a
+    config shape: W quantised once per resident copy (amun_quantize_mxfp4), X
+    quantised to E4M3 inside every step; one CUDA graph. Parity: the oracle
+    on the exactly dequantised values (its own quantisation of the same
+    inputs) for the first n_sent sentences."""
+    import paper_1805_09863_b200 as amun
+    w, dev = synth.CONFIGS[name], ctx.dev
+    X_h, W_h, b_h, pc_h = synth.gen_X(w), synth.gen_W(w), synth.gen_b(w), synth.gen_prev_cost(w)
+    X, b, pc, off = X_h.to(dev), b_h.to(dev), pc_h.to(dev), synth.gen_offsets(w, dev)
+    W0 = W_h.to(dev)
+    q0 = amun.quantize_mxfp4(W0)
+    n = w_copies(q0[0].numel() + q0[1].numel())
+    Wq = [q0] + [(q0[0].clone(), q0[1].clone()) for _ in range(n - 1)]
+    del W0
+    X8 = torch.empty((w.N, w.H), dtype=torch.uint8, device=dev)
+    xs = torch.empty(w.N, dtype=torch.float32, device=dev)
+    ol = amun.OutputLayer(w.H, w.V, dtype="mxfp4", k_max=w.k, max_rows=w.N, max_sentences=w.S,
+                          device=dev)
+    oi = torch.empty((w.S, w.k), dtype=torch.int64, device=dev)
+    oc = torch.empty((w.S, w.k), dtype=torch.float32, device=dev)
+
+    def step(i):
+        amun.quantize_e4m3(X, out=X8, scale=xs)
+        c = Wq[i % len(Wq)]
+        ol.call_mxfp4(X8, xs, c[0], c[1], b, pc, off, w.k, out_idx=oi, out_cost=oc)
+    for i in range(warmup):
+        step(i)
+    st = torch.cuda.Stream(dev)
+    with torch.cuda.stream(st):
+        step(0)
+    torch.cuda.synchronize()
+    g = capture(step, K, st)
+    replay_ms(g, st)
+    ms = replay_ms(g, st) / K
+    kg = capture(lambda i: ol.scores_mxfp4(X8, xs, Wq[i % len(Wq)][0], Wq[i % len(Wq)][1], b),
+                 K, st)
+    replay_ms(kg, st)
+    kms = replay_ms(kg, st) / K
+    res = {"workload": f"{name} shape, W in MXFP4 (E2M1 + E8M0 per 32), X in E4M3 quantised "
+                       f"inside every step (amun_output_layer_mxfp4)",
+           "value": w.N / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms, "steps": K,
+           "dtype": "e4m3 x mxfp4", "w_copies": len(Wq),
+           "roofline": roofline(w, w.V, kms, peaks, "ol_tc_kernel<.., ELT=3> (mxfp4)",
+                                plan_dtype="mxfp4")}
+    if n_sent > 0:
+        import oracle as O
+        step(0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        X8h, xsh = O.quantize_rows_e4m3(X_h.float().numpy())
+        codes, sexp = O.quantize_rows_mxfp4(W_h.float().numpy())
+        Xd, Wd = O.dequant_rows_e4m3(X8h, xsh), O.dequant_rows_mxfp4(codes, sexp)
+        rows = int(synth.gen_offsets(w)[n_sent])
+        L = O.add_bias(O.gemm(Xd[:rows], Wd), O.as_f64(b_h))
+        logp = O.log_softmax(L)
+        pcd = O.as_f64(pc_h)[:rows]
+        offs = synth.gen_offsets(w)[:n_sent + 1].numpy()
+        _, _, oc64, nxt = O.kbest_sentences(logp, pcd, offs, w.k)
+        from tests.compare import compare_kbest
+        try:
+            rep = compare_kbest(oi[:n_sent].cpu().numpy(), oc[:n_sent].cpu().numpy(),
+                                lambda s_, r, v: pcd[r] + logp[r, v], oc64, np.full(n_sent, w.k),
+                                "bf16", w.V, o_next=nxt)
+            res["parity"] = {"sentences": n_sent, "rows": rows, **rep, "status": "pass",
+                             "oracle_s": round(time.perf_counter() - t0, 1)}
+        except AssertionError as e:
+            res["parity"] = {"status": "FAIL", "sentences": n_sent, "error": str(e)[:300]}
+    del Wq, g, kg
+    torch.cuda.empty_cache()
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -762,6 +839,10 @@ def main():
                                            128 if not args.no_cpu_baseline else 0, args.eager)
             side["f32"] = f32_object(ctx, max(3, min(K, 50)), args.warmup, peaks,
                                      4 if not args.no_cpu_baseline else 0)
+            for nm in ("greedy", "beam"):
+                side[f"mxfp4_{nm}"] = mxfp4_object(nm, ctx, K, args.warmup, peaks,
+                                                   (128 if nm == "greedy" else 16)
+                                                   if not args.no_cpu_baseline else 0)
 
     if rank != 0:
         if world > 1:

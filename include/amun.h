@@ -291,7 +291,9 @@ amun_status amun_quantize_e4m3(const void* src, amun_dtype src_dtype, int R, int
  * computed by tcgen05.mma kind::mxf8f6f4.block_scale (the block scales are
  * applied inside the tensor core; fp32 accumulation), then the same
  * softmax / k-best / merge as amun_output_layer. Plan: amun_ol_create(...,
- * AMUN_MXFP4, ...), H % 128 == 0; single-CTA kernel, 128-column tiles.
+ * AMUN_MXFP4, ...), H % 128 == 0; single-CTA kernel, tiles of 256 and 128
+ * columns alternating (tensor memory holds the scales beside the narrow
+ * accumulator).
  *
  * Layouts (device):
  *   W4   [V_local, H/2] uint8: two codes per byte, element 2j in the low
@@ -299,7 +301,8 @@ amun_status amun_quantize_e4m3(const void* src, amun_dtype src_dtype, int R, int
  *   w_sf amun_mxfp4_sf_bytes(V_local, H) bytes, 16-byte aligned, in the
  *        scale-atom order the kernel copies to tensor memory unchanged: for
  *        W row v and element h, the E8M0 code of block h/32 is at byte
- *          ((v/128) * (H/128) + h/128) * 512 + 16 * (v%32) + 4 * ((v%128)/32) + (h%128)/32.
+ *          ((h/128) * ceil(V_local/128) + v/128) * 512
+ *            + 16 * (v%32) + 4 * ((v%128)/32) + (h%128)/32.
  *        Rows beyond V_local in the last 128-row atom: any code (their W
  *        rows read as zero and their columns are masked).
  * Parity: the oracle computes on the exactly dequantised values
@@ -322,8 +325,9 @@ amun_status amun_output_layer_mxfp4(amun_ol* plan, const uint8_t* X8, const floa
                                     const float* prev_cost, const int32_t* beam_offsets, int N,
                                     int S, const int32_t* k_per_sentence, int k, int64_t* out_idx,
                                     float* out_cost, void* workspace, void* stream);
-/* Stage 1 alone (variant 0; then amun_ol_select), or the bare-GEMM (2) /
- * no-k-best (3) benchmark builds. */
+/* Stage 1 alone (variant 0; then amun_ol_select), or the benchmark builds
+ * of amun_bench_variant: bare GEMM (2), no k-best (3), bare GEMM re-reading
+ * the first stages (5), with only X (6) / only W (7) copied again. */
 amun_status amun_ol_scores_mxfp4(amun_ol* plan, const uint8_t* X8, const float* x_scale,
                                  const uint8_t* W4, const uint8_t* w_sf, const float* b, int N,
                                  int variant, void* workspace, void* stream);

@@ -40,8 +40,10 @@ constexpr int TC_B_BYTES = TC_BN * TC_KBYTES;   // 16 KB (32 KB)
 constexpr int TC_SMEM = TC_STAGES * (TC_A_BYTES + TC_B_BYTES) + TC_BIAS_BYTES + TC_XCH_BYTES +
                         TC_THRX_BYTES + 1024 /*align*/ + 512 /*barriers*/;
 constexpr int TC_SMEM_F8 = TC_SMEM + TC_SCALE_BYTES;   // + the e4m3 column-scale ring
-constexpr int TC_SMEM_F4 = TC_SMEM + (TC_STAGES + 1) * TC_SF_ATOM;   // + the mxfp4 scale atoms
+constexpr int TC_SMEM_F4 = TC_SMEM + (2 * TC_STAGES + 1) * TC_SF_ATOM;   // + the mxfp4 scale atoms
 static_assert(TC_SMEM_F8 <= 227 * 1024 && TC_SMEM_F4 <= 227 * 1024, "shared memory budget");
+static_assert(TC_SFA_COL >= 256 + TC_BN_F4_ODD && tc_sfb_col(TC_STAGES - 1) + 8 <= 512,
+              "mxfp4 scale columns overlap an accumulator");
 static_assert(TC_NBIAS >= 2 + TC_STAGES, "bias ring too small for the producer's lead");
 
 // ELT = 0: bf16 X, W (kind::f16, 64 elements per 128-byte K block);
@@ -51,10 +53,11 @@ static_assert(TC_NBIAS >= 2 + TC_STAGES, "bias ring too small for the producer's
 // as [X_hi | X_hi | X_lo] and [W_hi | W_lo | W_hi], so the K = 3H product is
 // X_hi W_hi + X_hi W_lo + X_lo W_hi (NEXT f2).
 // ELT = 3: e4m3 X with per-row scales, MXFP4 W (E2M1 codes + one E8M0 scale
-// per 32 K elements) on kind::mxf8f6f4.block_scale; 128-column tiles (the
-// TMEM columns between the accumulators hold the scales, tc_epi.cuh); each
-// stage also carries W's 512-byte scale atom, copied to TMEM by the MMA
-// thread (tcgen05.cp) before that stage's MMAs (NEXT f4).
+// per 32 K elements) on kind::mxf8f6f4.block_scale; tiles of 256 and 128
+// columns alternate (TMEM holds the scales beside the 128-column
+// accumulator, tc_epi.cuh); each stage also carries the K block's W scale
+// atoms of the tile (one per 128 rows), copied to TMEM by the MMA thread
+// (tcgen05.cp, ordered before that stage's MMAs) (NEXT f4).
 template <int KB, int MODE, int NG, int ELT = 0>
 __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
     ol_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
@@ -78,9 +81,9 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
   float* sscale = (ELT == 1 && scale_ring_ok(p, TC_STAGES))
                       ? reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 512)
                       : nullptr;
-  // mxfp4: W scale atoms [TC_STAGES][512] then A's constant atom (TC_SMEM_F4)
+  // mxfp4: W scale atoms [TC_STAGES][2][512] then A's constant atom (TC_SMEM_F4)
   uint8_t* ssf = reinterpret_cast<uint8_t*>(full) + 512;
-  uint8_t* ssfa = ssf + TC_STAGES * TC_SF_ATOM;
+  uint8_t* ssfa = ssf + 2 * TC_STAGES * TC_SF_ATOM;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -162,7 +165,10 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
       const uint64_t pol_x = policy_evict_last();     // X is re-read by every CTA
       TileIter it{start, stop, dyn.sch};
       it.taper = p.taper;
-      if constexpr (ELT == 3) it.wmax = TC_BN_F4;
+      if constexpr (ELT == 3) {
+        it.wmax = TC_BN_F4;
+        it.wmax_odd = TC_BN_F4_ODD;
+      }
       int mt, v0, width;
       bool last;
       int stage = 0, tile = 0;
@@ -200,17 +206,19 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
             // (mxfp4 W: the transaction counts the packed global bytes, half
             // the unpacked shared-memory box)
             constexpr int kWDiv = ELT == 3 ? 2 : 1;
+            const int nsf = width > 128 ? 2 : 1;   // mxfp4 scale atoms of the tile
             mbar_arrive_expect_tx(&full[stage], (load_x ? p.a_box_bytes : 0) +
                                                     (load_w ? nbox * wbox * TC_KBYTES / kWDiv : 0) +
-                                                    (ELT == 3 && load_w ? TC_SF_ATOM : 0));
+                                                    (ELT == 3 && load_w ? nsf * TC_SF_ATOM : 0));
             if constexpr (ELT == 3) {
-              // the tile's scale atom for this K block (v0 is 128-aligned:
-              // schedule_for align 128)
-              AMUN_DCHECK(v0 % TC_BN_F4 == 0);
+              // this K block's scale atoms of the tile's rows: contiguous in the
+              // [kblock][row / 128][512] layout (v0 is 128-aligned)
+              AMUN_DCHECK(v0 % TC_F4_ALIGN == 0);
               if (load_w)
-                bulk_load(ssf + stage * TC_SF_ATOM,
-                          p.w_sf + ((long long)(v0 / TC_BN_F4) * p.n_kblk + kb) * TC_SF_ATOM,
-                          TC_SF_ATOM, &full[stage]);
+                bulk_load(ssf + stage * 2 * TC_SF_ATOM,
+                          p.w_sf + ((long long)kb * ((p.V_local + 127) / 128) + v0 / 128) *
+                                       TC_SF_ATOM,
+                          nsf * TC_SF_ATOM, &full[stage]);
             }
             if (load_x)
               tma_load_2d(&tmX, &full[stage], sA + stage * TC_A_BYTES, kb * kBlockElems, mt * TC_BM,
@@ -241,7 +249,10 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
       // commit tracks the MMAs issued by the same thread).
       TileIter it{start, stop, dyn.sch};
       it.taper = p.taper;
-      if constexpr (ELT == 3) it.wmax = TC_BN_F4;
+      if constexpr (ELT == 3) {
+        it.wmax = TC_BN_F4;
+        it.wmax_odd = TC_BN_F4_ODD;
+      }
       int mt, v0, width;
       bool last;
       int stage = 0;
@@ -267,8 +278,10 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
             const uint64_t bd = sdesc_k<TC_KBYTES>(smem_u32(sB + stage * TC_B_BYTES));
             uint32_t sfb = 0;
             if constexpr (ELT == 3) {   // this stage's W scales -> TMEM (ordered before the MMAs)
-              sfb = tmem_base + TC_SFB_COL + 4 * stage;
-              tmem_cp_sf(sfb, sdesc_rows16(smem_u32(ssf + stage * TC_SF_ATOM)));
+              sfb = tmem_base + tc_sfb_col(stage);
+              const uint32_t s0 = smem_u32(ssf + stage * 2 * TC_SF_ATOM);
+              tmem_cp_sf(sfb, sdesc_rows16(s0));
+              if (width > 128) tmem_cp_sf(sfb + 4, sdesc_rows16(s0 + TC_SF_ATOM));
             }
 #pragma unroll
             for (int k = 0; k < TC_KBYTES / 32; ++k) {   // +32 bytes of K per MMA (>>4 = 2)

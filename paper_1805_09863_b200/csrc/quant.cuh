@@ -55,9 +55,10 @@ __global__ void __launch_bounds__(QZ_THREADS) quantize_e4m3_kernel(const void* _
 // its max |x|. Shared exponent e = floor(log2 amax) - 2 (the biased fp32
 // exponent of amax minus 2 is the E8M0 code; 127 for an all-zero block;
 // clamped to [0, 254]); codes = RNE-to-E2M1(x * 2^-e), saturating, two per
-// byte, the lower element in the low nibble. Scales go to the atom layout
-// the fused kernel copies to TMEM (amun.h). Rows R..R_pad-1 of the last
-// 128-row atom get code 127 (their W rows read as zero).
+// byte, the lower element in the low nibble. Scales go to the
+// [kblock][row / 128][512-byte atom] layout the fused kernel copies to TMEM
+// (amun.h). Rows R..R_pad-1 of the last 128-row atom get code 127 (their W
+// rows read as zero).
 template <bool BF16>
 __global__ void __launch_bounds__(QZ_THREADS) quantize_mxfp4_kernel(const void* __restrict__ src,
                                                                     int R, int H,
@@ -104,7 +105,8 @@ __global__ void __launch_bounds__(QZ_THREADS) quantize_mxfp4_kernel(const void* 
     }
     if ((lane & 7) == 0) {
       const long long m = r & 127;
-      sf[((r >> 7) * KT + kt) * 512 + 16 * (m & 31) + 4 * (m >> 5) + kb] = (uint8_t)code;
+      sf[((long long)kt * (Rp >> 7) + (r >> 7)) * 512 + 16 * (m & 31) + 4 * (m >> 5) + kb] =
+          (uint8_t)code;
     }
   }
 }

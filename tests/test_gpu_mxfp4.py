@@ -32,7 +32,7 @@ def sf_offsets(R, H):
     """Byte offset of the E8M0 code of (row r, block j) in the atom layout."""
     r = np.arange(R)[:, None]
     j = np.arange(H // 32)[None, :]
-    return ((r // 128) * (H // 128) + j // 4) * 512 + 16 * (r % 32) + 4 * ((r % 128) // 32) + j % 4
+    return ((j // 4) * (-(-R // 128)) + r // 128) * 512 + 16 * (r % 32) + 4 * ((r % 128) // 32) + j % 4
 
 
 def to_device(codes, sexp):
@@ -91,13 +91,19 @@ def oracle_logits(X8, xs, codes, sexp, b):
                       O.as_f64(b))
 
 
-def test_logits_integer_regime_exact():
+@pytest.mark.parametrize("N,V", [
+    (200, 1000),     # 2 M-tiles (ragged), V not a multiple of 128
+    (128, 94720),    # one M-tile: CTA ranges of 640 = tiles 256 | 128 | 256
+    (300, 5000),     # 3 M-tiles, flattened schedule, ranges across M-tiles
+])
+def test_logits_integer_regime_exact(N, V):
     """Integer E4M3 X (x_scale exactly 1) and W on the E2M1 grid with block
     exponents in [-2, 2]: every product and partial sum is a small multiple of
-    1/4, exact in fp32, so the biased logits equal the oracle's bit for bit.
-    Pins the nibble order, the scale-atom layout and the sf ids."""
+    1/8, exact in fp32, so the biased logits equal the oracle's bit for bit.
+    Pins the nibble order, the scale-atom layout, the sf ids and both tile
+    widths (256 in accumulator 0, 128 in accumulator 1)."""
     rng = np.random.default_rng(12)
-    N, H, V = 200, 256, 1000                          # 2 M-tiles (ragged), V not a multiple of 128
+    H = 256
     X = rng.integers(-8, 9, (N, H)).astype(np.float32)
     X[:, 0] = 448.0
     X8, xs = O.quantize_rows_e4m3(X)
