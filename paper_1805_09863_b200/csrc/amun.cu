@@ -128,8 +128,6 @@ struct amun_ol {
   int wbox = 256;       // env AMUN_WBOX: W rows per TMA box, 256 or 64 (64 for tapered tiles)
   int mma_only = 0;     // (amun_bench_variant 5: the MMA issue rate alone)
   int mc = 0;           // env AMUN_MC: W multicast cluster size (experiment; ol_tc.cuh)
-  int early_w = 4;      // env AMUN_EARLYW=n: (PDL, launches without the fused tail) W loads
-                        // of the first n stages before griddepcontrol.wait (0 = none)
   int pdl = 1;          // env AMUN_PDL=0: no programmatic dependent launch of the fused kernel
                         // (single-CTA kernel; greedy path 20.7 -> 19.7 us)
   int pairs_mode = 0;   // env AMUN_PAIRS: 0 auto, 1 never ("off"), 2 always ("force"; tests)
@@ -339,7 +337,6 @@ amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b
     tp.wbox = wbox;
     tp.mc = mc;
     tp.pdl = pairs ? 0 : pl->pdl;
-    tp.early_w = pl->early_w;
     tp.mma_only = pl->mma_only;
     if ((mode == 0 || mode == 4) && pl->hint_ws != workspace) {
       // hint words carry the launch generation (advanced on the device by the
@@ -570,8 +567,6 @@ amun_status amun_ol_create(amun_ol** plan, int H, int V_local, int v_offset, int
     if (mcv) pl->mc = atoi(mcv);
     const char* pd = getenv("AMUN_PDL");
     if (pd) pl->pdl = atoi(pd) != 0;
-    const char* ew = getenv("AMUN_EARLYW");
-    if (ew) pl->early_w = atoi(ew);
     const char* wb = getenv("AMUN_WBOX");
     if (wb) pl->wbox = atoi(wb) == 64 ? 64 : 256;
     const char* pp = getenv("AMUN_PREPASS");

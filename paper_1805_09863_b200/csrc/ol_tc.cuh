@@ -132,21 +132,13 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
   tc_fence_after();
   // (PDL) everything above touched only shared memory / TMEM / the kernel
   // parameters; wait for the previous grid in the stream (completion and
-  // memory visibility) before any global memory access. Exception (early_w):
-  // the TMA producer first issues the W (and bias / scale) loads of its first
-  // stages and waits before its first X load, so the first W round trip
-  // overlaps the previous launch's end. Safe: this launch can only start
-  // early behind a grid that triggered launch_dependents, i.e. this same
-  // fused kernel, which never writes W, b or the scales (any other writer
-  // earlier in the stream has completed before that grid began). N_dev
-  // (written by the previous kernel) and multicast clusters keep the plain
-  // order. Launches with the fused tail too: there the next grid's CTAs get
-  // their SMs only as the tail's merge ends, and early W measured no gain
-  // (cfg greedy path 20.30 / 20.27 / 20.78 us with 0 / 1 / 4 early stages),
-  // while the fused kernel alone gains 16.15 -> 14.76 us with 4 (tools/ab_path.py).
-  const bool early_w = p.pdl && p.early_w && !p.tail && !p.N_dev && p.mc <= 1;
+  // memory visibility) before any global memory access. (Issuing the first
+  // W loads before this wait — W is read-only — gained 1.4 us for the fused
+  // kernel alone at cfg greedy but nothing with the fused tail, and its code
+  // in the producer cost the tail path 2.5 us at cfg beam even when off at
+  // run time; removed.)
   if (p.pdl) {
-    if (!(role == 0 && early_w)) asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (threadIdx.x == 0) tl_mark(p.tl, TL_ENTRY);
   }
   const uint32_t tmem_base = *tmem_holder;
@@ -189,25 +181,9 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
       constexpr int kBlockElems = ELT == 1 || ELT == 3 ? TC_KBYTES : ELT == 2 ? TC_KBYTES / 4
                                                                                : TC_KBYTES / 2;
       int loads = 0;
-      // early_w: the X loads of tile 0's first `deferred` stages (stage s =
-      // K block s, first pass of the ring) wait for griddepcontrol.wait
-      bool waited = !early_w;
-      int deferred = 0, mt0 = 0;
-      auto flush_x = [&]() {
-        asm volatile("griddepcontrol.wait;" ::: "memory");
-        waited = true;
-        if (lane == 0)
-          for (int s = 0; s < deferred; ++s)
-            tma_load_2d(&tmX, &full[s], sA + s * TC_A_BYTES, s * kBlockElems, mt0 * TC_BM, pol_x);
-        __syncwarp();
-      };
       while (it.next(mt, v0, width, last)) {
-        if (tile == 0) mt0 = mt;
-        if (!waited && tile > 0) flush_x();
         if (lane == 0) bias_ring_load(p, sbias, bfull, tile, v0, width, sscale);
         for (int kb = 0; kb < p.n_kblk; ++kb) {
-          // (before any stage is reused: its MMAs need the deferred X)
-          if (!waited && kb >= min(TC_STAGES, p.early_w)) flush_x();
           mbar_wait_spin(&empty[stage], phase ^ 1);
           // (experiment p.mma_only, MODE 2: only the first TC_STAGES blocks are
           // loaded; later stages are marked full without a copy, so the MMAs
@@ -224,7 +200,6 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
             continue;
           }
           const bool load_x = !warm || p.mma_only == 2, load_w = !warm || p.mma_only == 3;
-          if (load_x && !waited) ++deferred;   // (stage == kb here, tile 0)
           if (lane == 0) {
             if (tile == 0 && kb == 0) tl_mark(p.tl, TL_TMA0);
             // W in boxes of p.wbox rows (256, or 64 so narrow tapered tiles
@@ -249,7 +224,7 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
                                        TC_SF_ATOM,
                           nsf * TC_SF_ATOM, &full[stage]);
             }
-            if (load_x && waited)
+            if (load_x)
               tma_load_2d(&tmX, &full[stage], sA + stage * TC_A_BYTES, kb * kBlockElems, mt * TC_BM,
                           pol_x);
             if (p.mc > 1) {
@@ -272,7 +247,6 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
         }
         ++tile;
       }
-      if (!waited) flush_x();   // a range of one tile with <= TC_STAGES K blocks
     } else if (role == 1) {
       // ------------------------------------------------ MMA issuer
       // The whole warp waits; lane 0 issues tcgen05.mma and the commits (a

@@ -47,7 +47,6 @@ struct TcParams {
   int prepass;                             // k-best bound pre-pass over a segment's first n tiles
   int wbox;                                // W rows per TMA box (single-CTA kernel: 256 or 64)
   int pdl;                                 // launched with programmatic stream serialization
-  int early_w;                             // (pdl) W loads of the first early_w stages before the wait
   int mma_only;                            // (experiment, MODE 2) MMAs re-read the first stages
   int mc;                                  // > 1: clusters of mc M-tile CTAs share W (multicast)
 };

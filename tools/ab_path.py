@@ -40,16 +40,12 @@ for _p in (0, 1):
     VARIANTS[f"tail_pdl{_p}"] = {"AMUN_TAIL": "on", "AMUN_PDL": str(_p)}
     VARIANTS[f"sep_pdl{_p}"] = {"AMUN_TAIL": "off", "AMUN_PDL": str(_p)}
     VARIANTS[f"scores_pdl{_p}"] = {"AMUN_TAIL": "off", "AMUN_PDL": str(_p)}
-for _e in (0, 1, 2, 4):   # (PDL) W loads of the first _e stages before griddepcontrol.wait
-    VARIANTS[f"tail_ew{_e}"] = {"AMUN_TAIL": "on", "AMUN_EARLYW": str(_e)}
-    VARIANTS[f"scores_ew{_e}"] = {"AMUN_TAIL": "off", "AMUN_EARLYW": str(_e)}
 for _b in (64, 256):
     VARIANTS[f"sep_box{_b}"] = {"AMUN_TAIL": "off", "AMUN_WBOX": str(_b)}
     VARIANTS[f"scores_box{_b}"] = {"AMUN_TAIL": "off", "AMUN_WBOX": str(_b)}
 for _v in VARIANTS.values():
     _v.setdefault("AMUN_TAPER", "0")
     _v.setdefault("AMUN_PREPASS", "1")
-    _v.setdefault("AMUN_EARLYW", "1")
 NOCHECK = {v for v in VARIANTS if v.startswith("scores")} | {"tailwait", "waitnocoop", "arriveonly"}
 
 
