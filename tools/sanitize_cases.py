@@ -154,6 +154,27 @@ def case_e4m3():
     assert (idx >= 0).all()
 
 
+def case_mxfp4():
+    """MXFP4 W: both tile widths (256 / 128), 3 M-tiles, k = 5 and the k = 1
+    argmax; 3 bit-determinism repeats."""
+    w = synth.Workload("san", H=256, V=30001, S=60, B=5, k=5, seed=synth.BASE_SEED + 907)
+    X, W, b, pc, off = inputs(w)
+    X8, xs = amun().quantize_e4m3(X)
+    W4, sf = amun().quantize_mxfp4(W)
+    ol = amun().OutputLayer(w.H, w.V, dtype="mxfp4", k_max=w.k, max_rows=w.N, max_sentences=w.S)
+    ref = None
+    for _ in range(3):
+        idx, cost = ol.call_mxfp4(X8, xs, W4, sf, b, pc, off, w.k)
+        torch.cuda.synchronize()
+        if ref is None:
+            ref = (idx.clone(), cost.clone())
+        assert torch.equal(ref[0], idx) and torch.equal(ref[1], cost)
+    assert (idx >= 0).all()
+    tok, logit = ol.argmax_mxfp4(X8, xs, W4, sf, b)
+    torch.cuda.synchronize()
+    assert (tok >= 0).all() and (tok < w.V).all()
+
+
 def case_tf32x3():
     w = synth.Workload("san", H=128, V=2001, S=20, B=5, k=5, dtype="f32", seed=synth.BASE_SEED + 905)
     X, W, b, pc, off = inputs(w)
