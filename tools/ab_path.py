@@ -76,7 +76,11 @@ def main():
     variants = os.environ.get("AB_VARIANTS", ",".join(VARIANTS)).split(",")
     dev = torch.device("cuda", 0)
     for name in names:
-        w = synth.CONFIGS[name]
+        # "beam@176": the cfg with S overridden (N = S x B)
+        w = synth.CONFIGS[name.split("@")[0]]
+        if "@" in name:
+            import dataclasses
+            w = dataclasses.replace(w, S=int(name.split("@")[1]))
         X, W, b = synth.gen_X(w).to(dev), synth.gen_W(w).to(dev), synth.gen_b(w).to(dev)
         pc, off = synth.gen_prev_cost(w).to(dev), synth.gen_offsets(w).to(dev)
         wbytes = W.numel() * W.element_size()
