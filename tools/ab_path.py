@@ -40,12 +40,15 @@ for _p in (0, 1):
     VARIANTS[f"tail_pdl{_p}"] = {"AMUN_TAIL": "on", "AMUN_PDL": str(_p)}
     VARIANTS[f"sep_pdl{_p}"] = {"AMUN_TAIL": "off", "AMUN_PDL": str(_p)}
     VARIANTS[f"scores_pdl{_p}"] = {"AMUN_TAIL": "off", "AMUN_PDL": str(_p)}
+for _m in (0, 2, 4, 5, 6):   # W multicast clusters of the M-tiles of a split (experiment)
+    VARIANTS[f"tail_mc{_m}"] = {"AMUN_TAIL": "on", "AMUN_MC": str(_m)}
 for _b in (64, 256):
     VARIANTS[f"sep_box{_b}"] = {"AMUN_TAIL": "off", "AMUN_WBOX": str(_b)}
     VARIANTS[f"scores_box{_b}"] = {"AMUN_TAIL": "off", "AMUN_WBOX": str(_b)}
 for _v in VARIANTS.values():
     _v.setdefault("AMUN_TAPER", "0")
     _v.setdefault("AMUN_PREPASS", "1")
+    _v.setdefault("AMUN_MC", "0")
 NOCHECK = {v for v in VARIANTS if v.startswith("scores")} | {"tailwait", "waitnocoop", "arriveonly"}
 
 
