@@ -27,6 +27,8 @@ Readings of the paper (listed in DESIGN.md):
   G6    optional per-sentence k_s <= k (shrinking beam); default k.
   G8    compaction is stable.
   G11   fewer valid candidates than k -> pad with (idx=-1, cost=-inf).
+  G20   4-bit W storage: OCP MX v1.0 MXFP4 (E2M1 codes, one E8M0 scale per
+        32 elements), quantize_rows_mxfp4 / dequant_rows_mxfp4.
 
 Every function's pins (what fixes it independently of itself) are listed in
 tests/test_oracle.py; none of the functions below is "parity unpinned".
