@@ -291,9 +291,8 @@ amun_status amun_quantize_e4m3(const void* src, amun_dtype src_dtype, int R, int
  * computed by tcgen05.mma kind::mxf8f6f4.block_scale (the block scales are
  * applied inside the tensor core; fp32 accumulation), then the same
  * softmax / k-best / merge as amun_output_layer. Plan: amun_ol_create(...,
- * AMUN_MXFP4, ...), H % 128 == 0; single-CTA kernel, tiles of 256 and 128
- * columns alternating (tensor memory holds the scales beside the narrow
- * accumulator).
+ * AMUN_MXFP4, ...), H % 128 == 0; single-CTA kernel, 224-column tiles
+ * (tensor memory holds the scales beside the two accumulators).
  *
  * Layouts (device):
  *   W4   [V_local, H/2] uint8: two codes per byte, element 2j in the low

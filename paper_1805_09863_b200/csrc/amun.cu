@@ -213,7 +213,7 @@ Schedule make_schedule(const amun_ol* pl, int N, int* grid) {
   const bool pairs = use_pairs(pl, N);
   const long long G = pairs ? pl->num_sms / 2 : pl->num_sms;
   const long long n_mt = cdiv(N > 0 ? N : 1, pairs ? 256 : 128);
-  const long long align = pl->dtype == AMUN_MXFP4 ? TC_F4_ALIGN : 16;   // scale atoms: 128 W rows
+  const long long align = pl->dtype == AMUN_MXFP4 ? TC_F4_ALIGN : 16;   // mxfp4: 32-row groups
   Schedule s = schedule_for(n_mt, cdiv(pl->V_local, align) * align, G, align);
   const int units = (int)cdiv((n_mt - 1) * s.band + s.Vp, s.C);
   *grid = pairs ? 2 * units : units;
@@ -278,7 +278,7 @@ amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b
     if (pl->mc > 1 && !pairs && !N_dev && mode != 1 && sch.band != sch.Vp &&
         cdiv(N, TC_BM) == pl->mc && grid % pl->mc == 0)
       mc = pl->mc;
-    const int wbox = pl->dtype == AMUN_MXFP4 ? TC_BN_F4_ODD : mc > 1 ? 64 : pl->wbox;
+    const int wbox = pl->dtype == AMUN_MXFP4 ? TC_BN_F4 : mc > 1 ? 64 : pl->wbox;
     amun_status s = get_map(pl, pl->xmaps, 4, pl->xnext, X, N, a_rows, kbytes, &mx);
     if (s != AMUN_OK) return s;
     s = get_map(pl, pl->wmaps, 8, pl->wnext, W, pl->V_local, pairs ? TC_BN / 2 : wbox, kbytes,

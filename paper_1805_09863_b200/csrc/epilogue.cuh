@@ -450,9 +450,7 @@ struct TileIter {
   long long pos, end;
   Schedule sch;
   int taper = 0;
-  int wmax = 256;       // widest even tile (the CTA's 1st, 3rd, ... tile: accumulator 0)
-  int wmax_odd = 256;   // widest odd tile (accumulator 1; 128 for MXFP4, tc_epi.cuh)
-  int count = 0;
+  int wmax = 256;   // widest tile (224 for MXFP4: TMEM columns for the scale factors)
   __device__ __forceinline__ bool next(int& mt, int& v0, int& width, bool& last) {
     for (;;) {
       if (pos >= end) return false;
@@ -467,9 +465,8 @@ struct TileIter {
 #ifdef TC_BN_OVERRIDE
       width = (int)min((long long)TC_BN_OVERRIDE, seg_end - v0);
 #else
-      const int cap = (count++ & 1) ? wmax_odd : wmax;
       width = (taper && base + sch.Vp >= end) ? taper_width(seg_end - v0)
-                                              : (int)min((long long)cap, seg_end - v0);
+                                              : (int)min((long long)wmax, seg_end - v0);
 #endif
       last = (v0 + width == seg_end);
       pos += width;

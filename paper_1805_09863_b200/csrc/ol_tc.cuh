@@ -40,9 +40,17 @@ constexpr int TC_B_BYTES = TC_BN * TC_KBYTES;   // 16 KB (32 KB)
 constexpr int TC_SMEM = TC_STAGES * (TC_A_BYTES + TC_B_BYTES) + TC_BIAS_BYTES + TC_XCH_BYTES +
                         TC_THRX_BYTES + 1024 /*align*/ + 512 /*barriers*/;
 constexpr int TC_SMEM_F8 = TC_SMEM + TC_SCALE_BYTES;   // + the e4m3 column-scale ring
-constexpr int TC_SMEM_F4 = TC_SMEM + (2 * TC_STAGES + 1) * TC_SF_ATOM;   // + the mxfp4 scale atoms
+// MXFP4 (ELT 3): W stages of 224 rows (28 KB unpacked); per stage the raw
+// scale atoms (up to 3) and the 2 atoms re-based to the tile's first row;
+// A's constant atom.
+constexpr int TC_B_BYTES_F4 = TC_BN_F4 * TC_KBYTES;
+constexpr int TC_SMEM_F4 = TC_STAGES * (TC_A_BYTES + TC_B_BYTES_F4) + TC_BIAS_BYTES +
+                           TC_XCH_BYTES + TC_THRX_BYTES + 1024 + 512 +
+                           (1 + TC_STAGES * (TC_SF_RAW + 2)) * TC_SF_ATOM;
 static_assert(TC_SMEM_F8 <= 227 * 1024 && TC_SMEM_F4 <= 227 * 1024, "shared memory budget");
-static_assert(TC_SFA_COL >= 256 + TC_BN_F4_ODD && tc_sfb_col(TC_STAGES - 1) + 8 <= 512,
+static_assert(TC_B_BYTES_F4 % 1024 == 0, "SW128 tiles are 1024-byte aligned");
+static_assert(TC_SFA_COL >= TC_BN_F4 && tc_sfb_col(2) + 8 <= 256 &&
+              tc_sfb_col(3) >= 256 + TC_BN_F4 && tc_sfb_col(TC_STAGES - 1) + 8 <= 512,
               "mxfp4 scale columns overlap an accumulator");
 static_assert(TC_NBIAS >= 2 + TC_STAGES, "bias ring too small for the producer's lead");
 
@@ -53,22 +61,25 @@ static_assert(TC_NBIAS >= 2 + TC_STAGES, "bias ring too small for the producer's
 // as [X_hi | X_hi | X_lo] and [W_hi | W_lo | W_hi], so the K = 3H product is
 // X_hi W_hi + X_hi W_lo + X_lo W_hi (NEXT f2).
 // ELT = 3: e4m3 X with per-row scales, MXFP4 W (E2M1 codes + one E8M0 scale
-// per 32 K elements) on kind::mxf8f6f4.block_scale; tiles of 256 and 128
-// columns alternate (TMEM holds the scales beside the 128-column
-// accumulator, tc_epi.cuh); each stage also carries the K block's W scale
-// atoms of the tile (one per 128 rows), copied to TMEM by the MMA thread
-// (tcgen05.cp, ordered before that stage's MMAs) (NEXT f4).
+// per 32 K elements) on kind::mxf8f6f4.block_scale; 224-column tiles (TMEM
+// holds the scales beside the accumulators, tc_epi.cuh). Each stage also
+// carries the K block's W scale atoms covering the tile's rows (one bulk
+// copy of up to 3 contiguous 128-row atoms); warp 10 (a control warp that
+// was idle) re-bases them to the tile's first row (2 atoms, the layout
+// tcgen05.cp reads), and the MMA thread copies those to TMEM before the
+// stage's MMAs (NEXT f4).
 template <int KB, int MODE, int NG, int ELT = 0>
 __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
     ol_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                  const TcParams p) {
   using Cfg = TcCfg<NG>;
+  constexpr int kBBytes = ELT == 3 ? TC_B_BYTES_F4 : TC_B_BYTES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
   uint8_t* sB = sA + TC_STAGES * TC_A_BYTES;
-  float* sbias = reinterpret_cast<float*>(sB + TC_STAGES * TC_B_BYTES);
+  float* sbias = reinterpret_cast<float*>(sB + TC_STAGES * kBBytes);
   float* xch = sbias + TC_NBIAS * TC_BN;
   unsigned long long* thr_x = reinterpret_cast<unsigned long long*>(xch + 128 * TC_XCH_FLOATS);
   uint64_t* full = reinterpret_cast<uint64_t*>(thr_x + TC_THRX_BYTES / 8);
@@ -81,9 +92,13 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
   float* sscale = (ELT == 1 && scale_ring_ok(p, TC_STAGES))
                       ? reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(full) + 512)
                       : nullptr;
-  // mxfp4: W scale atoms [TC_STAGES][2][512] then A's constant atom (TC_SMEM_F4)
-  uint8_t* ssf = reinterpret_cast<uint8_t*>(full) + 512;
-  uint8_t* ssfa = ssf + 2 * TC_STAGES * TC_SF_ATOM;
+  // mxfp4 (TC_SMEM_F4): A's constant atom, the raw scale atoms
+  // [TC_STAGES][TC_SF_RAW][512], the re-based ones [TC_STAGES][2][512]; the
+  // re-based stages' barriers after the others in the barrier area
+  uint8_t* ssfa = reinterpret_cast<uint8_t*>(full) + 512;
+  uint8_t* ssf_raw = ssfa + TC_SF_ATOM;
+  uint8_t* ssf = ssf_raw + TC_STAGES * TC_SF_RAW * TC_SF_ATOM;
+  uint64_t* sfready = full + 40;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -120,6 +135,8 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
       mbar_init(&tempty[i], NG * 4);        // one arrival per epilogue warp
     }
     for (int i = 0; i < TC_NBIAS; ++i) mbar_init(&bfull[i], 1);
+    if constexpr (ELT == 3)
+      for (int i = 0; i < TC_STAGES; ++i) mbar_init(&sfready[i], 1);
     fence_barrier_init();
   }
   if (role == 1) {
@@ -169,10 +186,7 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
       const uint64_t pol_x = policy_evict_last();     // X is re-read by every CTA
       TileIter it{start, stop, dyn.sch};
       it.taper = p.taper;
-      if constexpr (ELT == 3) {
-        it.wmax = TC_BN_F4;
-        it.wmax_odd = TC_BN_F4_ODD;
-      }
+      if constexpr (ELT == 3) it.wmax = TC_BN_F4;
       int mt, v0, width;
       bool last;
       int stage = 0, tile = 0;
@@ -210,18 +224,18 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
             // (mxfp4 W: the transaction counts the packed global bytes, half
             // the unpacked shared-memory box)
             constexpr int kWDiv = ELT == 3 ? 2 : 1;
-            const int nsf = width > 128 ? 2 : 1;   // mxfp4 scale atoms of the tile
+            // mxfp4: this K block's 128-row scale atoms covering the tile's
+            // rows, contiguous in the [kblock][row / 128][512] layout
+            const int nb128 = (p.V_local + 127) / 128;
+            const int nsf = ELT == 3 ? min(((v0 & 127) + width - 1) / 128 + 1, nb128 - v0 / 128) : 0;
             mbar_arrive_expect_tx(&full[stage], (load_x ? p.a_box_bytes : 0) +
                                                     (load_w ? nbox * wbox * TC_KBYTES / kWDiv : 0) +
                                                     (ELT == 3 && load_w ? nsf * TC_SF_ATOM : 0));
             if constexpr (ELT == 3) {
-              // this K block's scale atoms of the tile's rows: contiguous in the
-              // [kblock][row / 128][512] layout (v0 is 128-aligned)
-              AMUN_DCHECK(v0 % TC_F4_ALIGN == 0);
+              AMUN_DCHECK(v0 % TC_F4_ALIGN == 0 && nsf >= 1 && nsf <= TC_SF_RAW);
               if (load_w)
-                bulk_load(ssf + stage * 2 * TC_SF_ATOM,
-                          p.w_sf + ((long long)kb * ((p.V_local + 127) / 128) + v0 / 128) *
-                                       TC_SF_ATOM,
+                bulk_load(ssf_raw + stage * TC_SF_RAW * TC_SF_ATOM,
+                          p.w_sf + ((long long)kb * nb128 + v0 / 128) * TC_SF_ATOM,
                           nsf * TC_SF_ATOM, &full[stage]);
             }
             if (load_x)
@@ -230,12 +244,12 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
             if (p.mc > 1) {
               // this CTA's box of the W tile, multicast to the whole cluster
               for (int j = (int)mc_rank; load_w && j < nbox; j += p.mc)
-                tma_load_2d_mc(&tmW, &full[stage], sB + stage * TC_B_BYTES + j * wbox * TC_KBYTES,
+                tma_load_2d_mc(&tmW, &full[stage], sB + stage * kBBytes + j * wbox * TC_KBYTES,
                                kb * kBlockElems, v0 + j * wbox, (uint16_t)((1u << p.mc) - 1u));
             }
             for (int j = 0; load_w && p.mc <= 1 && j < nbox; ++j) {
               // (the L2 hint measured the same as evict_first / evict_normal / none)
-              tma_load_2d(&tmW, &full[stage], sB + stage * TC_B_BYTES + j * wbox * TC_KBYTES,
+              tma_load_2d(&tmW, &full[stage], sB + stage * kBBytes + j * wbox * TC_KBYTES,
                           kb * kBlockElems, v0 + j * wbox, 0ull);
             }
           }
@@ -253,10 +267,7 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
       // commit tracks the MMAs issued by the same thread).
       TileIter it{start, stop, dyn.sch};
       it.taper = p.taper;
-      if constexpr (ELT == 3) {
-        it.wmax = TC_BN_F4;
-        it.wmax_odd = TC_BN_F4_ODD;
-      }
+      if constexpr (ELT == 3) it.wmax = TC_BN_F4;
       int mt, v0, width;
       bool last;
       int stage = 0;
@@ -275,11 +286,12 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
                                         : idesc_bf16_f32(TC_BM, width);
         for (int kb = 0; kb < p.n_kblk; ++kb) {
           mbar_wait_spin(&full[stage], phase);
+          if constexpr (ELT == 3) mbar_wait_spin(&sfready[stage], phase);   // re-based scales
           tc_fence_after();
           if (lane == 0) {
             if (kb == 0 && mtile == 1) tl_mark(p.tl, TL_FULL0);
             const uint64_t ad = sdesc_k<TC_KBYTES>(smem_u32(sA + stage * TC_A_BYTES));
-            const uint64_t bd = sdesc_k<TC_KBYTES>(smem_u32(sB + stage * TC_B_BYTES));
+            const uint64_t bd = sdesc_k<TC_KBYTES>(smem_u32(sB + stage * kBBytes));
             uint32_t sfb = 0;
             if constexpr (ELT == 3) {   // this stage's W scales -> TMEM (ordered before the MMAs)
               sfb = tmem_base + tc_sfb_col(stage);
@@ -317,6 +329,40 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
         if (acc == 0) acc_phase ^= 1;
       }
       if (lane == 0) tl_mark(p.tl, TL_MMA_END);
+    } else if (ELT == 3 && role == 2) {
+      // ------------------------------------------------ mxfp4 scale re-basing
+      // Per stage: the raw atoms hold rows 128 a + (0..383) of the K block's
+      // scales (a = v0 / 128); the tile's row n = 32 b + n' (b = (v0 % 128) /
+      // 32) goes to re-based atom n / 128, row n % 32, word (n / 32) % 4.
+      // Lane m0 moves the 8 words of rows m0 + 32 j, j < 8.
+      TileIter it{start, stop, dyn.sch};
+      it.wmax = TC_BN_F4;
+      int mt, v0, width;
+      bool last;
+      int stage = 0;
+      uint32_t phase = 0;
+      while (it.next(mt, v0, width, last)) {
+        const int b = (v0 & 127) >> 5;
+        for (int kb = 0; kb < p.n_kblk; ++kb) {
+          mbar_wait_spin(&full[stage], phase);
+          const uint32_t* raw =
+              reinterpret_cast<const uint32_t*>(ssf_raw + stage * TC_SF_RAW * TC_SF_ATOM);
+          uint32_t* dst = reinterpret_cast<uint32_t*>(ssf + stage * 2 * TC_SF_ATOM);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int g = b + j;   // 32-row group of the raw atoms
+            dst[(j >> 2) * (TC_SF_ATOM / 4) + 4 * lane + (j & 3)] =
+                raw[(g >> 2) * (TC_SF_ATOM / 4) + 4 * lane + (g & 3)];
+          }
+          fence_proxy_async_smem();   // generic writes -> tcgen05.cp (async proxy)
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&sfready[stage]);
+          if (++stage == TC_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
     }
   } else {
     reg_alloc<Cfg::kEpiRegs>();

@@ -114,19 +114,21 @@ constexpr int TC_NSCALE = 4;
 constexpr int TC_SCALE_BYTES = TC_NSCALE * TC_BN * 4;
 // MXFP4 plans (ELT 3). The block-scaled MMA costs about the same per
 // instruction at N = 128 as at N = 256 (bare GEMM at cfg beam 93 vs 51 us),
-// so tiles stay wide; but two 256-column accumulators fill TMEM, leaving no
-// columns for the scale factors. Tiles therefore alternate: even tiles of a
-// CTA up to 256 columns in accumulator 0 (TMEM columns [0, 256)), odd tiles
-// up to 128 columns in accumulator 1 ([256, 384)); the scales sit in
-// [384, 512): A's (constant 1.0, written once) at TC_SFA_COL, B's of
-// pipeline stage s (two 512-byte atoms = 256 rows, 8 columns) at
-// tc_sfb_col(s). Widths are 128 or 256 and every tile starts on a 128-row
-// boundary (the scale atoms cover 128 W rows; schedule_for align 128).
-constexpr int TC_BN_F4 = 256, TC_BN_F4_ODD = 128;
-constexpr int TC_F4_ALIGN = 128;
+// so tiles stay wide: TC_BN_F4 = 224 columns, the two accumulators in TMEM
+// columns [0, 224) and [256, 480), the scales in the 64 columns left: A's
+// (constant 1.0, written once) at TC_SFA_COL, B's of pipeline stage s (two
+// 512-byte atoms = 256 rows, 8 columns) at tc_sfb_col(s). Tiles start on
+// 32-row boundaries (schedule_for align 32): the stage's atoms are re-based
+// to the tile's first row in shared memory by a helper warp (the MMA's
+// scale address can only move in 64-row steps).
+constexpr int TC_BN_F4 = 224;
+constexpr int TC_F4_ALIGN = 32;
 constexpr int TC_SF_ATOM = 512;
-constexpr uint32_t TC_SFA_COL = 384;
-__host__ __device__ constexpr uint32_t tc_sfb_col(int stage) { return 392u + 8u * (uint32_t)stage; }
+constexpr int TC_SF_RAW = 3;   // 128-row atoms a stage's tile rows can touch
+constexpr uint32_t TC_SFA_COL = 224;
+__host__ __device__ constexpr uint32_t tc_sfb_col(int stage) {
+  return stage < 3 ? 228u + 8u * (uint32_t)stage : 480u + 8u * (uint32_t)(stage - 3);
+}
 
 // Launch configuration of NG epilogue warpgroups (warps 0 .. 4NG-1) + the
 // control warpgroup (TMA producer warp, MMA warp, 2 idle warps), and the setmaxnreg budget,
@@ -211,10 +213,7 @@ __device__ __forceinline__ void tc_epilogue(const TcParams& p, uint32_t tmem_bas
   st.reset();
   TileIter it{start, stop, dyn.sch};
   it.taper = PAIR ? 0 : p.taper;
-  if constexpr (ELT == 3) {
-    it.wmax = TC_BN_F4;
-    it.wmax_odd = TC_BN_F4_ODD;
-  }
+  if constexpr (ELT == 3) it.wmax = TC_BN_F4;
   int unit, v0, width;
   bool last;
   int acc = 0, tile = 0;
