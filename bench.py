@@ -520,47 +520,102 @@ def e2e_measure(p: Problem, ctx: Ctx, K: int, warmup: int, eager: bool):
         step(i)
     torch.cuda.synchronize()
     graphs = ctx.world == 1 and not eager
+    period = 2 * nW // (2 if nW % 2 == 0 else 1)
+    mode = "eager calls"
+    launch = [s_copy]   # streams the timed region's start / end are ordered with
     if graphs:
-        # one copy graph per buffer pair, one compute graph per (pair, W copy)
-        period = 2 * nW // (2 if nW % 2 == 0 else 1)
-        g_copy, g_comp = [], {}
-        for j in range(2):
-            gc = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(gc, stream=s_copy):
-                copies(j)
-            g_copy.append(gc)
-        for i in range(period):
-            j, c = i % 2, i % nW
-            if (j, c) in g_comp:
-                continue
-            gm = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(gm, stream=s_comp):
-                compute(j, c)
-            g_comp[(j, c)] = gm
-        torch.cuda.synchronize()
-        for e in comp_done:
-            e.record(s_comp)
+        try:
+            # ONE graph per step (per (buffer pair, W copy)): the copy branch
+            # waits (external event) for step i-2's call, reads its results
+            # back and brings step i's inputs; the compute branch waits for the
+            # copies and for step i-1's call (external event), then calls. The
+            # graphs are launched on two alternating streams, so step i+1's
+            # copies overlap step i's call with one host call per step.
+            xev = [torch.cuda.Event(external=True) for _ in range(2)]
+            s_a, s_b, s_cb = (torch.cuda.Stream(dev) for _ in range(3))
+            G = {}
+            for i in range(period):
+                j, c = i % 2, i % nW
+                if (j, c) in G:
+                    continue
+                origin = s_a if j == 0 else s_b
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=origin):
+                    origin.wait_event(xev[j])
+                    copies(j)
+                    ev = torch.cuda.Event()
+                    ev.record(origin)
+                    s_cb.wait_event(ev)
+                    s_cb.wait_event(xev[1 - j])
+                    with torch.cuda.stream(s_cb):
+                        compute(j, c)
+                    xev[j].record(s_cb)
+                    origin.wait_stream(s_cb)
+                G[(j, c)] = g
+            torch.cuda.synchronize()
+            for e in xev:
+                e.record(s_a)
+            prev = torch.cuda.current_stream(dev)
 
-        def step(i):   # noqa: F811  (graph-replay version of the step above)
-            j = i % 2
-            with torch.cuda.stream(s_copy):
-                s_copy.wait_event(comp_done[j])
-                g_copy[j].replay()
-                h2d_done[j].record(s_copy)
-            with torch.cuda.stream(s_comp):
-                s_comp.wait_event(h2d_done[j])
-                g_comp[(j, i % nW)].replay()
-                comp_done[j].record(s_comp)
+            def step(i):   # noqa: F811  (one graph launch per step)
+                torch.cuda.set_stream(s_a if i % 2 == 0 else s_b)
+                G[(i % 2, i % nW)].replay()
 
-        for i in range(warmup):
-            step(i)
-        torch.cuda.synchronize()
+            for i in range(warmup + 2):
+                step(i)
+            torch.cuda.set_stream(prev)
+            torch.cuda.synchronize()
+            comp_done = xev
+            launch = [s_a, s_b]
+            mode = "one CUDA graph per step (copies and call on two streams, external events)"
+        except Exception as ex:   # noqa: BLE001  (fall back: copy / call graphs per step)
+            torch.cuda.synchronize()
+            graphs = False
+            mode = f"copy and call graphs per step (one-graph steps failed: {type(ex).__name__})"
+            g_copy, g_comp = [], {}
+            for j in range(2):
+                gc = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gc, stream=s_copy):
+                    copies(j)
+                g_copy.append(gc)
+            for i in range(period):
+                j, c = i % 2, i % nW
+                if (j, c) in g_comp:
+                    continue
+                gm = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(gm, stream=s_comp):
+                    compute(j, c)
+                g_comp[(j, c)] = gm
+            torch.cuda.synchronize()
+            for e in comp_done:
+                e.record(s_comp)
+
+            def step(i):   # noqa: F811  (graph-replay version of the step above)
+                j = i % 2
+                with torch.cuda.stream(s_copy):
+                    s_copy.wait_event(comp_done[j])
+                    g_copy[j].replay()
+                    h2d_done[j].record(s_copy)
+                with torch.cuda.stream(s_comp):
+                    s_comp.wait_event(h2d_done[j])
+                    g_comp[(j, i % nW)].replay()
+                    comp_done[j].record(s_comp)
+
+            for i in range(warmup):
+                step(i)
+            torch.cuda.synchronize()
     ctx.barrier()
     s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s2.record(s_copy)
+    s2.record(launch[0])
+    for st_ in launch[1:]:
+        st_.wait_event(s2)
+    prev = torch.cuda.current_stream(dev)
     for i in range(K):
         step(i)
+    torch.cuda.set_stream(prev)
     with torch.cuda.stream(s_copy):   # the last two steps' results
+        for st_ in launch:
+            s_copy.wait_stream(st_)
         for i in (K - 2, K - 1):
             if i >= 0:
                 s_copy.wait_event(comp_done[i % 2])
@@ -574,9 +629,7 @@ def e2e_measure(p: Problem, ctx: Ctx, K: int, warmup: int, eager: bool):
                     "the previous step's idx | cost as ONE HBM -> pinned host copy on a copy "
                     "stream (inputs and outputs double-buffered, overlapping the compute "
                     "stream); the public-API call writing into its output buffer; the last two "
-                    "steps' results read back inside the timed region; W, b resident; "
-                    + ("each buffer pair's copies and each call replayed as CUDA graphs"
-                       if graphs else "eager calls")}
+                    "steps' results read back inside the timed region; W, b resident; " + mode}
 
 
 def side_workload(name, w, ctx, K, warmup, peaks, n_sent, eager):
