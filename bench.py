@@ -454,7 +454,7 @@ def ranks_identical(ctx, idx, cost):
     return bool(torch.equal(lo, hi))
 
 
-def e2e_measure(p: Problem, ctx: Ctx, K: int, warmup: int, eager: bool):
+def e2e_measure(p: Problem, ctx: Ctx, K: int, warmup: int, eager: bool, clk=None):
     """Same metric through the public API with host buffers. Every step: X |
     prev_cost | beam_offsets as ONE pinned host -> HBM copy and the previous
     results' idx | cost as ONE HBM -> pinned host copy, both on a copy stream
@@ -605,6 +605,9 @@ def e2e_measure(p: Problem, ctx: Ctx, K: int, warmup: int, eager: bool):
                 step(i)
             torch.cuda.synchronize()
     ctx.barrier()
+    if clk:
+        clk.wait_first()
+        clk.mark("t_start")
     s2, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s2.record(launch[0])
     for st_ in launch[1:]:
@@ -622,9 +625,23 @@ def e2e_measure(p: Problem, ctx: Ctx, K: int, warmup: int, eager: bool):
                 out_p[i % 2].copy_(out_d[i % 2], non_blocking=True)
         e2.record(s_copy)
     torch.cuda.synchronize()
+    if clk:
+        clk.mark("t_end")
     ms = ctx.max(s2.elapsed_time(e2))
+    # context: this box's pinned host -> HBM bandwidth for the step's input
+    # copy alone (when it is slower than the call, e2e is copy-bound)
+    reps = 20
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(s_copy):
+        c0.record(s_copy)
+        for _ in range(reps):
+            in_d[0].copy_(in_p, non_blocking=True)
+        c1.record(s_copy)
+    torch.cuda.synchronize()
+    h2d_us = c0.elapsed_time(c1) / reps * 1e3
     return {"value": w.N / (ms / K * 1e-3), "unit": UNIT, "h2d_bytes_per_step": in_bytes,
             "d2h_bytes_per_step": out_bytes,
+            "h2d_copy_alone_us": h2d_us, "h2d_GBps": in_bytes / (h2d_us * 1e-6) / 1e9,
             "note": "every step: X | prev_cost | beam_offsets as ONE pinned host -> HBM copy and "
                     "the previous step's idx | cost as ONE HBM -> pinned host copy on a copy "
                     "stream (inputs and outputs double-buffered, overlapping the compute "
@@ -884,7 +901,12 @@ def main():
     roof["kernel_share_of_step"] = m["kernel_ms"] / ms_per_step
     roof["kernel_alone_no_tail_ms"] = m["kernel_alone_no_tail_ms"]
 
-    e2e = e2e_measure(p, ctx, K, args.warmup, args.eager)
+    # (a short pause: the e2e region starts from the same thermal / power
+    # state as the device-timed one; its clocks are reported with it)
+    time.sleep(1.0)
+    with ClockSampler(local) as clk_e2e:
+        e2e = e2e_measure(p, ctx, K, args.warmup, args.eager, clk_e2e)
+    e2e["clocks"] = clk_e2e.summary()
 
     # ---- CPU baseline (oracle, rank 0, N = 1) and oracle parity (rank 0, every N)
     cpu, parity = None, None

@@ -18,6 +18,10 @@ __global__ void __launch_bounds__(QZ_THREADS) quantize_e4m3_kernel(const void* _
                                                                    uint8_t* __restrict__ dst,
                                                                    float* __restrict__ scale) {
   __shared__ float red[QZ_THREADS / 32];
+  // the fused output-layer kernel that reads these codes is launched with
+  // programmatic stream serialization: let it start its prologue now (it
+  // waits for this grid's completion before any global access)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int tid = threadIdx.x;
   for (int r = blockIdx.x; r < R; r += gridDim.x) {
     auto at = [&](int h) -> float {
