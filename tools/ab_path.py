@@ -42,6 +42,8 @@ for _p in (0, 1):
     VARIANTS[f"scores_pdl{_p}"] = {"AMUN_TAIL": "off", "AMUN_PDL": str(_p)}
 for _m in (0, 2, 4, 5, 6):   # W multicast clusters of the M-tiles of a split (experiment)
     VARIANTS[f"tail_mc{_m}"] = {"AMUN_TAIL": "on", "AMUN_MC": str(_m)}
+for _g in (2, 4):   # epilogue warpgroups (4 needs a -DAMUN_WITH_NG4 build, AMUN_LIB)
+    VARIANTS[f"tail_ng{_g}"] = {"AMUN_TAIL": "on", "AMUN_NG": str(_g)}
 for _b in (64, 256):
     VARIANTS[f"sep_box{_b}"] = {"AMUN_TAIL": "off", "AMUN_WBOX": str(_b)}
     VARIANTS[f"scores_box{_b}"] = {"AMUN_TAIL": "off", "AMUN_WBOX": str(_b)}
@@ -49,6 +51,7 @@ for _v in VARIANTS.values():
     _v.setdefault("AMUN_TAPER", "0")
     _v.setdefault("AMUN_PREPASS", "1")
     _v.setdefault("AMUN_MC", "0")
+    _v.setdefault("AMUN_NG", "2")
 NOCHECK = {v for v in VARIANTS if v.startswith("scores")} | {"tailwait", "waitnocoop", "arriveonly"}
 
 
@@ -95,9 +98,9 @@ def main():
             os.environ.update(VARIANTS[v])
             layers[v] = amun.OutputLayer(w.H, w.V, dtype=w.dtype, k_max=w.k, max_rows=w.N,
                                          max_sentences=w.S)
-        ref = {}   # bit-identical outputs within one taper setting (the tile
-        # widths decide which warpgroup sums which chunk, so taper on / off
-        # differ in the last bits of the sums)
+        ref = {}   # bit-identical outputs within one taper / NG setting (the
+        # tile widths and warpgroup count decide which warpgroup sums which
+        # chunk, so they differ in the last bits of the sums)
         res = {v: [] for v in variants}
         for rnd in range(3):
             for v in variants:
@@ -117,7 +120,7 @@ def main():
                 if v in NOCHECK:
                     pass
                 else:
-                    t = VARIANTS[v]["AMUN_TAPER"]
+                    t = (VARIANTS[v]["AMUN_TAPER"], VARIANTS[v]["AMUN_NG"])
                     if t not in ref:
                         ref[t] = (oi.clone(), oc.clone())
                     assert torch.equal(ref[t][0], oi) and torch.equal(ref[t][1], oc), v
