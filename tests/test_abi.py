@@ -93,3 +93,22 @@ def test_null_plan_calls(lib):
     assert lib.amun_ol_scores(None, None, None, None, 1, None, None) == 1
     assert lib.amun_argmax(None, None, None, None, 1, None, None, None, None) == 1
     assert lib.amun_merge_partials(None, None, 1, None, None, 0, 0, None, 1, None, None, None) == 1
+
+
+def test_mxfp4_host_checks(lib):
+    """MXFP4 scale-atom sizes (amun.h layout: [H/128][ceil(R/128)][512 B])
+    and the quantiser's / entry points' host validation (no launch)."""
+    assert lib.amun_mxfp4_sf_bytes(300, 256) == 2 * 3 * 512
+    assert lib.amun_mxfp4_sf_bytes(128, 1024) == 8 * 1 * 512
+    assert lib.amun_mxfp4_sf_bytes(0, 256) == 0
+    assert lib.amun_mxfp4_sf_bytes(10, 192) == 0        # H % 128 != 0
+    assert lib.amun_mxfp4_sf_bytes(-1, 256) == 0
+    buf = ctypes.c_void_p(16)
+    assert lib.amun_quantize_mxfp4(buf, 7, 4, 256, buf, buf, None) == 1          # bad src dtype
+    assert lib.amun_quantize_mxfp4(buf, 0, 4, 192, buf, buf, None) == 1          # H % 128
+    assert b"128" in lib.amun_last_error()
+    assert lib.amun_quantize_mxfp4(None, 0, 4, 256, buf, buf, None) == 1         # NULL src
+    assert lib.amun_quantize_mxfp4(buf, 0, 0, 256, None, None, None) == 0        # R = 0: no-op
+    assert lib.amun_argmax_mxfp4(None, None, None, None, None, None, 1, None, None, None, None) == 1
+    assert lib.amun_output_layer_mxfp4(None, None, None, None, None, None, None, None, 1, 1, None,
+                                       1, None, None, None, None) == 1
