@@ -128,11 +128,12 @@ struct amun_ol {
   int wbox = 256;       // env AMUN_WBOX: W rows per TMA box, 256 or 64 (64 for tapered tiles)
   int mma_only = 0;     // (amun_bench_variant 5: the MMA issue rate alone)
   int mc = 0;           // env AMUN_MC: W multicast cluster size (experiment; ol_tc.cuh)
+  int wnarrow = 1;      // env AMUN_WNARROW=0: remainder tiles load full 256-row W boxes
   int pdl = 1;          // env AMUN_PDL=0: no programmatic dependent launch of the fused kernel
                         // (single-CTA kernel; greedy path 20.7 -> 19.7 us)
   int pairs_mode = 0;   // env AMUN_PAIRS: 0 auto, 1 never ("off"), 2 always ("force"; tests)
   MapEntry xmaps[4];
-  MapEntry wmaps[8];
+  MapEntry wmaps[16];   // (two maps per W: 256- and 64-row boxes)
   int xnext = 0, wnext = 0;
 };
 
@@ -281,9 +282,18 @@ amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b
     const int wbox = pl->dtype == AMUN_MXFP4 ? TC_BN_F4 : mc > 1 ? 64 : pl->wbox;
     amun_status s = get_map(pl, pl->xmaps, 4, pl->xnext, X, N, a_rows, kbytes, &mx);
     if (s != AMUN_OK) return s;
-    s = get_map(pl, pl->wmaps, 8, pl->wnext, W, pl->V_local, pairs ? TC_BN / 2 : wbox, kbytes,
+    s = get_map(pl, pl->wmaps, 16, pl->wnext, W, pl->V_local, pairs ? TC_BN / 2 : wbox, kbytes,
                 &mw);
     if (s != AMUN_OK) return s;
+    // single CTAs with 256-row W boxes: a second map of 64-row boxes for the
+    // narrow remainder tile of each CTA range (ol_tc.cuh)
+    const CUtensorMap* mwn = mw;
+    const bool wnarrow = pl->wnarrow && !pairs && pl->dtype != AMUN_MXFP4 && wbox == 256 &&
+                         mc <= 1;
+    if (wnarrow) {
+      s = get_map(pl, pl->wmaps, 16, pl->wnext, W, pl->V_local, 64, kbytes, &mwn);
+      if (s != AMUN_OK) return s;
+    }
     TcParams tp;
     memset(&tp, 0, sizeof(tp));
     tp.mp.part_floats = (long long)(pl->slots_bytes / 4);   // (checked builds' bound)
@@ -338,6 +348,7 @@ amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b
     tp.mc = mc;
     tp.pdl = pairs ? 0 : pl->pdl;
     tp.mma_only = pl->mma_only;
+    tp.wnarrow = wnarrow ? 1 : 0;
     if ((mode == 0 || mode == 4) && pl->hint_ws != workspace) {
       // hint words carry the launch generation (advanced on the device by the
       // kernel itself); zero words + counters + tail flags once per workspace
@@ -345,7 +356,8 @@ amun_status run_scores(amun_ol* pl, const void* X, const void* W, const float* b
       CUDA_TRY(cudaMemsetAsync(tp.hint, 0, pl->hint_bytes + 256 + pl->flags_bytes, st));
       pl->hint_ws = workspace;
     }
-#define TC_CALL(K) launch_tc<K>((int)pl->dtype, pl->ng_override, mx, mw, tp, grid, st, mode, pairs)
+#define TC_CALL(K) launch_tc<K>((int)pl->dtype, pl->ng_override, mx, mw, mwn, tp, grid, st, mode, \
+                                pairs)
     AMUN_KB_SWITCH(mode == 1 || mode == 4 ? 1 : pl->kb, TC_CALL)
 #undef TC_CALL
   } else {
@@ -567,6 +579,8 @@ amun_status amun_ol_create(amun_ol** plan, int H, int V_local, int v_offset, int
     if (mcv) pl->mc = atoi(mcv);
     const char* pd = getenv("AMUN_PDL");
     if (pd) pl->pdl = atoi(pd) != 0;
+    const char* wn = getenv("AMUN_WNARROW");
+    if (wn) pl->wnarrow = atoi(wn) != 0;
     const char* wb = getenv("AMUN_WBOX");
     if (wb) pl->wbox = atoi(wb) == 64 ? 64 : 256;
     const char* pp = getenv("AMUN_PREPASS");

@@ -19,7 +19,8 @@ amun_status launch_fail(const char* fmt, ...);
 
 template <int KB>
 amun_status launch_tc(int dtype, int ng_override, const CUtensorMap* mx, const CUtensorMap* mw,
-                      const TcParams& tp, int grid, cudaStream_t st, int mode, bool pairs);
+                      const CUtensorMap* mwn, const TcParams& tp, int grid, cudaStream_t st,
+                      int mode, bool pairs);
 
 }  // namespace amun
 
@@ -38,9 +39,9 @@ namespace amun {
 // Launch one fused-kernel instantiation; the warpgroup register hand-off
 // needs the full launch pool (see TcCfg), checked here.
 template <int NG>
-amun_status launch_kernel(void (*kern)(const CUtensorMap, const CUtensorMap, const TcParams),
-                          const CUtensorMap* mx, const CUtensorMap* mw, const TcParams& tp,
-                          int grid, cudaStream_t st, int smem_bytes) {
+amun_status launch_kernel(void (*kern)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const TcParams),
+                          const CUtensorMap* mx, const CUtensorMap* mw, const CUtensorMap* mwn,
+                          const TcParams& tp, int grid, cudaStream_t st, int smem_bytes) {
   cudaFuncAttributes fa;
   LT_TRY(cudaFuncGetAttributes(&fa, kern));
   if (fa.numRegs < TcCfg<NG>::kLaunchRegs)
@@ -49,7 +50,7 @@ amun_status launch_kernel(void (*kern)(const CUtensorMap, const CUtensorMap, con
   LT_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
   const bool coop = tp.tail && !(tp.tail & TAIL_X_NOCOOP);
   if (!coop && !tp.pdl && tp.mc <= 1) {
-    kern<<<grid, TcCfg<NG>::kThreads, smem_bytes, st>>>(*mx, *mw, tp);
+    kern<<<grid, TcCfg<NG>::kThreads, smem_bytes, st>>>(*mx, *mw, *mwn, tp);
     LT_TRY(cudaGetLastError());
     return AMUN_OK;
   }
@@ -82,16 +83,16 @@ amun_status launch_kernel(void (*kern)(const CUtensorMap, const CUtensorMap, con
   }
   cfg.attrs = attr;
   cfg.numAttrs = na;
-  LT_TRY(cudaLaunchKernelEx(&cfg, kern, *mx, *mw, tp));
+  LT_TRY(cudaLaunchKernelEx(&cfg, kern, *mx, *mw, *mwn, tp));
   return AMUN_OK;
 }
 
 template <int KB, int NG>
-amun_status launch_tc_ng(const CUtensorMap* mx, const CUtensorMap* mw, const TcParams& tp,
-                         int grid, cudaStream_t st, int mode, bool pairs) {
+amun_status launch_tc_ng(const CUtensorMap* mx, const CUtensorMap* mw, const CUtensorMap* mwn,
+                         const TcParams& tp, int grid, cudaStream_t st, int mode, bool pairs) {
   // modes 1 (debug logits) and 4 (argmax) exist for KB = 1 only (the caller
   // dispatches them there), so other buckets do not compile them again
-  void (*kern)(const CUtensorMap, const CUtensorMap, const TcParams);
+  void (*kern)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const TcParams);
   if (pairs) {
     kern = mode == 2 ? ol_tc2_kernel<KB, 2, NG> : mode == 3 ? ol_tc2_kernel<KB, 3, NG>
                                                             : ol_tc2_kernel<KB, 0, NG>;
@@ -107,50 +108,50 @@ amun_status launch_tc_ng(const CUtensorMap* mx, const CUtensorMap* mw, const TcP
       if (mode == 1) kern = ol_tc_kernel<1, 1, NG>;
     }
   }
-  return launch_kernel<NG>(kern, mx, mw, tp, grid, st, pairs ? TC2_SMEM : TC_SMEM);
+  return launch_kernel<NG>(kern, mx, mw, mwn, tp, grid, st, pairs ? TC2_SMEM : TC_SMEM);
 }
 
 // e4m3 plans: single CTAs; the full path and the two benchmark builds.
 template <int KB, int NG>
-amun_status launch_tc_f8(const CUtensorMap* mx, const CUtensorMap* mw, const TcParams& tp,
-                         int grid, cudaStream_t st, int mode) {
-  void (*kern)(const CUtensorMap, const CUtensorMap, const TcParams) =
+amun_status launch_tc_f8(const CUtensorMap* mx, const CUtensorMap* mw, const CUtensorMap* mwn,
+                         const TcParams& tp, int grid, cudaStream_t st, int mode) {
+  void (*kern)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const TcParams) =
       mode == 2 ? ol_tc_kernel<KB, 2, NG, 1> : mode == 3 ? ol_tc_kernel<KB, 3, NG, 1>
                                              : ol_tc_kernel<KB, 0, NG, 1>;
   if constexpr (KB == 1) {
     if (mode == 4) kern = ol_tc_kernel<1, 4, NG, 1>;
   }
-  return launch_kernel<NG>(kern, mx, mw, tp, grid, st, TC_SMEM_F8);
+  return launch_kernel<NG>(kern, mx, mw, mwn, tp, grid, st, TC_SMEM_F8);
 }
 
 // mxfp4 plans: single CTAs; every mode (the fused path, the test/bench
 // builds and the argmax kernel).
 template <int KB, int NG>
-amun_status launch_tc_f4(const CUtensorMap* mx, const CUtensorMap* mw, const TcParams& tp,
-                         int grid, cudaStream_t st, int mode) {
-  void (*kern)(const CUtensorMap, const CUtensorMap, const TcParams) =
+amun_status launch_tc_f4(const CUtensorMap* mx, const CUtensorMap* mw, const CUtensorMap* mwn,
+                         const TcParams& tp, int grid, cudaStream_t st, int mode) {
+  void (*kern)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const TcParams) =
       mode == 2 ? ol_tc_kernel<KB, 2, NG, 3> : mode == 3 ? ol_tc_kernel<KB, 3, NG, 3>
                                              : ol_tc_kernel<KB, 0, NG, 3>;
   if constexpr (KB == 1) {
     if (mode == 1) kern = ol_tc_kernel<1, 1, NG, 3>;
     if (mode == 4) kern = ol_tc_kernel<1, 4, NG, 3>;
   }
-  return launch_kernel<NG>(kern, mx, mw, tp, grid, st, TC_SMEM_F4);
+  return launch_kernel<NG>(kern, mx, mw, mwn, tp, grid, st, TC_SMEM_F4);
 }
 
 // tf32x3 plans: single CTAs; every mode (the fused path, the test/bench
 // builds and the argmax kernel).
 template <int KB, int NG>
-amun_status launch_tc_t3(const CUtensorMap* mx, const CUtensorMap* mw, const TcParams& tp,
-                         int grid, cudaStream_t st, int mode) {
-  void (*kern)(const CUtensorMap, const CUtensorMap, const TcParams) =
+amun_status launch_tc_t3(const CUtensorMap* mx, const CUtensorMap* mw, const CUtensorMap* mwn,
+                         const TcParams& tp, int grid, cudaStream_t st, int mode) {
+  void (*kern)(const CUtensorMap, const CUtensorMap, const CUtensorMap, const TcParams) =
       mode == 2 ? ol_tc_kernel<KB, 2, NG, 2> : mode == 3 ? ol_tc_kernel<KB, 3, NG, 2>
                                              : ol_tc_kernel<KB, 0, NG, 2>;
   if constexpr (KB == 1) {
     if (mode == 1) kern = ol_tc_kernel<1, 1, NG, 2>;
     if (mode == 4) kern = ol_tc_kernel<1, 4, NG, 2>;
   }
-  return launch_kernel<NG>(kern, mx, mw, tp, grid, st, TC_SMEM);
+  return launch_kernel<NG>(kern, mx, mw, mwn, tp, grid, st, TC_SMEM);
 }
 
 // Two epilogue warpgroups. bf16: measured faster than three or four (their
@@ -160,23 +161,24 @@ amun_status launch_tc_t3(const CUtensorMap* mx, const CUtensorMap* mw, const TcP
 // -DAMUN_WITH_NG4 adds the other counts (env AMUN_NG).
 template <int KB>
 amun_status launch_tc(int dtype, int ng_override, const CUtensorMap* mx, const CUtensorMap* mw,
-                      const TcParams& tp, int grid, cudaStream_t st, int mode, bool pairs) {
-  if (dtype == AMUN_TF32X3) return launch_tc_t3<KB, 2>(mx, mw, tp, grid, st, mode);
-  if (dtype == AMUN_MXFP4) return launch_tc_f4<KB, 2>(mx, mw, tp, grid, st, mode);
+                      const CUtensorMap* mwn, const TcParams& tp, int grid, cudaStream_t st,
+                      int mode, bool pairs) {
+  if (dtype == AMUN_TF32X3) return launch_tc_t3<KB, 2>(mx, mw, mwn, tp, grid, st, mode);
+  if (dtype == AMUN_MXFP4) return launch_tc_f4<KB, 2>(mx, mw, mwn, tp, grid, st, mode);
   if (dtype == AMUN_E4M3) {
 #ifdef AMUN_WITH_NG4
-    if (ng_override == 4) return launch_tc_f8<KB, 4>(mx, mw, tp, grid, st, mode);
+    if (ng_override == 4) return launch_tc_f8<KB, 4>(mx, mw, mwn, tp, grid, st, mode);
 #endif
-    return launch_tc_f8<KB, 2>(mx, mw, tp, grid, st, mode);
+    return launch_tc_f8<KB, 2>(mx, mw, mwn, tp, grid, st, mode);
   }
 #ifdef AMUN_WITH_NG4
-  if (ng_override == 4) return launch_tc_ng<KB, 4>(mx, mw, tp, grid, st, mode, pairs);
+  if (ng_override == 4) return launch_tc_ng<KB, 4>(mx, mw, mwn, tp, grid, st, mode, pairs);
 #endif
 #ifdef AMUN_WITH_NG3
-  if (ng_override == 3) return launch_tc_ng<KB, 3>(mx, mw, tp, grid, st, mode, pairs);
+  if (ng_override == 3) return launch_tc_ng<KB, 3>(mx, mw, mwn, tp, grid, st, mode, pairs);
 #endif
   (void)ng_override;
-  return launch_tc_ng<KB, 2>(mx, mw, tp, grid, st, mode, pairs);
+  return launch_tc_ng<KB, 2>(mx, mw, mwn, tp, grid, st, mode, pairs);
 }
 
 }  // namespace amun

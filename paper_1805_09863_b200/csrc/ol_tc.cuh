@@ -75,7 +75,7 @@ static_assert(TC_NBIAS >= 2 + TC_STAGES, "bias ring too small for the producer's
 template <int KB, int MODE, int NG, int ELT = 0>
 __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
     ol_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
-                 const TcParams p) {
+                 const __grid_constant__ CUtensorMap tmWn, const TcParams p) {
   using Cfg = TcCfg<NG>;
   constexpr int kBBytes = ELT == 3 ? TC_B_BYTES_F4 : TC_B_BYTES;
   extern __shared__ uint8_t smem_raw[];
@@ -130,6 +130,7 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
   if (role == 0 && lane == 0) {
     prefetch_tmap(&tmX);
     prefetch_tmap(&tmW);
+    if (p.wnarrow) prefetch_tmap(&tmWn);
     for (int i = 0; i < TC_STAGES; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], p.mc > 1 ? p.mc : 1);   // W multicast: every cluster CTA's MMAs
@@ -223,8 +224,12 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
             // W in boxes of p.wbox rows (256, or 64 so narrow tapered tiles
             // do not drag 256 rows through L2 -> SMEM); the boxes land
             // contiguously, i.e. the same SW128 K-major tile
-            const int wbox = p.wbox;
+            // a narrow tile (a range's remainder, <= 192 columns) loads only
+            // the 64-row boxes it needs (tmWn), not a full 256-row box
+            const bool narrow = p.wnarrow && width <= 192;
+            const int wbox = narrow ? 64 : p.wbox;
             const int nbox = (width + wbox - 1) / wbox;
+            const CUtensorMap* tw = narrow ? &tmWn : &tmW;
             // (mxfp4 W: the transaction counts the packed global bytes, half
             // the unpacked shared-memory box)
             constexpr int kWDiv = ELT == 3 ? 2 : 1;
@@ -253,7 +258,7 @@ __global__ void __launch_bounds__(TcCfg<NG>::kThreads, 1)
             }
             for (int j = 0; load_w && p.mc <= 1 && j < nbox; ++j) {
               // (the L2 hint measured the same as evict_first / evict_normal / none)
-              tma_load_2d(&tmW, &full[stage], sB + stage * kBBytes + j * wbox * TC_KBYTES,
+              tma_load_2d(tw, &full[stage], sB + stage * kBBytes + j * wbox * TC_KBYTES,
                           kb * kBlockElems, v0 + j * wbox, 0ull);
             }
           }

@@ -33,6 +33,7 @@ static_assert(TC_NBIAS >= 2 + TC2_STAGES, "bias ring too small for the producer'
 template <int KB, int MODE, int NG>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TcCfg<NG>::kThreads, 1)
     ol_tc2_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
+                  const __grid_constant__ CUtensorMap /*tmWn: single-CTA kernel only*/,
                   const TcParams p) {
   using Cfg = TcCfg<NG>;
   extern __shared__ uint8_t smem_raw[];

@@ -49,6 +49,7 @@ struct TcParams {
   int pdl;                                 // launched with programmatic stream serialization
   int mma_only;                            // (experiment, MODE 2) MMAs re-read the first stages
   int mc;                                  // > 1: clusters of mc M-tile CTAs share W (multicast)
+  int wnarrow;                             // single-CTA kernel: narrow tiles load 64-row W boxes
 };
 
 // Timeline probe points (globaltimer ns; per CTA; see amun_debug_timeline).

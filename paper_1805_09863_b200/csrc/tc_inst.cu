@@ -9,4 +9,5 @@
 #endif
 
 template amun_status amun::launch_tc<AMUN_KB>(int, int, const CUtensorMap*, const CUtensorMap*,
-                                              const amun::TcParams&, int, cudaStream_t, int, bool);
+                                              const CUtensorMap*, const amun::TcParams&, int,
+                                              cudaStream_t, int, bool);

@@ -42,6 +42,8 @@ for _p in (0, 1):
     VARIANTS[f"scores_pdl{_p}"] = {"AMUN_TAIL": "off", "AMUN_PDL": str(_p)}
 for _m in (0, 2, 4, 5, 6):   # W multicast clusters of the M-tiles of a split (experiment)
     VARIANTS[f"tail_mc{_m}"] = {"AMUN_TAIL": "on", "AMUN_MC": str(_m)}
+for _n in (0, 1):   # narrow remainder tiles load 64-row W boxes
+    VARIANTS[f"tail_wn{_n}"] = {"AMUN_TAIL": "on", "AMUN_WNARROW": str(_n)}
 for _g in (2, 4):   # epilogue warpgroups (4 needs a -DAMUN_WITH_NG4 build, AMUN_LIB)
     VARIANTS[f"tail_ng{_g}"] = {"AMUN_TAIL": "on", "AMUN_NG": str(_g)}
 for _b in (64, 256):
@@ -52,6 +54,7 @@ for _v in VARIANTS.values():
     _v.setdefault("AMUN_PREPASS", "1")
     _v.setdefault("AMUN_MC", "0")
     _v.setdefault("AMUN_NG", "2")
+    _v.setdefault("AMUN_WNARROW", "1")
 NOCHECK = {v for v in VARIANTS if v.startswith("scores")} | {"tailwait", "waitnocoop", "arriveonly"}
 
 
