@@ -1,19 +1,25 @@
 // ol_tc.cuh — fused output layer on the 5th-gen tensor cores (sm_100a),
 // single-CTA version (tcgen05.mma.cta_group::1).
 //
-// Steps 1-4 of PAPER.md P:81-87 in one persistent, warp-specialised kernel:
-//   warp 0  TMA producer: X tile [128 rows x 64 K] and W tile [256 vocab x 64 K]
-//           per stage (128B swizzle), STAGES-deep mbarrier ring; with each
-//           tile also a 1-D bulk copy of its bias slice into the bias ring.
-//   warp 1  TMEM allocator + single-thread tcgen05.mma issuer:
-//           D[128 x width] (fp32, TMEM) += X_tile * W_tile^T, K = 16 per MMA.
-//           Two TMEM accumulators (2 x 256 columns = all 512) so the epilogue
-//           of tile t overlaps the MMAs of tile t+1.
-//   warps 2-3  idle (the control warpgroup gives its registers away)
-//   warps 4..  epilogue, NG warpgroups (tc_epi.cuh): + bias (step 2), online
-//           softmax statistics (step 3), register k-best (step 4); the N x V
-//           logits never reach HBM; one partial record {m, s, top-k} per
-//           (row, CTA range) (Alg. 6's per-shard state).
+// Steps 1-4 of PAPER.md P:81-87 in one persistent, warp-specialised kernel
+// (epilogue warpgroups on the low warp ids, the control warpgroup on the
+// highest four):
+//   warps 0 .. 4NG-1  epilogue, NG warpgroups (tc_epi.cuh): + bias (step 2),
+//           online softmax statistics (step 3), register k-best (step 4);
+//           the N x V logits never reach HBM; one partial record
+//           {m, s, top-k} per (row, CTA range) (Alg. 6's per-shard state,
+//           P:232-242); then the merge in the launch's tail (tail.cuh).
+//   warp 4NG    TMA producer: X tile [128 rows x 128 bytes of K] and W tile
+//           [256 vocab rows x 128 bytes of K] per stage (128B swizzle),
+//           STAGES-deep mbarrier ring; with each tile a 1-D bulk copy of its
+//           bias slice into the bias ring. A range's narrow remainder tile
+//           reads W in 64-row boxes (tmWn).
+//   warp 4NG+1  TMEM allocator + single-thread tcgen05.mma issuer:
+//           D[128 x width] (fp32, TMEM) += X_tile * W_tile^T, 32 bytes of K
+//           per MMA. Two TMEM accumulators (2 x 256 columns = all 512) so the
+//           epilogue of tile t overlaps the MMAs of tile t+1.
+//   warp 4NG+2  mxfp4 plans: re-bases each stage's W scale atoms; else idle
+//   warp 4NG+3  idle (the control warpgroup gives its registers away)
 // MODE 1 (test hook) writes the biased logits instead of statistics.
 // MODE 2 / 3 (benchmark hooks, the analogue of the paper's Table 4 split):
 // 2 = bare GEMM (the epilogue only drains TMEM), 3 = GEMM + bias + online
